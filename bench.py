@@ -1,0 +1,448 @@
+#!/usr/bin/env python
+"""bench.py -- megapixels/s of the ImageCL hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl icl|reference]
+                    [--workload suite|sepconv16k] [--batch B] [--size S] [--radius R]
+
+Default workload ("suite", BASELINE.json configs[4] per GPU): every rank
+processes its own batch of B (default 8) synthetic 4096x4096 fp32 images
+through the whole hot path each step -- separable Gaussian convolution
+(r=2, constant 0), Harris (3x3 Sobel, 5x5 window, k=0.04, clamp, + mask) and
+NLM (5x5 patch, 11x11 search, h=0.1, clamp).  Weak scaling: at N=8 the job is
+the 64-image configs[4].  Inputs (3 x 512 MiB per rank) are larger than L2,
+so no flush is needed between steps.
+
+``value`` = whole-job suite throughput (pixels that went through all three
+filters per second, summed over ranks, Mpx/s).  ``e2e`` = the same through the
+public API with pinned HOST buffers (H2D of the step's inputs and D2H of all
+outputs inside the timed region).  ``roofline`` is for the dominant kernel
+(NLM, FP32-bound); ``rooflines`` lists all three.  ``cpu_baseline`` times the
+double-precision oracle (oracle/) on a bounded pixel sample on this host.
+
+``--impl reference``: the reference arm is the CPU oracle (no runnable
+reference implementation exists -- the reference is a paper), timed on the
+host cores on a bounded sample per step; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # DESIGN.md "FP32 roof" (74.4 TFLOP/s)
+NLM_FLOP_PER_PAIR = {"direct": 79, "boxsum": 14}     # SURVEY.md §8(d), DESIGN.md "NLM flops"
+SEP_BYTES_PER_PX = 8
+HARRIS_BYTES_PER_PX = 9                               # in + R (4+4) + uint8 mask
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() in ("active", "1", "0x1"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- distributed
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def init_dist(ws, backend):
+    import torch.distributed as dist
+    if ws > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend)
+    return dist
+
+
+def max_over_ranks(x: float, ws: int, device) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- workload
+SUITE = dict(sep_r=2, sep_border="constant", har_block=5, har_k=0.04, har_border="clamp", nlm_P=2, nlm_S=5,
+             nlm_h=0.1, nlm_border="clamp")
+
+
+def gen_inputs(rank, batch, size):
+    """Per-rank host inputs (numpy, fp32): uniform (sepconv), rect scenes (Harris, NLM)."""
+    u = np.empty((batch, size, size), np.float32)
+    hs = np.empty_like(u)
+    ns = np.empty_like(u)
+    for i in range(batch):
+        seed = rank * batch + i
+        u[i] = synth.uniform_image(1000 + seed, size, size)
+        hs[i] = synth.rect_scene(2000 + seed, size, size, n_rect=256, noise=0.01)
+        ns[i] = synth.rect_scene(3000 + seed, size, size, n_rect=256, noise=0.0866)
+    return u, hs, ns
+
+
+def cpu_oracle_sample(inputs, size, target_s=8.0, threads=0):
+    """Time the oracle on a bounded random pixel sample of the suite workload."""
+    import oracle
+    u, hs, ns = inputs
+    rng = np.random.default_rng(0)
+    fx = synth.gaussian_taps(SUITE["sep_r"])
+    c = SUITE
+
+    def run(n):
+        ys, xs = rng.integers(0, size, n), rng.integers(0, size, n)
+        t = {}
+        t0 = time.perf_counter()
+        oracle.sepconv(u[0], fx, fx, c["sep_border"], points=(xs, ys), threads=threads)
+        t["sepconv"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        oracle.harris(hs[0], c["har_block"], c["har_k"], c["har_border"], points=(xs, ys), threads=threads)
+        t["harris"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        oracle.nlm(ns[0], c["nlm_P"], c["nlm_S"], c["nlm_h"], c["nlm_border"], points=(xs, ys), threads=threads)
+        t["nlm"] = time.perf_counter() - t0
+        return t
+
+    n = 2048
+    t = run(n)
+    tot = sum(t.values())
+    n = int(min(1 << 22, max(2048, n * target_s / max(tot, 1e-3))))
+    t = run(n)
+    tot = sum(t.values())
+    return n, t, tot
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    size = args.size
+    threads = oracle.default_threads()
+    inputs = tuple(a[:1] for a in gen_inputs(0, 1, size))
+    fx = synth.gaussian_taps(SUITE["sep_r"])
+    c = SUITE
+    rng = np.random.default_rng(1)
+    u, hs, ns = inputs
+
+    def step(n):
+        ys, xs = rng.integers(0, size, n), rng.integers(0, size, n)
+        oracle.sepconv(u[0], fx, fx, c["sep_border"], points=(xs, ys), threads=threads)
+        oracle.harris(hs[0], c["har_block"], c["har_k"], c["har_border"], points=(xs, ys), threads=threads)
+        oracle.nlm(ns[0], c["nlm_P"], c["nlm_S"], c["nlm_h"], c["nlm_border"], points=(xs, ys), threads=threads)
+
+    t0 = time.perf_counter()
+    step(1024)
+    dt = time.perf_counter() - t0
+    budget = 150.0 / max(1, args.steps + args.warmup)  # whole run within a few minutes
+    n = int(min(1 << 20, max(256, 1024 * min(budget, 4.0) / max(dt, 1e-4))))
+    for _ in range(args.warmup):
+        step(n)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(n)
+    el = time.perf_counter() - t0
+    value = args.steps * n / el / 1e6
+    sample = f"{n} random pixels per step of one {size}x{size} image, each through sepconv+Harris+NLM (oracle, f64)"
+    line = {
+        "impl": "reference", "metric": "suite megapixels/s (sepconv r2 + Harris B5 + NLM 5x5/11x11)",
+        "value": value, "unit": "Mpx/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "suite", "images_per_gpu": args.batch, "size": [size, size], **SUITE},
+        "cpu_baseline": {"value": value, "unit": "Mpx/s", "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "Mpx/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- icl arm: suite
+def run_suite(args):
+    import torch
+
+    import paper_1605_06399_b200 as icl
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = init_dist(ws, "nccl")
+    icl.load_library()
+    B, S = args.batch, args.size
+    t_gen = time.perf_counter()
+    u_h, hs_h, ns_h = gen_inputs(rank, B, S)
+    t_gen = time.perf_counter() - t_gen
+    u = torch.from_numpy(u_h).to(dev)
+    hs = torch.from_numpy(hs_h).to(dev)
+    ns = torch.from_numpy(ns_h).to(dev)
+    o_sep = torch.empty_like(u)
+    o_har = torch.empty_like(u)
+    o_mask = torch.empty(B, S, S, dtype=torch.uint8, device=dev)
+    o_nlm = torch.empty_like(u)
+    fx = synth.gaussian_taps(SUITE["sep_r"])
+    c = SUITE
+    stream = torch.cuda.Stream(device=dev)
+    thr = 1.0  # absolute threshold on R (R10)
+
+    # auto-tune once per shape (untimed), §4: the winner is cached.
+    tuned = {}
+    with torch.cuda.stream(stream):
+        if not args.no_tune:
+            tuned["sepconv"] = icl.tune("sepconv", u, o_sep, taps_x=fx, taps_y=fx, border=c["sep_border"],
+                                        stream=stream)
+            tuned["harris"] = icl.tune("harris", hs, o_har, block=c["har_block"], k=c["har_k"],
+                                       border=c["har_border"], mask=o_mask, threshold=thr, stream=stream)
+            tuned["nlm"] = icl.tune("nlm", ns, o_nlm, patch_radius=c["nlm_P"], search_radius=c["nlm_S"],
+                                    h=c["nlm_h"], border=c["nlm_border"], stream=stream)
+    stream.synchronize()
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        icl.sepconv(u, o_sep, fx, fx, c["sep_border"], stream=stream)
+        if ev:
+            ev[1].record(stream)
+        icl.harris(hs, o_har, c["har_block"], c["har_k"], c["har_border"], mask=o_mask, threshold=thr,
+                   stream=stream)
+        if ev:
+            ev[2].record(stream)
+        icl.nlm(ns, o_nlm, c["nlm_P"], c["nlm_S"], c["nlm_h"], c["nlm_border"], stream=stream)
+        if ev:
+            ev[3].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    stream.synchronize()
+    variants = {f: icl.variant_names(f)[icl.last_variant(f)] for f in ("sepconv", "harris", "nlm")}
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    n0 = icl.launch_count()
+    with ClockSampler(local) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for k in range(args.steps):
+            step(evs[k])
+        end.record(stream)
+        stream.synchronize()
+    launches = icl.launch_count() - n0
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    total_ms = start.elapsed_time(end)
+    per = {"sepconv": [], "harris": [], "nlm": []}
+    for e in evs:
+        per["sepconv"].append(e[0].elapsed_time(e[1]))
+        per["harris"].append(e[1].elapsed_time(e[2]))
+        per["nlm"].append(e[2].elapsed_time(e[3]))
+    step_ms = max_over_ranks(total_ms / args.steps, ws, dev)
+    px_rank = B * S * S
+    value = ws * px_rank / (step_ms * 1e-3) / 1e6
+
+    # ---------------- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hu = torch.from_numpy(u_h).pin_memory()
+        hh = torch.from_numpy(hs_h).pin_memory()
+        hn = torch.from_numpy(ns_h).pin_memory()
+        outs_h = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in (o_sep, o_har, o_mask, o_nlm)]
+
+        def e2e_step():
+            u.copy_(hu, non_blocking=True)
+            hs.copy_(hh, non_blocking=True)
+            ns.copy_(hn, non_blocking=True)
+            step()
+            for hb, db in zip(outs_h, (o_sep, o_har, o_mask, o_nlm)):
+                hb.copy_(db, non_blocking=True)
+
+        ksteps = max(1, min(args.steps, 5))
+        with torch.cuda.stream(stream):
+            e2e_step()
+            stream.synchronize()
+            if ws > 1:
+                dist.barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            bq = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(ksteps):
+                e2e_step()
+            bq.record(stream)
+            stream.synchronize()
+        e2e_ms = max_over_ranks(a.elapsed_time(bq) / ksteps, ws, dev)
+        h2d = 3 * B * S * S * 4
+        d2h = B * S * S * (4 + 4 + 1 + 4)
+        e2e = {"value": ws * px_rank / (e2e_ms * 1e-3) / 1e6, "unit": "Mpx/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": ksteps}
+
+    # ---------------- rooflines (algorithmic work / per-launch device time)
+    hbm, hbm_kind = measured_peaks()
+    traffic = ncu_traffic()
+    med = {f: statistics.median(v) for f, v in per.items()}
+    nlm_kind = "boxsum" if variants["nlm"].startswith("boxsum") else "direct"
+    P, Sr = c["nlm_P"], c["nlm_S"]
+    pairs = (2 * Sr + 1) ** 2
+    nlm_flop_px = pairs * (NLM_FLOP_PER_PAIR[nlm_kind] if nlm_kind == "boxsum" else
+                           (2 * P + 1) ** 2 * 3 + 4)
+    roof = {
+        "nlm": {"bound": "alu", "achieved": nlm_flop_px * px_rank / (med["nlm"] * 1e-3) / 1e12,
+                "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "flop_per_px": nlm_flop_px,
+                "formulation": nlm_kind, "kernel": variants["nlm"],
+                "traffic": traffic.get("nlm")},
+        "sepconv": {"bound": "hbm", "achieved": SEP_BYTES_PER_PX * px_rank / (med["sepconv"] * 1e-3) / 1e9,
+                    "peak": hbm, "unit": "GB/s", "kernel": variants["sepconv"],
+                    "traffic": traffic.get("sepconv")},
+        "harris": {"bound": "hbm", "achieved": HARRIS_BYTES_PER_PX * px_rank / (med["harris"] * 1e-3) / 1e9,
+                   "peak": hbm, "unit": "GB/s", "kernel": variants["harris"],
+                   "traffic": traffic.get("harris")},
+    }
+    for r in roof.values():
+        r["frac"] = r["achieved"] / r["peak"]
+    roof["sepconv"]["frac_of_8TBs_spec"] = roof["sepconv"]["achieved"] / 8000.0
+    roof["harris"]["frac_of_8TBs_spec"] = roof["harris"]["achieved"] / 8000.0
+    roof["sepconv"]["peak_kind"] = roof["harris"]["peak_kind"] = hbm_kind
+    roof["nlm"]["peak_kind"] = "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz"
+    dominant = max(med, key=med.get)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        import oracle
+        n, t, tot = cpu_oracle_sample((u_h[:1], hs_h[:1], ns_h[:1]), S)
+        cpu = {"value": n / tot / 1e6, "unit": "Mpx/s", "cores": oracle.default_threads(), "kind": "oracle",
+               "sample": f"{n} random pixels of one {S}x{S} image through sepconv+Harris+NLM (f64 oracle); "
+                         f"per-filter s: " + ", ".join(f"{k}={v:.2f}" for k, v in t.items())}
+
+    if rank == 0:
+        line = {
+            "metric": "suite megapixels/s (sepconv r2 + Harris B5 + NLM 5x5/11x11)",
+            "value": value, "unit": "Mpx/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "suite (BASELINE.json configs[4] per GPU)", "images_per_gpu": B,
+                       "size": [S, S], "global_batch": B * ws, **SUITE, "harris_threshold": thr,
+                       "l2": "inputs (3 x %d MiB per rank) exceed the 126 MB L2; no flush" % (B * S * S * 4 >> 20),
+                       "variants": variants, "tuned": {k: v["name"] for k, v in tuned.items()},
+                       "input_gen_s": round(t_gen, 1)},
+            "per_filter_mpx_s": {f: px_rank / (m * 1e-3) / 1e6 for f, m in med.items()},
+            "per_filter_ms": med,
+            "roofline": {k: roof[dominant][k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
+            "roofline_kernel": dominant,
+            "rooflines": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="icl", choices=["icl", "reference"])
+    ap.add_argument("--workload", default="suite", choices=["suite"])
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--size", type=int, default=4096)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tune", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_suite(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

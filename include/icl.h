@@ -1,0 +1,223 @@
+/*
+ * icl.h -- C ABI of the B200-native ImageCL hot-path library (libicl.so).
+ *
+ * The library computes the per-pixel image filters of the three benchmarks
+ * that ImageCL's compiler + auto-tuner exist to speed up (§6,
+ * lines 546-603; NLM replaces non-separable convolution per BASELINE.json
+ * north_star), over the tuned variant space of PAPER.md Table 1 (lines
+ * 364-393, §5.2.1-5.2.5), re-designed for sm_100a.
+ *
+ * Conventions (all entry points):
+ *  - extern "C", no C++ exceptions cross the ABI, no torch/CUDA types in the
+ *    signatures: streams are passed as `void*` holding a cudaStream_t
+ *    (NULL = legacy default stream).
+ *  - Image pixel pointers are DEVICE pointers owned by the caller; the
+ *    library never frees or retains them beyond the call.  Filter
+ *    parameters (taps) are HOST pointers read during the call and copied by
+ *    value into the kernel parameter block (the "constant memory" parameter
+ *    of PAPER.md:477-482).
+ *  - Filter calls only ENQUEUE work on `stream` and return; they never
+ *    synchronise the host.  Asynchronous CUDA faults surface at the caller's
+ *    next synchronisation.  icl_tune() synchronises.
+ *  - On any non-OK status nothing has been enqueued, and icl_last_error()
+ *    returns a thread-local human-readable message.
+ *  - Image layout: fp32 (masks: uint8), row-major; pixel (x, y) of image b
+ *    is at  data + b*batch_stride_bytes + y*pitch_bytes + x*elem_size
+ *    (x = column = contiguous axis = ImageCL idx; y = row = idy;
+ *    PAPER.md:289-296).
+ *  - Boundary conditions: reads outside the image return the nearest edge
+ *    pixel (CLAMP) or `border_value` (CONSTANT) -- PAPER.md:303-308 and
+ *    Fig. 3 (lines 311-327).  Boundaries are applied in GLOBAL image
+ *    coordinates, also for row bands (icl_band).
+ *  - Aliasing between a source and any destination is rejected
+ *    (ICL_ERR_ALIASING): "In ImageCL, we disallow aliasing".
+ */
+#ifndef ICL_H_
+#define ICL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ICL_ABI_VERSION 1
+
+typedef enum {
+    ICL_OK = 0,
+    ICL_ERR_INVALID_ARG = 1, /* null pointer, bad size/pitch/parameter */
+    ICL_ERR_ALIASING = 2,    /* source and destination byte ranges overlap */
+    ICL_ERR_UNSUPPORTED = 3, /* parameter outside the compiled variant space */
+    ICL_ERR_WORKSPACE = 4,   /* forced variant needs more workspace than given */
+    ICL_ERR_CUDA = 5,        /* CUDA launch/runtime error */
+    ICL_ERR_NCCL = 6,        /* NCCL error (sharded calls) */
+    ICL_ERR_NOT_TUNED = 7    /* ICL_TUNE_POLICY=require and no cache entry */
+} icl_status;
+
+typedef enum { ICL_BORDER_CONSTANT = 0, ICL_BORDER_CLAMP = 1 } icl_border;
+
+typedef enum { ICL_FILTER_SEPCONV = 0, ICL_FILTER_HARRIS = 1, ICL_FILTER_NLM = 2 } icl_filter;
+
+/* A (batch of) 2-D image(s).  `data` is a device pointer (fp32 pixels for
+ * images, uint8 for masks).  width, height >= 1 and < 2^31; pitch_bytes >=
+ * width*elem_size and a multiple of elem_size; batch >= 1; when batch > 1,
+ * batch_stride_bytes >= height*pitch_bytes (images must not overlap). */
+typedef struct {
+    void* data;
+    int64_t width;
+    int64_t height;
+    int64_t pitch_bytes;
+    int64_t batch;
+    int64_t batch_stride_bytes;
+} icl_image;
+
+/* Row band of a taller GLOBAL image (row-band sharding).
+ * src row 0 is global row src_y0; dst row 0 is global row dst_y0; the call
+ * computes every dst row.  Every global row in [0, global_height) that a dst
+ * row's stencil touches must be present in src.  NULL band == the whole
+ * image: {global_height = src.height, src_y0 = 0, dst_y0 = 0} and
+ * dst.height == src.height. */
+typedef struct {
+    int64_t global_height;
+    int64_t src_y0;
+    int64_t dst_y0;
+} icl_band;
+
+/* ------------------------------------------------------------------------
+ * Separable convolution (§6; Table 2 R and C kernels,
+ * lines 611-629).  Correlation form (Listing 1):
+ *     out(x,y) = sum_{j=-ry..ry} taps_y[j+ry] * sum_{i=-rx..rx} taps_x[i+rx] * src_B(x+i, y+j)
+ * Every variant evaluates, per output, the same fp32 FMA chain (inner over
+ * i = -rx..rx, intermediate rounded to fp32, outer over j), so all variants
+ * and all band splits are bit-identical (R16).
+ * rx, ry in [0, 15]  (> 15 -> ICL_ERR_UNSUPPORTED); taps are HOST arrays of
+ * 2r+1 floats.  src/dst: fp32, same width; dst.height = band rows.
+ * workspace: optional device scratch for two-pass variants (size from
+ * icl_sepconv_workspace_bytes); may be NULL, in which case only single-pass
+ * variants are eligible.
+ * ---------------------------------------------------------------------- */
+icl_status icl_sepconv(const icl_image* src, const icl_image* dst, const float* taps_x, int rx,
+                       const float* taps_y, int ry, icl_border border, float border_value,
+                       const icl_band* band, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Workspace (bytes) that lets every sepconv variant run for these sizes. */
+size_t icl_sepconv_workspace_bytes(int64_t width, int64_t height, int64_t batch, int ry);
+
+/* ------------------------------------------------------------------------
+ * Harris corner response (§6; Table 4 Sobel kernel,
+ * Table 5 Harris kernel, lines 651-687), per-stage semantics (DESIGN.md
+ * R6-R10):  dx = Kx * src_B, dy = Ky * src_B with the unnormalised 3x3
+ * Sobel Kx = [1,2,1]^T[-1,0,1], Ky = Kx^T; dx/dy outside the image are
+ * dx(clamp(q)) (CLAMP) or 0 (CONSTANT); window sums over
+ * [-floor(B/2), B-1-floor(B/2)]^2;
+ *     R = Sxx*Syy - Sxy^2 - k*(Sxx+Syy)^2.
+ * block (window side B) in [1, 7]; k finite.
+ * mask: optional uint8 device image (same width/height/batch as response,
+ * own pitch); mask = (R > threshold) ? 1 : 0, decided in fp32.
+ * ---------------------------------------------------------------------- */
+icl_status icl_harris(const icl_image* src, const icl_image* response, int block, float k,
+                      icl_border border, float border_value, const icl_image* mask, float threshold,
+                      const icl_band* band, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Non-local-means denoising (not in PAPER.md -- BASELINE.json north_star;
+ * definition DESIGN.md R11-R14):
+ *   d2(p,q) = (1/(2P+1)^2) sum_{t in [-P,P]^2} (src_B(p+t) - src_B(q+t))^2,
+ *   w = exp(-d2/h^2), out(p) = sum_{q in p+[-S,S]^2} w src_B(q) / sum w.
+ * patch_radius P in [0,3], search_radius S in [0,10]; h > 0 or +INF
+ * (box mean); h <= 0 or NaN -> ICL_ERR_INVALID_ARG.
+ * ---------------------------------------------------------------------- */
+icl_status icl_nlm(const icl_image* src, const icl_image* dst, int patch_radius, int search_radius,
+                   float h, icl_border border, float border_value, const icl_band* band,
+                   void* stream);
+
+/* ------------------------------------------------------------------------
+ * Variant space + auto-tuner (§4, Table 1 lines
+ * 364-393).
+ * ---------------------------------------------------------------------- */
+
+/* Tagged union of the three calls' arguments. */
+typedef struct {
+    icl_filter filter;
+    icl_image src;
+    icl_image dst; /* sepconv out / harris response / nlm out */
+    icl_border border;
+    float border_value;
+    /* sepconv */
+    const float* taps_x;
+    int rx;
+    const float* taps_y;
+    int ry;
+    void* workspace;
+    size_t workspace_bytes;
+    /* harris */
+    int block;
+    float k;
+    icl_image mask; /* mask.data == NULL -> no mask */
+    float threshold;
+    /* nlm */
+    int patch_radius;
+    int search_radius;
+    float h;
+} icl_problem;
+
+typedef struct {
+    int variant_id;
+    char name[96];
+    float median_us;  /* median of the timed launches of the winner */
+    int n_candidates; /* eligible variants timed */
+    int n_rejected;   /* variants whose output differed from the naive one */
+    int from_cache;   /* 1 if the answer came from the cache */
+} icl_variant_info;
+
+#define ICL_TUNE_FORCE 1u     /* re-time even if the key is cached */
+#define ICL_TUNE_NO_VERIFY 2u /* skip the equivalence check against the naive variant */
+
+/* Time every eligible variant for this problem (CUDA events, median of >= 10
+ * launches after warm-up), reject any whose output differs from the naive
+ * variant (bit-exact for sepconv, tolerance for Harris/NLM), cache the
+ * fastest per problem key (ties within 0.5% -> lower id).  Synchronises.
+ * Leaves the winner's result in dst. */
+icl_status icl_tune(const icl_problem* problem, unsigned flags, void* stream, icl_variant_info* chosen);
+
+/* Persist / restore the winner cache (JSON; keyed by device name, SM count
+ * and library version + problem key -- the "final implementation" of
+ * PAPER.md:233-234). */
+icl_status icl_tune_cache_save(const char* path);
+icl_status icl_tune_cache_load(const char* path);
+void icl_tune_cache_clear(void);
+int icl_tune_cache_size(void);
+
+/* Variant registry.  Ids are stable within a library build. */
+int icl_variant_count(icl_filter filter);
+icl_status icl_variant_name(icl_filter filter, int variant_id, char* buf, size_t buf_len);
+
+/* Force a variant for subsequent calls on the CALLING thread (the "force
+ * on/off" directive analog); -1 restores automatic
+ * dispatch.  A forced variant that is ineligible for a call makes that call
+ * fail with ICL_ERR_UNSUPPORTED (or ICL_ERR_WORKSPACE). */
+icl_status icl_force_variant(icl_filter filter, int variant_id);
+
+/* Variant the last successful call of `filter` on this thread dispatched to. */
+int icl_last_variant(icl_filter filter);
+
+/* Number of kernel launches this library issued on the calling process since
+ * load (for the bench's gpu_launches claim). */
+uint64_t icl_launch_count(void);
+
+/* ------------------------------------------------------------------------
+ * Misc
+ * ---------------------------------------------------------------------- */
+const char* icl_last_error(void);
+const char* icl_version(void);
+/* Fill a device fp32 image with the synthetic U[0,1) SplitMix64 stream of
+ * synth.uniform_image(seed, ...) (input generation for large benches; holds
+ * no filter arithmetic).  Pixel (x, y) of image b uses counter
+ * (row0 + y)*width + x and seed (seed + b). */
+icl_status icl_fill_uniform(const icl_image* img, uint64_t seed, int64_t row0, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ICL_H_ */

@@ -1,0 +1,292 @@
+"""paper_1605_06399_b200 -- Python binding of libicl.so (include/icl.h).
+
+Argument marshalling only: every step of every filter runs in the CUDA
+kernels of libicl.so.  There is no CPU fallback: if the library is missing or
+no CUDA device is present, calls raise.  PyTorch is used only for device
+memory and streams.
+
+Images are torch tensors of shape (H, W) or (batch, H, W), dtype float32
+(masks: uint8), on a CUDA device, with unit stride along W (rows may be
+padded: pitch = stride(-2) * element size).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libicl.so")
+
+ICL_OK = 0
+STATUS = {0: "ICL_OK", 1: "ICL_ERR_INVALID_ARG", 2: "ICL_ERR_ALIASING", 3: "ICL_ERR_UNSUPPORTED",
+          4: "ICL_ERR_WORKSPACE", 5: "ICL_ERR_CUDA", 6: "ICL_ERR_NCCL", 7: "ICL_ERR_NOT_TUNED"}
+BORDER = {"constant": 0, "clamp": 1}
+FILTER = {"sepconv": 0, "harris": 1, "nlm": 2}
+
+# Symbols include/icl.h declares (checked by tests/test_abi.py).
+EXPORTS = ("icl_sepconv", "icl_sepconv_workspace_bytes", "icl_harris", "icl_nlm", "icl_tune",
+           "icl_tune_cache_save", "icl_tune_cache_load", "icl_tune_cache_clear", "icl_tune_cache_size",
+           "icl_variant_count", "icl_variant_name", "icl_force_variant", "icl_last_variant",
+           "icl_launch_count", "icl_last_error", "icl_version", "icl_fill_uniform")
+
+
+class IclError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class icl_image(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("width", ctypes.c_int64), ("height", ctypes.c_int64),
+                ("pitch_bytes", ctypes.c_int64), ("batch", ctypes.c_int64),
+                ("batch_stride_bytes", ctypes.c_int64)]
+
+
+class icl_band(ctypes.Structure):
+    _fields_ = [("global_height", ctypes.c_int64), ("src_y0", ctypes.c_int64), ("dst_y0", ctypes.c_int64)]
+
+
+class icl_problem(ctypes.Structure):
+    _fields_ = [("filter", ctypes.c_int), ("src", icl_image), ("dst", icl_image), ("border", ctypes.c_int),
+                ("border_value", ctypes.c_float), ("taps_x", ctypes.c_void_p), ("rx", ctypes.c_int),
+                ("taps_y", ctypes.c_void_p), ("ry", ctypes.c_int), ("workspace", ctypes.c_void_p),
+                ("workspace_bytes", ctypes.c_size_t), ("block", ctypes.c_int), ("k", ctypes.c_float),
+                ("mask", icl_image), ("threshold", ctypes.c_float), ("patch_radius", ctypes.c_int),
+                ("search_radius", ctypes.c_int), ("h", ctypes.c_float)]
+
+
+class icl_variant_info(ctypes.Structure):
+    _fields_ = [("variant_id", ctypes.c_int), ("name", ctypes.c_char * 96), ("median_us", ctypes.c_float),
+                ("n_candidates", ctypes.c_int), ("n_rejected", ctypes.c_int), ("from_cache", ctypes.c_int)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libicl.so (raises if it was not built -- there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libicl.so not built at {path}: run `python -m paper_1605_06399_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    P, I, I64, F, U = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float, ctypes.c_uint
+    img, band = ctypes.POINTER(icl_image), ctypes.POINTER(icl_band)
+    sig = {
+        "icl_sepconv": ([img, img, P, I, P, I, I, F, band, P, ctypes.c_size_t, P], I),
+        "icl_sepconv_workspace_bytes": ([I64, I64, I64, I], ctypes.c_size_t),
+        "icl_harris": ([img, img, I, F, I, F, img, F, band, P], I),
+        "icl_nlm": ([img, img, I, I, F, I, F, band, P], I),
+        "icl_tune": ([ctypes.POINTER(icl_problem), U, P, ctypes.POINTER(icl_variant_info)], I),
+        "icl_tune_cache_save": ([ctypes.c_char_p], I),
+        "icl_tune_cache_load": ([ctypes.c_char_p], I),
+        "icl_tune_cache_clear": ([], None),
+        "icl_tune_cache_size": ([], I),
+        "icl_variant_count": ([I], I),
+        "icl_variant_name": ([I, I, ctypes.c_char_p, ctypes.c_size_t], I),
+        "icl_force_variant": ([I, I], I),
+        "icl_last_variant": ([I], I),
+        "icl_launch_count": ([], ctypes.c_uint64),
+        "icl_last_error": ([], ctypes.c_char_p),
+        "icl_version": ([], ctypes.c_char_p),
+        "icl_fill_uniform": ([img, ctypes.c_uint64, I64, P], I),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != ICL_OK:
+        raise IclError(status, load_library().icl_last_error().decode())
+
+
+# ----------------------------------------------------------------------------- marshalling
+def _image(t, elem: int = 4) -> icl_image:
+    """icl_image descriptor of a CUDA tensor (H, W) or (B, H, W)."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("images are torch tensors")
+    if not t.is_cuda:
+        raise ValueError("images must live on a CUDA device (no CPU fallback)")
+    if t.element_size() != elem:
+        raise TypeError(f"expected element size {elem}, got {t.dtype}")
+    if t.dim() not in (2, 3) or t.stride(-1) != 1:
+        raise ValueError("images are (H, W) or (B, H, W) with unit stride along W")
+    b = t.shape[0] if t.dim() == 3 else 1
+    bs = t.stride(0) * elem if t.dim() == 3 else 0
+    return icl_image(t.data_ptr(), t.shape[-1], t.shape[-2], t.stride(-2) * elem, b, bs)
+
+
+def _stream(stream) -> Optional[int]:
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _taps(taps) -> "ctypes.Array":
+    vals = [float(v) for v in (taps.tolist() if hasattr(taps, "tolist") else taps)]
+    if len(vals) % 2 != 1:
+        raise ValueError("taps must have odd length 2r+1")
+    return (ctypes.c_float * len(vals))(*vals)
+
+
+def _band(band) -> Optional[icl_band]:
+    if band is None:
+        return None
+    gh, sy0, dy0 = band
+    return icl_band(gh, sy0, dy0)
+
+
+def _ref(x):
+    return None if x is None else ctypes.byref(x)
+
+
+# ----------------------------------------------------------------------------- filters
+def sepconv(src, dst, taps_x: Sequence[float], taps_y: Sequence[float], border: str = "constant",
+            border_value: float = 0.0, band=None, workspace=None, stream=None):
+    """Separable convolution (icl_sepconv).  Returns dst."""
+    lib = load_library()
+    fx, gy = _taps(taps_x), _taps(taps_y)
+    s, d = _image(src), _image(dst)
+    ws = workspace.data_ptr() if workspace is not None else None
+    wsb = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    _check(lib.icl_sepconv(ctypes.byref(s), ctypes.byref(d), ctypes.cast(fx, ctypes.c_void_p), len(fx) // 2,
+                           ctypes.cast(gy, ctypes.c_void_p), len(gy) // 2, BORDER[border], border_value,
+                           _ref(_band(band)), ws, wsb, _stream(stream)))
+    return dst
+
+
+def sepconv_workspace_bytes(width: int, height: int, batch: int = 1, ry: int = 15) -> int:
+    return int(load_library().icl_sepconv_workspace_bytes(width, height, batch, ry))
+
+
+def harris(src, response, block: int = 5, k: float = 0.04, border: str = "clamp", border_value: float = 0.0,
+           mask=None, threshold: float = 0.0, band=None, stream=None):
+    """Harris response (+ optional uint8 mask R > threshold) (icl_harris)."""
+    lib = load_library()
+    s, r = _image(src), _image(response)
+    m = _image(mask, 1) if mask is not None else None
+    _check(lib.icl_harris(ctypes.byref(s), ctypes.byref(r), block, k, BORDER[border], border_value, _ref(m),
+                          threshold, _ref(_band(band)), _stream(stream)))
+    return response
+
+
+def nlm(src, dst, patch_radius: int = 2, search_radius: int = 5, h: float = 0.1, border: str = "clamp",
+        border_value: float = 0.0, band=None, stream=None):
+    """Non-local means (icl_nlm; R11-R14)."""
+    lib = load_library()
+    s, d = _image(src), _image(dst)
+    _check(lib.icl_nlm(ctypes.byref(s), ctypes.byref(d), patch_radius, search_radius, h, BORDER[border],
+                       border_value, _ref(_band(band)), _stream(stream)))
+    return dst
+
+
+# ----------------------------------------------------------------------------- tuner / registry
+def tune(filter: str, src, dst, *, force: bool = False, verify: bool = True, stream=None, **params) -> dict:
+    """Auto-tune one problem (icl_tune).  ``params`` as for the filter call."""
+    lib = load_library()
+    p = icl_problem()
+    p.filter = FILTER[filter]
+    p.src, p.dst = _image(src), _image(dst)
+    p.border = BORDER[params.get("border", "constant" if filter == "sepconv" else "clamp")]
+    p.border_value = params.get("border_value", 0.0)
+    keep = []
+    if filter == "sepconv":
+        fx, gy = _taps(params["taps_x"]), _taps(params["taps_y"])
+        keep += [fx, gy]
+        p.taps_x, p.rx = ctypes.cast(fx, ctypes.c_void_p), len(fx) // 2
+        p.taps_y, p.ry = ctypes.cast(gy, ctypes.c_void_p), len(gy) // 2
+        ws = params.get("workspace")
+        if ws is not None:
+            p.workspace, p.workspace_bytes = ws.data_ptr(), ws.numel() * ws.element_size()
+    elif filter == "harris":
+        p.block, p.k = params.get("block", 5), params.get("k", 0.04)
+        if params.get("mask") is not None:
+            p.mask = _image(params["mask"], 1)
+        p.threshold = params.get("threshold", 0.0)
+    else:
+        p.patch_radius, p.search_radius = params.get("patch_radius", 2), params.get("search_radius", 5)
+        p.h = params.get("h", 0.1)
+    info = icl_variant_info()
+    flags = (1 if force else 0) | (0 if verify else 2)
+    _check(lib.icl_tune(ctypes.byref(p), flags, _stream(stream), ctypes.byref(info)))
+    return {"variant_id": info.variant_id, "name": info.name.decode(), "median_us": info.median_us,
+            "n_candidates": info.n_candidates, "n_rejected": info.n_rejected, "from_cache": bool(info.from_cache)}
+
+
+def tune_cache_save(path: str):
+    _check(load_library().icl_tune_cache_save(path.encode()))
+
+
+def tune_cache_load(path: str):
+    _check(load_library().icl_tune_cache_load(path.encode()))
+
+
+def tune_cache_clear():
+    load_library().icl_tune_cache_clear()
+
+
+def tune_cache_size() -> int:
+    return int(load_library().icl_tune_cache_size())
+
+
+def variant_names(filter: str) -> list:
+    lib = load_library()
+    out = []
+    buf = ctypes.create_string_buffer(128)
+    for i in range(lib.icl_variant_count(FILTER[filter])):
+        _check(lib.icl_variant_name(FILTER[filter], i, buf, 128))
+        out.append(buf.value.decode())
+    return out
+
+
+def force_variant(filter: str, variant):
+    """Force a variant (id or name) on this thread; None/-1 = automatic dispatch."""
+    if variant is None:
+        variant = -1
+    if isinstance(variant, str):
+        variant = variant_names(filter).index(variant)
+    _check(load_library().icl_force_variant(FILTER[filter], int(variant)))
+
+
+def last_variant(filter: str) -> int:
+    return int(load_library().icl_last_variant(FILTER[filter]))
+
+
+def launch_count() -> int:
+    return int(load_library().icl_launch_count())
+
+
+def version() -> str:
+    return load_library().icl_version().decode()
+
+
+def fill_uniform(img, seed: int, row0: int = 0, stream=None):
+    """Device SplitMix64 U[0,1) fill, equal to synth.uniform_image(seed + b, ...)."""
+    _check(load_library().icl_fill_uniform(ctypes.byref(_image(img)), seed, row0, _stream(stream)))
+    return img
+
+
+def harris_halo(block: int):
+    """Rows of input a Harris output row needs above / below (per-stage Sobel + window)."""
+    a = block // 2
+    return a + 1, block - 1 - a + 1
+
+
+def nlm_halo(patch_radius: int, search_radius: int):
+    r = patch_radius + search_radius
+    return r, r
+
+
+__all__ = ["sepconv", "harris", "nlm", "tune", "tune_cache_save", "tune_cache_load", "tune_cache_clear",
+           "tune_cache_size", "variant_names", "force_variant", "last_variant", "launch_count", "version",
+           "fill_uniform", "load_library", "IclError", "sepconv_workspace_bytes", "harris_halo", "nlm_halo",
+           "EXPORTS", "LIB_PATH"]

@@ -1,0 +1,708 @@
+// api.cu -- the C ABI of include/icl.h: argument validation, row-band views,
+// the variant registry (Table 1 -> B200 axes),
+// dispatch, the auto-tuner and its winner cache (§4;
+// SURVEY.md §8(a) a11).  No compute happens here: every step of the filters
+// runs in the kernels of sepconv.cu / harris.cu / nlm.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/icl.h"
+#include "internal.h"
+
+#define ICL_VERSION_STRING "icl-b200 0.1 (sm_100a)"
+
+namespace icl {
+
+bool nlm_tiled_supported(int P, int S);
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string t_err;
+static icl_status fail(icl_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  return st;
+}
+static icl_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(ICL_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------ images
+static icl_status check_image(const icl_image* im, int64_t elem, const char* name) {
+  if (!im) return fail(ICL_ERR_INVALID_ARG, "%s: null image descriptor", name);
+  if (!im->data) return fail(ICL_ERR_INVALID_ARG, "%s: null data pointer", name);
+  if (im->width < 1 || im->height < 1 || im->batch < 1)
+    return fail(ICL_ERR_INVALID_ARG, "%s: width/height/batch must be >= 1", name);
+  if (im->width >= (1ll << 31) || im->height >= (1ll << 31) || im->batch > 65535)
+    return fail(ICL_ERR_INVALID_ARG, "%s: size out of range", name);
+  if (im->pitch_bytes < im->width * elem || im->pitch_bytes % elem)
+    return fail(ICL_ERR_INVALID_ARG, "%s: pitch_bytes must be >= width*%lld and a multiple of %lld", name,
+                (long long)elem, (long long)elem);
+  if (im->batch > 1 && (im->batch_stride_bytes < im->height * im->pitch_bytes || im->batch_stride_bytes % elem))
+    return fail(ICL_ERR_INVALID_ARG, "%s: batch_stride_bytes must be >= height*pitch_bytes", name);
+  if (reinterpret_cast<uintptr_t>(im->data) % elem)
+    return fail(ICL_ERR_INVALID_ARG, "%s: data pointer not aligned to the element size", name);
+  return ICL_OK;
+}
+
+struct Range {
+  uintptr_t lo, hi;
+};
+static Range byte_range(const icl_image* im, int64_t elem) {
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(im->data);
+  const int64_t last = (im->batch - 1) * (im->batch > 1 ? im->batch_stride_bytes : 0) +
+                       (im->height - 1) * im->pitch_bytes + im->width * elem;
+  return {lo, lo + (uintptr_t)last};
+}
+static bool overlap(Range a, Range b) { return a.lo < b.hi && b.lo < a.hi; }
+
+static bool aligned16(const icl_image* im) {
+  const uint64_t bits = reinterpret_cast<uintptr_t>(im->data) | (uint64_t)im->pitch_bytes |
+                        (im->batch > 1 ? (uint64_t)im->batch_stride_bytes : 0);
+  return bits % 16 == 0;
+}
+static bool aligned4(const icl_image* im) {
+  const uint64_t bits = reinterpret_cast<uintptr_t>(im->data) | (uint64_t)im->pitch_bytes |
+                        (im->batch > 1 ? (uint64_t)im->batch_stride_bytes : 0);
+  return bits % 4 == 0;
+}
+
+// Resolve band + views; `up`/`down` = rows of stencil above/below an output.
+static icl_status make_views(const icl_image* src, const icl_image* dst, const icl_band* band, icl_border border,
+                             float cval, int up, int down, SrcView* sv, DstView* dv) {
+  if (border != ICL_BORDER_CONSTANT && border != ICL_BORDER_CLAMP)
+    return fail(ICL_ERR_INVALID_ARG, "border must be ICL_BORDER_CONSTANT or ICL_BORDER_CLAMP");
+  if (std::isnan(cval)) return fail(ICL_ERR_INVALID_ARG, "border_value is NaN");
+  if (src->width != dst->width) return fail(ICL_ERR_INVALID_ARG, "src and dst widths differ");
+  if (src->batch != dst->batch) return fail(ICL_ERR_INVALID_ARG, "src and dst batch differ");
+  int64_t Hg, sy0, dy0;
+  if (band) {
+    Hg = band->global_height;
+    sy0 = band->src_y0;
+    dy0 = band->dst_y0;
+    if (Hg < 1 || Hg >= (1ll << 31)) return fail(ICL_ERR_INVALID_ARG, "band: bad global_height");
+    if (sy0 < 0 || sy0 + src->height > Hg) return fail(ICL_ERR_INVALID_ARG, "band: src rows outside the image");
+    if (dy0 < 0 || dy0 + dst->height > Hg) return fail(ICL_ERR_INVALID_ARG, "band: dst rows outside the image");
+    const int64_t need_lo = std::max<int64_t>(0, dy0 - up);
+    const int64_t need_hi = std::min<int64_t>(Hg - 1, dy0 + dst->height - 1 + down);
+    if (need_lo < sy0 || need_hi > sy0 + src->height - 1)
+      return fail(ICL_ERR_INVALID_ARG, "band: src rows [%lld,%lld) do not cover the stencil rows [%lld,%lld]",
+                  (long long)sy0, (long long)(sy0 + src->height), (long long)need_lo, (long long)need_hi);
+  } else {
+    Hg = src->height;
+    sy0 = dy0 = 0;
+    if (dst->height != src->height) return fail(ICL_ERR_INVALID_ARG, "src and dst heights differ");
+  }
+  sv->base = static_cast<const char*>(src->data);
+  sv->pitch = src->pitch_bytes;
+  sv->bstride = src->batch > 1 ? src->batch_stride_bytes : 0;
+  sv->W = (int)src->width;
+  sv->Hg = (int)Hg;
+  sv->y0 = (int)sy0;
+  sv->border = border == ICL_BORDER_CLAMP ? kBorderClamp : kBorderConstant;
+  sv->cval = cval;
+  dv->base = static_cast<char*>(dst->data);
+  dv->pitch = dst->pitch_bytes;
+  dv->bstride = dst->batch > 1 ? dst->batch_stride_bytes : 0;
+  dv->H = (int)dst->height;
+  dv->y0 = (int)dy0;
+  return ICL_OK;
+}
+
+// ------------------------------------------------------------------ variants
+enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM };
+struct Variant {
+  const char* name;
+  Kind kind;
+  int nt, vec, S;
+};
+
+static const Variant kSepVariants[] = {
+    {"naive_direct", K_NAIVE, 0, 0, 0},           {"naive_2pass", K_TWOPASS, 0, 0, 0},
+    {"stream_nt64_s64_v4", K_STREAM, 64, 4, 64},  {"stream_nt32_s32_v4", K_STREAM, 32, 4, 32},
+    {"stream_nt128_s64_v4", K_STREAM, 128, 4, 64}, {"stream_nt64_s128_v4", K_STREAM, 64, 4, 128},
+    {"stream_nt32_s16_v4", K_STREAM, 32, 4, 16},  {"stream_nt64_s256_v4", K_STREAM, 64, 4, 256},
+    {"stream_nt64_s64_v1", K_STREAM, 64, 1, 64},
+};
+static const Variant kHarVariants[] = {
+    {"naive_direct", K_NAIVE, 0, 0, 0},           {"stream_nt64_s64_v4", K_STREAM, 64, 4, 64},
+    {"stream_nt32_s32_v4", K_STREAM, 32, 4, 32},  {"stream_nt128_s64_v4", K_STREAM, 128, 4, 64},
+    {"stream_nt64_s128_v4", K_STREAM, 64, 4, 128}, {"stream_nt32_s16_v4", K_STREAM, 32, 4, 16},
+    {"stream_nt64_s64_v1", K_STREAM, 64, 1, 64},
+};
+static const Variant kNlmVariants[] = {
+    {"naive_direct", K_NAIVE, 0, 0, 0},
+    {"tiled_direct_32x8", K_TILED, 32, 0, 8},
+};
+
+static const Variant* table(icl_filter f, int* n) {
+  switch (f) {
+    case ICL_FILTER_SEPCONV: *n = (int)(sizeof kSepVariants / sizeof *kSepVariants); return kSepVariants;
+    case ICL_FILTER_HARRIS: *n = (int)(sizeof kHarVariants / sizeof *kHarVariants); return kHarVariants;
+    case ICL_FILTER_NLM: *n = (int)(sizeof kNlmVariants / sizeof *kNlmVariants); return kNlmVariants;
+  }
+  *n = 0;
+  return nullptr;
+}
+
+static thread_local int t_force[3] = {-1, -1, -1};
+static thread_local int t_last[3] = {-1, -1, -1};
+
+// Prepared call of any filter (what a variant launcher needs).
+struct Prepared {
+  icl_filter f;
+  SepCall sep;
+  HarrisCall har;
+  NlmCall nlm;
+  bool a16;       // src/dst (and mask) 16B-aligned
+  int64_t pixels; // W * H * batch
+  size_t dst_bytes_compact;
+  std::string key;
+};
+
+static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
+  *why = ICL_ERR_UNSUPPORTED;
+  if (v.kind == K_STREAM && v.vec == 4 && !pc.a16) return false;
+  if (pc.f == ICL_FILTER_SEPCONV && v.kind == K_TWOPASS) {
+    const size_t need = sep_2pass_workspace(pc.sep.src.W, pc.sep.dst.H, pc.sep.batch, pc.sep.ry);
+    if (!pc.sep.workspace || pc.sep.workspace_bytes < need) {
+      *why = ICL_ERR_WORKSPACE;
+      return false;
+    }
+  }
+  if (pc.f == ICL_FILTER_NLM && v.kind == K_TILED && !nlm_tiled_supported(pc.nlm.P, pc.nlm.S)) return false;
+  if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXSUM) return false;
+  return true;
+}
+
+static cudaError_t run_variant(const Prepared& pc, const Variant& v, cudaStream_t s) {
+  switch (pc.f) {
+    case ICL_FILTER_SEPCONV:
+      if (v.kind == K_NAIVE) return launch_sep_naive_direct(pc.sep, s);
+      if (v.kind == K_TWOPASS) return launch_sep_naive_2pass(pc.sep, s);
+      return launch_sep_stream(pc.sep, v.nt, v.vec, v.S, s);
+    case ICL_FILTER_HARRIS:
+      if (v.kind == K_NAIVE) return launch_harris_naive(pc.har, s);
+      return launch_harris_stream(pc.har, v.nt, v.vec, v.S, s);
+    case ICL_FILTER_NLM:
+      if (v.kind == K_NAIVE) return launch_nlm_naive(pc.nlm, s);
+      if (v.kind == K_TILED) return launch_nlm_tiled(pc.nlm, v.nt, v.S, s);
+      return launch_nlm_boxsum(pc.nlm, 0, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// Default (untuned) choice: a heuristic per filter.
+static int default_variant(const Prepared& pc) {
+  switch (pc.f) {
+    case ICL_FILTER_SEPCONV:
+      if (!pc.a16) return 8;
+      return pc.pixels < (1 << 20) ? 6 : 2;
+    case ICL_FILTER_HARRIS:
+      if (!pc.a16) return 6;
+      return pc.pixels < (1 << 20) ? 5 : 1;
+    case ICL_FILTER_NLM:
+      return nlm_tiled_supported(pc.nlm.P, pc.nlm.S) ? 1 : 0;
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------ tune cache
+static std::mutex g_cache_mu;
+static std::map<std::string, int> g_cache;
+
+static std::string device_tag() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return "unknown";
+  std::ostringstream os;
+  os << prop.name << "|sm" << prop.major << prop.minor << "|" << prop.multiProcessorCount << "SMs|"
+     << ICL_VERSION_STRING;
+  return os.str();
+}
+
+static int cache_lookup(const std::string& key) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto it = g_cache.find(key);
+  return it == g_cache.end() ? -1 : it->second;
+}
+
+static const char* policy() {
+  const char* p = getenv("ICL_TUNE_POLICY");
+  return p ? p : "off";
+}
+
+static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, icl_variant_info* info);
+
+static icl_status dispatch(Prepared& pc, cudaStream_t s) {
+  int n;
+  const Variant* vt = table(pc.f, &n);
+  int vid = t_force[pc.f];
+  icl_status why;
+  if (vid >= 0) {
+    if (vid >= n) return fail(ICL_ERR_INVALID_ARG, "forced variant %d out of range", vid);
+    if (!eligible(pc, vt[vid], &why)) return fail(why, "forced variant %s is not eligible for this call", vt[vid].name);
+  } else {
+    vid = cache_lookup(pc.key);
+    if (vid >= n || (vid >= 0 && !eligible(pc, vt[vid], &why))) vid = -1;
+    if (vid < 0) {
+      const char* pol = policy();
+      if (!strcmp(pol, "require")) return fail(ICL_ERR_NOT_TUNED, "no tune-cache entry for %s", pc.key.c_str());
+      if (!strcmp(pol, "on_miss")) {
+        icl_variant_info info;
+        icl_status st = tune_prepared(pc, 0, s, &info);
+        if (st != ICL_OK) return st;
+        t_last[pc.f] = info.variant_id;
+        return ICL_OK;  // the tuner leaves the winner's output in dst
+      }
+      vid = default_variant(pc);
+      if (!eligible(pc, vt[vid], &why)) vid = 0;
+    }
+  }
+  cudaError_t e = run_variant(pc, vt[vid], s);
+  if (e != cudaSuccess) return cuda_fail(e, vt[vid].name);
+  t_last[pc.f] = vid;
+  return ICL_OK;
+}
+
+// ------------------------------------------------------------------ preparation
+static std::string fmt_key(const char* f, const icl_image* dst, bool a16, const std::string& params) {
+  std::ostringstream os;
+  os << f << ":W" << dst->width << ":H" << dst->height << ":B" << dst->batch << ":a" << (a16 ? 16 : 4) << ":"
+     << params;
+  return os.str();
+}
+
+static icl_status prep_sepconv(const icl_image* src, const icl_image* dst, const float* tx, int rx, const float* ty,
+                               int ry, icl_border border, float cval, const icl_band* band, void* ws, size_t wsb,
+                               Prepared* pc) {
+  icl_status st;
+  if ((st = check_image(src, 4, "src")) || (st = check_image(dst, 4, "dst"))) return st;
+  if (!tx || !ty) return fail(ICL_ERR_INVALID_ARG, "null taps");
+  if (rx < 0 || ry < 0) return fail(ICL_ERR_INVALID_ARG, "negative radius");
+  if (rx > kMaxRadius || ry > kMaxRadius) return fail(ICL_ERR_UNSUPPORTED, "radius > %d", kMaxRadius);
+  for (int i = 0; i < 2 * rx + 1; ++i)
+    if (!std::isfinite(tx[i])) return fail(ICL_ERR_INVALID_ARG, "non-finite tap");
+  for (int i = 0; i < 2 * ry + 1; ++i)
+    if (!std::isfinite(ty[i])) return fail(ICL_ERR_INVALID_ARG, "non-finite tap");
+  if (overlap(byte_range(src, 4), byte_range(dst, 4))) return fail(ICL_ERR_ALIASING, "src and dst overlap");
+  pc->f = ICL_FILTER_SEPCONV;
+  if ((st = make_views(src, dst, band, border, cval, ry, ry, &pc->sep.src, &pc->sep.dst))) return st;
+  pc->sep.batch = (int)src->batch;
+  pc->sep.rx = rx;
+  pc->sep.ry = ry;
+  pc->sep.fx = tx;
+  pc->sep.gy = ty;
+  pc->sep.workspace = ws;
+  pc->sep.workspace_bytes = wsb;
+  if (ws && wsb) {
+    Range w{reinterpret_cast<uintptr_t>(ws), reinterpret_cast<uintptr_t>(ws) + wsb};
+    if (overlap(w, byte_range(src, 4)) || overlap(w, byte_range(dst, 4)))
+      return fail(ICL_ERR_ALIASING, "workspace overlaps an image");
+  }
+  pc->a16 = aligned16(src) && aligned16(dst);
+  pc->pixels = src->width * dst->height * src->batch;
+  pc->dst_bytes_compact = (size_t)pc->pixels * 4;
+  std::ostringstream ps;
+  ps << "rx" << rx << ":ry" << ry << ":bd" << (int)border;
+  pc->key = fmt_key("sepconv", dst, pc->a16, ps.str());
+  return ICL_OK;
+}
+
+static icl_status prep_harris(const icl_image* src, const icl_image* resp, int block, float k, icl_border border,
+                              float cval, const icl_image* mask, float thr, const icl_band* band, Prepared* pc) {
+  icl_status st;
+  if ((st = check_image(src, 4, "src")) || (st = check_image(resp, 4, "response"))) return st;
+  if (block < 1 || block > 7) return fail(ICL_ERR_INVALID_ARG, "block must be in [1, 7]");
+  if (!std::isfinite(k)) return fail(ICL_ERR_INVALID_ARG, "k must be finite");
+  if (std::isnan(thr)) return fail(ICL_ERR_INVALID_ARG, "threshold is NaN");
+  if (overlap(byte_range(src, 4), byte_range(resp, 4))) return fail(ICL_ERR_ALIASING, "src and response overlap");
+  pc->f = ICL_FILTER_HARRIS;
+  const int a = block / 2, bb = block - 1 - a;
+  if ((st = make_views(src, resp, band, border, cval, a + 1, bb + 1, &pc->har.src, &pc->har.dst))) return st;
+  pc->har.mask = nullptr;
+  pc->har.mpitch = pc->har.mbstride = 0;
+  bool mask_a4 = true;
+  if (mask && mask->data) {
+    if ((st = check_image(mask, 1, "mask"))) return st;
+    if (mask->width != resp->width || mask->height != resp->height || mask->batch != resp->batch)
+      return fail(ICL_ERR_INVALID_ARG, "mask shape differs from the response");
+    if (overlap(byte_range(mask, 1), byte_range(src, 4)) || overlap(byte_range(mask, 1), byte_range(resp, 4)))
+      return fail(ICL_ERR_ALIASING, "mask overlaps an image");
+    pc->har.mask = static_cast<char*>(mask->data);
+    pc->har.mpitch = mask->pitch_bytes;
+    pc->har.mbstride = mask->batch > 1 ? mask->batch_stride_bytes : 0;
+    mask_a4 = aligned4(mask);
+  }
+  pc->har.batch = (int)src->batch;
+  pc->har.block = block;
+  pc->har.k = k;
+  pc->har.threshold = thr;
+  pc->a16 = aligned16(src) && aligned16(resp) && mask_a4;
+  pc->pixels = src->width * resp->height * src->batch;
+  pc->dst_bytes_compact = (size_t)pc->pixels * 4;
+  std::ostringstream ps;
+  ps << "B" << block << ":bd" << (int)border << ":m" << (pc->har.mask ? 1 : 0);
+  pc->key = fmt_key("harris", resp, pc->a16, ps.str());
+  return ICL_OK;
+}
+
+static icl_status prep_nlm(const icl_image* src, const icl_image* dst, int P, int S, float h, icl_border border,
+                           float cval, const icl_band* band, Prepared* pc) {
+  icl_status st;
+  if ((st = check_image(src, 4, "src")) || (st = check_image(dst, 4, "dst"))) return st;
+  if (P < 0 || P > 3) return fail(ICL_ERR_INVALID_ARG, "patch_radius must be in [0, 3]");
+  if (S < 0 || S > 10) return fail(ICL_ERR_INVALID_ARG, "search_radius must be in [0, 10]");
+  if (std::isnan(h) || !(h > 0.0f)) return fail(ICL_ERR_INVALID_ARG, "h must be > 0 (or +INF)");
+  if (overlap(byte_range(src, 4), byte_range(dst, 4))) return fail(ICL_ERR_ALIASING, "src and dst overlap");
+  pc->f = ICL_FILTER_NLM;
+  if ((st = make_views(src, dst, band, border, cval, P + S, P + S, &pc->nlm.src, &pc->nlm.dst))) return st;
+  pc->nlm.batch = (int)src->batch;
+  pc->nlm.P = P;
+  pc->nlm.S = S;
+  pc->nlm.h = h;
+  if (std::isinf(h)) {
+    pc->nlm.coef = 0.0f;
+  } else {
+    const double pw = 2.0 * P + 1.0;
+    const double coef = 1.4426950408889634 / (pw * pw * (double)h * (double)h);
+    pc->nlm.coef = coef > 3.0e38 ? 3.0e38f : (float)coef;
+  }
+  pc->a16 = aligned16(src) && aligned16(dst);
+  pc->pixels = src->width * dst->height * src->batch;
+  pc->dst_bytes_compact = (size_t)pc->pixels * 4;
+  std::ostringstream ps;
+  ps << "P" << P << ":S" << S << ":bd" << (int)border;
+  pc->key = fmt_key("nlm", dst, pc->a16, ps.str());
+  return ICL_OK;
+}
+
+// ------------------------------------------------------------------ tuner
+__global__ void compare_kernel(const char* a, int64_t apitch, int64_t abstride, const float* ref, int W, int H,
+                               unsigned long long* out) {
+  // out[0] = #unequal, out[1] = max|a-ref| (float bits), out[2] = max|ref| (float bits)
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  const int b = blockIdx.z;
+  if (x >= W) return;
+  const float va = reinterpret_cast<const float*>(a + (int64_t)b * abstride + (int64_t)y * apitch)[x];
+  const float vr = ref[((int64_t)b * H + y) * W + x];
+  const bool eq = (va == vr) || (va != va && vr != vr);
+  if (!eq) atomicAdd(out, 1ull);
+  const float d = fabsf(va - vr);
+  atomicMax(reinterpret_cast<unsigned int*>(out + 1), __float_as_uint(d != d ? 3.0e38f : d));
+  atomicMax(reinterpret_cast<unsigned int*>(out + 2), __float_as_uint(fabsf(vr)));
+}
+
+static std::mutex g_tune_mu;
+static void* g_flush = nullptr;
+static size_t g_flush_bytes = 0;
+
+static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, icl_variant_info* info) {
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  int n;
+  const Variant* vt = table(pc.f, &n);
+  if (!(flags & ICL_TUNE_FORCE)) {
+    const int hit = cache_lookup(pc.key);
+    icl_status why;
+    if (hit >= 0 && hit < n && eligible(pc, vt[hit], &why)) {
+      cudaError_t e = run_variant(pc, vt[hit], s);
+      if (e != cudaSuccess) return cuda_fail(e, "tune (cached winner)");
+      if (info) {
+        memset(info, 0, sizeof *info);
+        info->variant_id = hit;
+        snprintf(info->name, sizeof info->name, "%s", vt[hit].name);
+        info->median_us = -1.0f;
+        info->from_cache = 1;
+      }
+      return ICL_OK;
+    }
+  }
+  // Views of the real destination (the problem's dst).
+  const DstView real_dst = pc.f == ICL_FILTER_SEPCONV ? pc.sep.dst : (pc.f == ICL_FILTER_HARRIS ? pc.har.dst : pc.nlm.dst);
+  const int W = pc.f == ICL_FILTER_SEPCONV ? pc.sep.src.W : (pc.f == ICL_FILTER_HARRIS ? pc.har.src.W : pc.nlm.src.W);
+  const int H = real_dst.H;
+  const int batch = (int)(pc.pixels / ((int64_t)W * H));
+  float* ref = nullptr;
+  unsigned long long* cmp = nullptr;
+  cudaError_t e;
+  if ((e = cudaMalloc(&ref, pc.dst_bytes_compact)) != cudaSuccess) return cuda_fail(e, "tune: cudaMalloc");
+  if ((e = cudaMalloc(&cmp, 3 * sizeof(unsigned long long))) != cudaSuccess) {
+    cudaFree(ref);
+    return cuda_fail(e, "tune: cudaMalloc");
+  }
+  // L2 flush buffer (timing hygiene): 2x L2, allocated once.
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+  const size_t ws_bytes = 2 * pc.dst_bytes_compact;
+  const bool flush = ws_bytes < (size_t)l2 * 2;
+  if (flush && g_flush_bytes < (size_t)l2 * 2) {
+    if (g_flush) cudaFree(g_flush);
+    g_flush = nullptr;
+    g_flush_bytes = 0;
+    if (cudaMalloc(&g_flush, (size_t)l2 * 2) == cudaSuccess) g_flush_bytes = (size_t)l2 * 2;
+  }
+  // Reference: the naive variant (id 0) into the compact scratch buffer.
+  Prepared pref = pc;
+  DstView cdst{reinterpret_cast<char*>(ref), (int64_t)W * 4, (int64_t)W * H * 4, H, real_dst.y0};
+  if (pc.f == ICL_FILTER_SEPCONV) pref.sep.dst = cdst;
+  else if (pc.f == ICL_FILTER_HARRIS) { pref.har.dst = cdst; pref.har.mask = nullptr; }
+  else pref.nlm.dst = cdst;
+  if ((e = run_variant(pref, vt[0], s)) != cudaSuccess) {
+    cudaFree(ref);
+    cudaFree(cmp);
+    return cuda_fail(e, "tune: reference");
+  }
+  cudaEvent_t ev0, ev1;
+  cudaEventCreate(&ev0);
+  cudaEventCreate(&ev1);
+  int best = -1, ncand = 0, nrej = 0;
+  float best_us = 0.0f;
+  for (int v = 0; v < n; ++v) {
+    icl_status why;
+    if (!eligible(pc, vt[v], &why)) continue;
+    ++ncand;
+    if ((e = run_variant(pc, vt[v], s)) != cudaSuccess) { ++nrej; cudaGetLastError(); continue; }
+    if (!(flags & ICL_TUNE_NO_VERIFY) && v != 0) {
+      cudaMemsetAsync(cmp, 0, 3 * sizeof(unsigned long long), s);
+      dim3 g((W + 255) / 256, H, batch);
+      compare_kernel<<<g, 256, 0, s>>>(real_dst.base, real_dst.pitch, real_dst.bstride, ref, W, H, cmp);
+      unsigned long long hc[3];
+      cudaMemcpyAsync(hc, cmp, sizeof hc, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      float md, mr;
+      unsigned int b1 = (unsigned int)hc[1], b2 = (unsigned int)hc[2];
+      memcpy(&md, &b1, 4);
+      memcpy(&mr, &b2, 4);
+      const bool ok = pc.f == ICL_FILTER_SEPCONV ? hc[0] == 0 : md <= 1e-4f * std::max(mr, 1e-30f);
+      if (!ok) { ++nrej; continue; }
+    }
+    // warm-up then timed reps (median)
+    for (int w = 0; w < 2; ++w) run_variant(pc, vt[v], s);
+    std::vector<float> ts;
+    float total = 0.0f;
+    for (int r = 0; r < 50 && (r < 10 || total < 50000.0f); ++r) {
+      if (flush && g_flush) cudaMemsetAsync(g_flush, r & 0xff, g_flush_bytes, s);
+      cudaEventRecord(ev0, s);
+      run_variant(pc, vt[v], s);
+      cudaEventRecord(ev1, s);
+      cudaEventSynchronize(ev1);
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, ev0, ev1);
+      ts.push_back(ms * 1000.0f);
+      total += ms * 1000.0f;
+      if (r >= 10 && total > 200000.0f) break;
+    }
+    std::sort(ts.begin(), ts.end());
+    const float med = ts[ts.size() / 2];
+    if (best < 0 || med < best_us * 0.995f) { best = v; best_us = med; }
+  }
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  icl_status st = ICL_OK;
+  if (best < 0) st = fail(ICL_ERR_CUDA, "tune: no variant succeeded");
+  else {
+    if ((e = run_variant(pc, vt[best], s)) != cudaSuccess) st = cuda_fail(e, "tune: winner");
+    {
+      std::lock_guard<std::mutex> lk2(g_cache_mu);
+      g_cache[pc.key] = best;
+    }
+    if (info) {
+      memset(info, 0, sizeof *info);
+      info->variant_id = best;
+      snprintf(info->name, sizeof info->name, "%s", vt[best].name);
+      info->median_us = best_us;
+      info->n_candidates = ncand;
+      info->n_rejected = nrej;
+      info->from_cache = 0;
+    }
+  }
+  cudaStreamSynchronize(s);
+  cudaFree(ref);
+  cudaFree(cmp);
+  if (st == ICL_OK && (e = cudaGetLastError()) != cudaSuccess) st = cuda_fail(e, "tune");
+  return st;
+}
+
+}  // namespace icl
+
+using namespace icl;
+
+// ======================================================================== C ABI
+extern "C" {
+
+icl_status icl_sepconv(const icl_image* src, const icl_image* dst, const float* taps_x, int rx, const float* taps_y,
+                       int ry, icl_border border, float border_value, const icl_band* band, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  Prepared pc;
+  icl_status st = prep_sepconv(src, dst, taps_x, rx, taps_y, ry, border, border_value, band, workspace,
+                               workspace_bytes, &pc);
+  if (st != ICL_OK) return st;
+  return dispatch(pc, static_cast<cudaStream_t>(stream));
+}
+
+size_t icl_sepconv_workspace_bytes(int64_t width, int64_t height, int64_t batch, int ry) {
+  if (width < 1 || height < 1 || batch < 1 || ry < 0) return 0;
+  return sep_2pass_workspace(width, height, batch, ry);
+}
+
+icl_status icl_harris(const icl_image* src, const icl_image* response, int block, float k, icl_border border,
+                      float border_value, const icl_image* mask, float threshold, const icl_band* band,
+                      void* stream) {
+  Prepared pc;
+  icl_status st = prep_harris(src, response, block, k, border, border_value, mask, threshold, band, &pc);
+  if (st != ICL_OK) return st;
+  return dispatch(pc, static_cast<cudaStream_t>(stream));
+}
+
+icl_status icl_nlm(const icl_image* src, const icl_image* dst, int patch_radius, int search_radius, float h,
+                   icl_border border, float border_value, const icl_band* band, void* stream) {
+  Prepared pc;
+  icl_status st = prep_nlm(src, dst, patch_radius, search_radius, h, border, border_value, band, &pc);
+  if (st != ICL_OK) return st;
+  return dispatch(pc, static_cast<cudaStream_t>(stream));
+}
+
+icl_status icl_tune(const icl_problem* p, unsigned flags, void* stream, icl_variant_info* chosen) {
+  if (!p) return fail(ICL_ERR_INVALID_ARG, "null problem");
+  Prepared pc;
+  icl_status st;
+  switch (p->filter) {
+    case ICL_FILTER_SEPCONV:
+      st = prep_sepconv(&p->src, &p->dst, p->taps_x, p->rx, p->taps_y, p->ry, p->border, p->border_value, nullptr,
+                        p->workspace, p->workspace_bytes, &pc);
+      break;
+    case ICL_FILTER_HARRIS:
+      st = prep_harris(&p->src, &p->dst, p->block, p->k, p->border, p->border_value, &p->mask, p->threshold,
+                       nullptr, &pc);
+      break;
+    case ICL_FILTER_NLM:
+      st = prep_nlm(&p->src, &p->dst, p->patch_radius, p->search_radius, p->h, p->border, p->border_value,
+                    nullptr, &pc);
+      break;
+    default:
+      return fail(ICL_ERR_INVALID_ARG, "unknown filter");
+  }
+  if (st != ICL_OK) return st;
+  return tune_prepared(pc, flags, static_cast<cudaStream_t>(stream), chosen);
+}
+
+icl_status icl_tune_cache_save(const char* path) {
+  if (!path) return fail(ICL_ERR_INVALID_ARG, "null path");
+  std::ofstream f(path);
+  if (!f) return fail(ICL_ERR_INVALID_ARG, "cannot open %s", path);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  f << "{\n\"device\": \"" << device_tag() << "\",\n\"entries\": {\n";
+  size_t i = 0;
+  for (auto& kv : g_cache) {
+    int n;
+    const Variant* vt = table(kv.first.rfind("sepconv", 0) == 0   ? ICL_FILTER_SEPCONV
+                              : kv.first.rfind("harris", 0) == 0 ? ICL_FILTER_HARRIS
+                                                                  : ICL_FILTER_NLM,
+                              &n);
+    f << "\"" << kv.first << "\": [" << kv.second << ", \"" << (kv.second < n ? vt[kv.second].name : "?") << "\"]"
+      << (++i < g_cache.size() ? "," : "") << "\n";
+  }
+  f << "}\n}\n";
+  return f ? ICL_OK : fail(ICL_ERR_INVALID_ARG, "write failed: %s", path);
+}
+
+icl_status icl_tune_cache_load(const char* path) {
+  if (!path) return fail(ICL_ERR_INVALID_ARG, "null path");
+  std::ifstream f(path);
+  if (!f) return fail(ICL_ERR_INVALID_ARG, "cannot open %s", path);
+  std::string line, dev;
+  std::map<std::string, int> entries;
+  while (std::getline(f, line)) {
+    if (line.rfind("\"device\": \"", 0) == 0) {
+      const size_t e = line.rfind('"');
+      dev = line.substr(11, e - 11);
+    } else if (!line.empty() && line[0] == '"' && line.find("\": [") != std::string::npos) {
+      const size_t q = line.find("\": [");
+      const std::string key = line.substr(1, q - 1);
+      const int id = atoi(line.c_str() + q + 4);
+      entries[key] = id;
+    }
+  }
+  if (dev != device_tag()) return fail(ICL_ERR_INVALID_ARG, "tune cache is for another device/build: %s", dev.c_str());
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (auto& kv : entries) g_cache[kv.first] = kv.second;
+  return ICL_OK;
+}
+
+void icl_tune_cache_clear(void) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cache.clear();
+}
+
+int icl_tune_cache_size(void) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  return (int)g_cache.size();
+}
+
+int icl_variant_count(icl_filter filter) {
+  int n;
+  table(filter, &n);
+  return n;
+}
+
+icl_status icl_variant_name(icl_filter filter, int id, char* buf, size_t len) {
+  int n;
+  const Variant* vt = table(filter, &n);
+  if (!vt || id < 0 || id >= n || !buf || !len) return fail(ICL_ERR_INVALID_ARG, "bad variant query");
+  snprintf(buf, len, "%s", vt[id].name);
+  return ICL_OK;
+}
+
+icl_status icl_force_variant(icl_filter filter, int id) {
+  int n;
+  if (!table(filter, &n)) return fail(ICL_ERR_INVALID_ARG, "unknown filter");
+  if (id < -1 || id >= n) return fail(ICL_ERR_INVALID_ARG, "variant id %d out of range", id);
+  t_force[filter] = id;
+  return ICL_OK;
+}
+
+int icl_last_variant(icl_filter filter) {
+  if (filter < 0 || filter > 2) return -1;
+  return t_last[filter];
+}
+
+uint64_t icl_launch_count(void) { return g_launches.load(); }
+
+const char* icl_last_error(void) { return t_err.c_str(); }
+
+const char* icl_version(void) { return ICL_VERSION_STRING; }
+
+icl_status icl_fill_uniform(const icl_image* img, uint64_t seed, int64_t row0, void* stream) {
+  icl_status st = check_image(img, 4, "img");
+  if (st != ICL_OK) return st;
+  cudaError_t e = launch_fill_uniform(static_cast<float*>(img->data), img->width, img->height, img->pitch_bytes,
+                                      img->batch, img->batch > 1 ? img->batch_stride_bytes : 0, seed, row0,
+                                      static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fill_uniform");
+  return ICL_OK;
+}
+
+}  // extern "C"

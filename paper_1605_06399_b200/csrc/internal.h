@@ -1,0 +1,64 @@
+// internal.h -- host-side declarations shared by the C-ABI layer (api.cu) and
+// the kernel translation units.  Product code only.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace icl {
+
+void count_launch();
+
+struct SepCall {
+  SrcView src;
+  DstView dst;
+  int batch;
+  int rx, ry;
+  const float* fx;  // host, 2rx+1
+  const float* gy;  // host, 2ry+1
+  void* workspace;
+  size_t workspace_bytes;
+};
+
+struct HarrisCall {
+  SrcView src;
+  DstView dst;      // response
+  char* mask;       // nullable
+  int64_t mpitch, mbstride;
+  int batch;
+  int block;
+  float k;
+  float threshold;
+};
+
+struct NlmCall {
+  SrcView src;
+  DstView dst;
+  int batch;
+  int P;      // patch radius
+  int S;      // search radius
+  float h;    // +inf allowed
+  float coef; // log2(e) / ((2P+1)^2 h^2), 0 when h = +inf
+};
+
+// sepconv
+cudaError_t launch_sep_naive_direct(const SepCall& c, cudaStream_t s);
+cudaError_t launch_sep_naive_2pass(const SepCall& c, cudaStream_t s);
+size_t sep_2pass_workspace(int64_t W, int64_t H, int64_t batch, int ry);
+cudaError_t launch_sep_stream(const SepCall& c, int nt, int vec, int S, cudaStream_t s);
+
+// harris
+cudaError_t launch_harris_naive(const HarrisCall& c, cudaStream_t s);
+cudaError_t launch_harris_stream(const HarrisCall& c, int nt, int vec, int S, cudaStream_t s);
+
+// nlm
+cudaError_t launch_nlm_naive(const NlmCall& c, cudaStream_t s);
+cudaError_t launch_nlm_tiled(const NlmCall& c, int tw, int th, cudaStream_t s);
+cudaError_t launch_nlm_boxsum(const NlmCall& c, int variant, cudaStream_t s);
+
+// synthetic inputs
+cudaError_t launch_fill_uniform(float* base, int64_t W, int64_t H, int64_t pitch, int64_t batch,
+                                int64_t bstride, uint64_t seed, int64_t row0, cudaStream_t s);
+
+}  // namespace icl

@@ -1,0 +1,49 @@
+"""Tolerance definitions of BASELINE.json north_star, made well-defined near
+cancellation as SURVEY.md §8(c) / DESIGN.md "Tolerances" state.  Test-only."""
+import numpy as np
+
+import oracle
+
+SEP_TOL = 1e-5      # north_star: max relative error 1e-5 for convolution
+HARRIS_TOL = 1e-4   # north_star: 1e-4 for the Harris response
+NLM_TOL = 1e-4      # north_star: 1e-4 for NLM
+
+
+def sep_scale(img, fx, gy, border, c, points=None):
+    """(|g| * |f| * |x|)(p): the magnitude the fp32 sum is computed over."""
+    a = np.abs(img)
+    return oracle.sepconv(a, np.abs(fx), np.abs(gy), border, abs(c), points=points)
+
+
+def check_sepconv(got, img, fx, gy, border, c, points=None, tol=SEP_TOL):
+    ref = oracle.sepconv(img, fx, gy, border, c, points=points)
+    scale = sep_scale(img, fx, gy, border, c, points=points)
+    got = np.asarray(got, dtype=np.float64)
+    err = np.abs(got - ref)
+    bad = np.where(scale > 0, err > tol * scale, err != 0)
+    assert not bad.any(), f"sepconv: {bad.sum()} pixels out of tolerance; max rel {np.max(err / np.maximum(scale, 1e-300))}"
+    return float(np.max(err / np.maximum(scale, 1e-300))) if err.size else 0.0
+
+
+def check_harris(R, mask, img, block, k, border, c, threshold, points=None, tol=HARRIS_TOL):
+    Rr, S = oracle.harris(img, block, k, border, c, points=points, with_tensor=True)
+    D = oracle.harris_scale(S, k)
+    R = np.asarray(R, dtype=np.float64)
+    err = np.abs(R - Rr)
+    bad = np.where(D > 0, err > tol * D, err != 0)
+    assert not bad.any(), f"harris: {bad.sum()} pixels out of tolerance; max rel {np.max(err / np.maximum(D, 1e-300))}"
+    if mask is not None:
+        mref = Rr > threshold
+        near = np.abs(Rr - threshold) <= tol * D
+        diff = (np.asarray(mask) != 0) != mref
+        assert not (diff & ~near).any(), f"harris mask: {(diff & ~near).sum()} pixels differ away from the threshold"
+    return float(np.max(err / np.maximum(D, 1e-300))) if err.size else 0.0
+
+
+def check_nlm(got, img, P, S, h, border, c, points=None, tol=NLM_TOL):
+    ref, scale = oracle.nlm(img, P, S, h, border, c, points=points, with_scale=True)
+    got = np.asarray(got, dtype=np.float64)
+    err = np.abs(got - ref)
+    bad = np.where(scale > 0, err > tol * scale, err != 0)
+    assert not bad.any(), f"nlm: {bad.sum()} pixels out of tolerance; max rel {np.max(err / np.maximum(scale, 1e-300))}"
+    return float(np.max(err / np.maximum(scale, 1e-300))) if err.size else 0.0

@@ -1,0 +1,87 @@
+"""CPU checks of the C-ABI boundary: the library loads, exports every symbol
+include/icl.h declares, and the host-side registry answers without a GPU.
+No compute calls (there is no GPU here)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_1605_06399_b200 as icl
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "icl.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(icl_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_builds_and_loads():
+    from paper_1605_06399_b200 import build
+    path = build.build()
+    assert os.path.exists(path)
+    icl.load_library()
+    assert icl.version().startswith("icl-b200")
+
+
+def test_every_declared_symbol_is_exported():
+    decl = _declared()
+    assert set(decl) == set(icl.EXPORTS), (set(decl) ^ set(icl.EXPORTS))
+    out = subprocess.run(["nm", "-D", "--defined-only", icl.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (icl_[a-z0-9_]+)$", out, flags=re.M))
+    missing = set(decl) - exported
+    assert not missing, missing
+    lib = icl.load_library()
+    for name in decl:
+        assert getattr(lib, name)
+
+
+def test_kernels_are_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", icl.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_registry_without_gpu():
+    names = icl.variant_names("sepconv")
+    assert names[0] == "naive_direct" and any(n.startswith("stream") for n in names)
+    assert icl.variant_names("harris")[0] == "naive_direct"
+    assert icl.variant_names("nlm")[0] == "naive_direct"
+    icl.force_variant("sepconv", 2)
+    icl.force_variant("sepconv", None)
+    with pytest.raises(icl.IclError):
+        icl.force_variant("sepconv", 999)
+    assert icl.sepconv_workspace_bytes(512, 512, 1, 2) >= 512 * 516 * 4
+    assert icl.tune_cache_size() == 0
+
+
+def test_invalid_arguments_fail_before_any_launch():
+    """Validation is host-side: null / bad descriptors are rejected without a device."""
+    lib = icl.load_library()
+    img = icl.icl_image(0, 16, 16, 64, 1, 0)  # null data
+    taps = (ctypes.c_float * 3)(0.25, 0.5, 0.25)
+    st = lib.icl_sepconv(ctypes.byref(img), ctypes.byref(img), ctypes.cast(taps, ctypes.c_void_p), 1,
+                         ctypes.cast(taps, ctypes.c_void_p), 1, 0, 0.0, None, None, 0, None)
+    assert st == 1 and b"null" in lib.icl_last_error()
+    a = icl.icl_image(4096, 16, 16, 32, 1, 0)  # pitch < 4*width
+    st = lib.icl_nlm(ctypes.byref(a), ctypes.byref(a), 2, 5, 0.1, 1, 0.0, None, None)
+    assert st == 1 and b"pitch" in lib.icl_last_error()
+    src = icl.icl_image(4096, 16, 16, 64, 1, 0)
+    dst = icl.icl_image(4096 + 64, 16, 16, 64, 1, 0)  # overlaps src
+    st = lib.icl_harris(ctypes.byref(src), ctypes.byref(dst), 5, 0.04, 1, 0.0, None, 0.0, None, None)
+    assert st == 2
+    dst2 = icl.icl_image(1 << 20, 16, 16, 64, 1, 0)
+    st = lib.icl_nlm(ctypes.byref(src), ctypes.byref(dst2), 2, 5, 0.0, 1, 0.0, None, None)  # h = 0
+    assert st == 1
+    st = lib.icl_sepconv(ctypes.byref(src), ctypes.byref(dst2), ctypes.cast(taps, ctypes.c_void_p), 16,
+                         ctypes.cast(taps, ctypes.c_void_p), 1, 0, 0.0, None, None, 0, None)
+    assert st == 3  # radius > 15
+
+
+def test_cpu_tensors_are_rejected():
+    import torch
+    t = torch.zeros(8, 8)
+    with pytest.raises(ValueError, match="CUDA"):
+        icl.sepconv(t, t.clone(), [1.0], [1.0])
