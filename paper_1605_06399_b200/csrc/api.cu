@@ -27,6 +27,7 @@
 namespace icl {
 
 bool nlm_tiled_supported(int P, int S);
+bool nlm_boxsum_supported(int P, int S);
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -152,6 +153,7 @@ static const Variant kHarVariants[] = {
 static const Variant kNlmVariants[] = {
     {"naive_direct", K_NAIVE, 0, 0, 0},
     {"tiled_direct_32x8", K_TILED, 32, 0, 8},
+    {"boxsum_32x32", K_BOXSUM, 32, 0, 32},
 };
 
 static const Variant* table(icl_filter f, int* n) {
@@ -190,7 +192,7 @@ static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
     }
   }
   if (pc.f == ICL_FILTER_NLM && v.kind == K_TILED && !nlm_tiled_supported(pc.nlm.P, pc.nlm.S)) return false;
-  if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXSUM) return false;
+  if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXSUM && !nlm_boxsum_supported(pc.nlm.P, pc.nlm.S)) return false;
   return true;
 }
 
@@ -221,6 +223,7 @@ static int default_variant(const Prepared& pc) {
       if (!pc.a16) return 6;
       return pc.pixels < (1 << 20) ? 5 : 1;
     case ICL_FILTER_NLM:
+      if (nlm_boxsum_supported(pc.nlm.P, pc.nlm.S)) return 2;
       return nlm_tiled_supported(pc.nlm.P, pc.nlm.S) ? 1 : 0;
   }
   return 0;

@@ -5,8 +5,10 @@
 // boundary (clamp: dx(clamp(q)); constant: 0 outside), the input is read
 // with in_B.  All variants use the SAME fp32 operation order per output, so
 // they are bit-identical (and so are row-band splits):
-//   vs(c) = fma(2, in(c,r), in(c,r-1)) + in(c,r+1);  vd(c) = in(c,r+1) - in(c,r-1)
-//   dx(c) = vs(c+1) - vs(c-1);                      dy(c) = fma(2, vd(c), vd(c-1)) + vd(c+1)
+//   hd(r) = in(c+1,r) - in(c-1,r)  (r = y-1, y, y+1);  vd(c) = in(c,y+1) - in(c,y-1)
+//   dx = fma(2, hd(y), hd(y-1) + hd(y+1));            dy = fma(2, vd(x), vd(x-1) + vd(x+1))
+// (differences first: the rounding error of dx/dy is then relative to the
+// gradient terms, not to the pixel level -- DESIGN.md "Harris numerics")
 //   H*(r) = fma-chain over tx = -a..b of the products (from 0.0f)
 //   S*    = H*(y-a) + H*(y-a+1) + ... + H*(y+b)       (left to right)
 //   R     = fma(-k, tr*tr, fma(Sxx, Syy, -(Sxy*Sxy))),  tr = Sxx + Syy
@@ -39,17 +41,14 @@ __device__ __forceinline__ void sobel_B(const SrcView& s, int b, int qx, int qy,
     qx = clampi(qx, 0, s.W - 1);
     qy = clampi(qy, 0, s.Hg - 1);
   }
-  float vs[3], vd[3];
+  float hd[3], vd[3];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const float a = read_B(s, b, qx - 1 + c, qy - 1);
-    const float m = read_B(s, b, qx - 1 + c, qy);
-    const float z = read_B(s, b, qx - 1 + c, qy + 1);
-    vs[c] = __fadd_rn(__fmaf_rn(2.0f, m, a), z);
-    vd[c] = __fsub_rn(z, a);
+  for (int i = 0; i < 3; ++i) {
+    hd[i] = __fsub_rn(read_B(s, b, qx + 1, qy - 1 + i), read_B(s, b, qx - 1, qy - 1 + i));
+    vd[i] = __fsub_rn(read_B(s, b, qx - 1 + i, qy + 1), read_B(s, b, qx - 1 + i, qy - 1));
   }
-  dx = __fsub_rn(vs[2], vs[0]);
-  dy = __fadd_rn(__fmaf_rn(2.0f, vd[1], vd[0]), vd[2]);
+  dx = __fmaf_rn(2.0f, hd[1], __fadd_rn(hd[0], hd[2]));
+  dy = __fmaf_rn(2.0f, vd[1], __fadd_rn(vd[0], vd[2]));
 }
 
 // --------------------------------------------------------------------------
@@ -88,7 +87,7 @@ __global__ void __launch_bounds__(256) harris_naive(HarrisParams p) {
 // S output rows; input rows (with 4 halo columns each side) stream through an
 // NS-stage cp.async ring in shared memory.  For every H-row yy (the rows the
 // window sums touch) the thread reads the 3 input rows around
-// r = clamp(yy, 0, Hg-1) from the ring, computes vs/vd -> dx/dy -> the three
+// r = clamp(yy, 0, Hg-1) from the ring, computes hd/vd -> dx/dy -> the three
 // horizontal product sums for its 4 columns, and keeps the last B of them in
 // a register ring; each step emits one output row.  For clamp, yy outside the
 // image reuses row r's values (== dx(clamp(q))); for constant they are 0.
@@ -216,17 +215,17 @@ __global__ void __launch_bounds__(NT) harris_stream(HarrisParams p, int S) {
             }
           }
           // window column c <-> global column xc - 4 + c
-          float vs[12], vd[12];
+          float vd[12];
 #pragma unroll
-          for (int c = 3 - A; c <= 8 + BB; ++c) {
-            vs[c] = __fadd_rn(__fmaf_rn(2.0f, in[1][c], in[0][c]), in[2][c]);
-            vd[c] = __fsub_rn(in[2][c], in[0][c]);
-          }
+          for (int c = 3 - A; c <= 8 + BB; ++c) vd[c] = __fsub_rn(in[2][c], in[0][c]);
           float dx[12], dy[12];
 #pragma unroll
           for (int c = 4 - A; c <= 7 + BB; ++c) {
-            dx[c] = __fsub_rn(vs[c + 1], vs[c - 1]);
-            dy[c] = __fadd_rn(__fmaf_rn(2.0f, vd[c], vd[c - 1]), vd[c + 1]);
+            const float h0 = __fsub_rn(in[0][c + 1], in[0][c - 1]);
+            const float h1 = __fsub_rn(in[1][c + 1], in[1][c - 1]);
+            const float h2 = __fsub_rn(in[2][c + 1], in[2][c - 1]);
+            dx[c] = __fmaf_rn(2.0f, h1, __fadd_rn(h0, h2));
+            dy[c] = __fmaf_rn(2.0f, vd[c], __fadd_rn(vd[c - 1], vd[c + 1]));
           }
           if (edge) {  // per-stage boundary of dx/dy at columns outside [0, W)
             float lx = 0.0f, ly = 0.0f, rx = 0.0f, ry = 0.0f;

@@ -159,11 +159,145 @@ cudaError_t launch_nlm_tiled(const NlmCall& c, int tw, int th, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
+// --------------------------------------------------------------------------
+// Variant "boxsum<P,S>": offset-major NLM.  For a fixed offset o the patch
+// distance is a (2P+1)^2 box sum of D_o(x) = (u(x) - u(x+o))^2, which is
+// separable: d(p,o) = sum_ty H_o(p + (0,ty)),  H_o(x,y) = sum_tx D_o(x+tx, y).
+// A CTA owns a 32x32 output tile; its bounding-box input tile (halo P+S,
+// boundary applied at load) sits in shared memory.  For
+// each search row oy:
+//   phase A  every thread computes H_o for a 4-pixel row segment and ALL
+//            2S+1 ox (the candidate row is loaded once and reused across ox)
+//            into shared memory, rows -P .. 32+P of the tile;
+//   phase B  every thread owns one column x and 4 consecutive rows, sums
+//            2P+1 H rows per output (d), and accumulates w = 2^(-d*coef),
+//            num += w u(q), den += w in registers.
+// Arithmetic per (pixel, offset): 2 FSUB(+halo) + (2P+1) FFMA (H) + 2P FADD
+// (d) + FMUL + MUFU.EX2 + FFMA + FADD -- versus (2P+1)^2 x 3 flops direct.
+// d is re-associated w.r.t. the direct form (compared by tolerance).
+// --------------------------------------------------------------------------
+template <int P, int S>
+struct BoxGeom {
+  static constexpr int TW = 32, TH = 32, NT = 256;
+  static constexpr int HR = P + S;
+  static constexpr int UW0 = TW + 2 * HR;
+  static constexpr int UW = ((UW0 + 30) / 32) * 32 + 1;  // row stride == 1 (mod 32): conflict-free phase A
+  static constexpr int UH = TH + 2 * HR;
+  static constexpr int HROWS = TH + 2 * P;
+  static constexpr int NO = 2 * S + 1;
+  static constexpr int UOFF = ((UH * UW + 3) / 4) * 4;  // Hs starts 16-byte aligned
+  static constexpr size_t smem_bytes = (size_t)(UOFF + NO * HROWS * TW) * sizeof(float);
+};
+
+template <int P, int S>
+__global__ void __launch_bounds__(256) nlm_boxsum(NlmParams p) {
+  using G = BoxGeom<P, S>;
+  constexpr int TW = G::TW, TH = G::TH, HR = G::HR, UW = G::UW, UH = G::UH, HROWS = G::HROWS, NO = G::NO;
+  constexpr int PW = 2 * P + 1;
+  extern __shared__ __align__(16) float sm[];
+  float* U = sm;                 // [UH][UW]
+  float* Hs = sm + G::UOFF;      // [NO][HROWS][TW]
+  const int tid = threadIdx.x;
+  const int b = blockIdx.z;
+  const int bx = blockIdx.x * TW, bly = blockIdx.y * TH;
+  const int gy0 = p.dst.y0 + bly;
+  for (int i = tid; i < UH * (TW + 2 * HR); i += G::NT) {
+    const int r = i / (TW + 2 * HR), c = i % (TW + 2 * HR);
+    U[r * UW + c] = read_B(p.src, b, bx - HR + c, gy0 - HR + r);
+  }
+  __syncthreads();
+
+  // phase-B ownership: column xb, rows 4*run .. 4*run+3
+  const int xb = tid & 31, run = tid >> 5;
+  float num[4] = {0.f, 0.f, 0.f, 0.f}, den[4] = {0.f, 0.f, 0.f, 0.f};
+
+#pragma unroll 1
+  for (int oy = -S; oy <= S; ++oy) {
+    // ---------------- phase A: H_o rows for all ox
+    for (int item = tid; item < HROWS * (TW / 4); item += G::NT) {
+      const int yr = item / (TW / 4);   // H row index (tile row yr - P)
+      const int x = 4 * (item % (TW / 4));
+      const float* urow = U + (yr - P + HR) * UW + (x + HR - P);
+      const float* qrow = U + (yr - P + oy + HR) * UW + (x + HR - P - S);
+      float up[4 + 2 * P], uq[4 + 2 * P + 2 * S];
+#pragma unroll
+      for (int c = 0; c < 4 + 2 * P; ++c) up[c] = urow[c];
+#pragma unroll
+      for (int c = 0; c < 4 + 2 * P + 2 * S; ++c) uq[c] = qrow[c];
+#pragma unroll
+      for (int ox = 0; ox < NO; ++ox) {
+        float df[4 + 2 * P];
+#pragma unroll
+        for (int c = 0; c < 4 + 2 * P; ++c) df[c] = __fsub_rn(up[c], uq[c + ox]);
+        float h[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float a = 0.0f;
+#pragma unroll
+          for (int t = 0; t < PW; ++t) a = __fmaf_rn(df[j + t], df[j + t], a);
+          h[j] = a;
+        }
+        *reinterpret_cast<float4*>(Hs + (ox * HROWS + yr) * TW + x) = make_float4(h[0], h[1], h[2], h[3]);
+      }
+    }
+    __syncthreads();
+    // ---------------- phase B: vertical sums, weights, accumulation
+#pragma unroll
+    for (int ox = 0; ox < NO; ++ox) {
+      const float* hc = Hs + (ox * HROWS + 4 * run) * TW + xb;
+      float hv[4 + 2 * P];
+#pragma unroll
+      for (int k = 0; k < 4 + 2 * P; ++k) hv[k] = hc[k * TW];
+      const float* qc = U + (4 * run + oy + HR) * UW + (xb + ox - S + HR);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float d = hv[j];
+#pragma unroll
+        for (int t = 1; t < PW; ++t) d = __fadd_rn(d, hv[j + t]);
+        const float w = ex2_approx(-__fmul_rn(d, p.coef));
+        num[j] = __fmaf_rn(w, qc[j * UW], num[j]);
+        den[j] = __fadd_rn(den[j], w);
+      }
+    }
+    __syncthreads();
+  }
+  const int x = bx + xb;
+  if (x < p.src.W) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int ly = bly + 4 * run + j;
+      if (ly < p.dst.H) dst_row(p.dst, b, ly)[x] = __fdiv_rn(num[j], den[j]);
+    }
+  }
+}
+
+template <int P, int S>
+static cudaError_t launch_box_PS(const NlmParams& p, int batch, cudaStream_t s) {
+  using G = BoxGeom<P, S>;
+  static_assert(G::TH == 4 * (G::NT / 32), "phase B covers the tile");
+  const size_t smem = G::smem_bytes;
+  auto kern = nlm_boxsum<P, S>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grd((p.src.W + G::TW - 1) / G::TW, (p.dst.H + G::TH - 1) / G::TH, batch);
+  kern<<<grd, G::NT, smem, s>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+bool nlm_boxsum_supported(int P, int S) { return nlm_tiled_supported(P, S); }
+
 cudaError_t launch_nlm_boxsum(const NlmCall& c, int variant, cudaStream_t s) {
-  (void)c;
   (void)variant;
-  (void)s;
-  return cudaErrorNotSupported;
+  NlmParams p = make_params(c);
+  if (c.P == 2 && c.S == 5) return launch_box_PS<2, 5>(p, c.batch, s);
+  if (c.P == 1 && c.S == 3) return launch_box_PS<1, 3>(p, c.batch, s);
+  if (c.P == 3 && c.S == 7) return launch_box_PS<3, 7>(p, c.batch, s);
+  if (c.P == 2 && c.S == 3) return launch_box_PS<2, 3>(p, c.batch, s);
+  if (c.P == 1 && c.S == 5) return launch_box_PS<1, 5>(p, c.batch, s);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace icl
