@@ -11,21 +11,9 @@
 //   out = num / den
 #include "common.cuh"
 #include "internal.h"
+#include "nlm_common.cuh"
 
 namespace icl {
-
-struct NlmParams {
-  SrcView src;
-  DstView dst;
-  int P, S;
-  float coef;
-};
-
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
 // --------------------------------------------------------------------------
 // Variant "naive_direct": one logical thread per pixel, every read from
@@ -115,18 +103,8 @@ __global__ void __launch_bounds__(TW* TH) nlm_tiled(NlmParams p) {
 }
 
 // ----------------------------------------------------------------- launchers
-static NlmParams make_params(const NlmCall& c) {
-  NlmParams p;
-  p.src = c.src;
-  p.dst = c.dst;
-  p.P = c.P;
-  p.S = c.S;
-  p.coef = c.coef;
-  return p;
-}
-
 cudaError_t launch_nlm_naive(const NlmCall& c, cudaStream_t s) {
-  NlmParams p = make_params(c);
+  NlmParams p = make_nlm_params(c);
   dim3 blk(32, 8), grd((c.src.W + 31) / 32, (c.dst.H + 7) / 8, c.batch);
   nlm_naive<<<grd, blk, 0, s>>>(p);
   count_launch();
@@ -150,7 +128,7 @@ bool nlm_tiled_supported(int P, int S) {
 cudaError_t launch_nlm_tiled(const NlmCall& c, int tw, int th, cudaStream_t s) {
   (void)tw;
   (void)th;
-  NlmParams p = make_params(c);
+  NlmParams p = make_nlm_params(c);
   if (c.P == 2 && c.S == 5) return launch_tiled_PS<2, 5>(p, c.batch, s);
   if (c.P == 1 && c.S == 3) return launch_tiled_PS<1, 3>(p, c.batch, s);
   if (c.P == 3 && c.S == 7) return launch_tiled_PS<3, 7>(p, c.batch, s);
@@ -291,7 +269,7 @@ bool nlm_boxsum_supported(int P, int S) { return nlm_tiled_supported(P, S); }
 
 cudaError_t launch_nlm_boxsum(const NlmCall& c, int variant, cudaStream_t s) {
   (void)variant;
-  NlmParams p = make_params(c);
+  NlmParams p = make_nlm_params(c);
   if (c.P == 2 && c.S == 5) return launch_box_PS<2, 5>(p, c.batch, s);
   if (c.P == 1 && c.S == 3) return launch_box_PS<1, 3>(p, c.batch, s);
   if (c.P == 3 && c.S == 7) return launch_box_PS<3, 7>(p, c.batch, s);

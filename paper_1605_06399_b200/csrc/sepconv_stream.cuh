@@ -1,0 +1,200 @@
+// sepconv_stream.cuh -- the fused streaming sepconv kernel template and its
+// launch helpers; instantiated per CTA width in sepconv_nt*.cu (parallel build).
+#pragma once
+#include "common.cuh"
+#include "internal.h"
+
+namespace icl {
+
+struct SepParams {
+  SrcView src;
+  DstView dst;
+  int rx, ry;
+  float fx[2 * kMaxRadius + 1];
+  float gy[2 * kMaxRadius + 1];
+};
+
+// --------------------------------------------------------------------------
+// Variant family "stream<R,NT,VEC>": fused single pass (A20).  A CTA owns a
+// column strip of TW = 4*NT pixels and a segment of S output rows.  It
+// streams the S + 2R input rows of its strip (plus HP halo columns on each
+// side) top-down through an NS-stage cp.async ring in shared memory (the
+// paper's "local memory" staging, Fig. 5, made a pipeline);
+// each thread computes the row pass for its 4 columns ("blocked" mapping,
+// float4) into a register ring of 2R+1 intermediate rows and emits one
+// output row per input row.  HBM traffic ~= 8 B/px + vertical halo 2R/S.
+// VEC=4: 16-byte cp.async (needs 16B-aligned data/pitch); VEC=1: 4-byte.
+// --------------------------------------------------------------------------
+template <int R>
+struct SepGeom {
+  static constexpr int HP = ((R + 3) / 4) * 4;  // halo columns, padded to float4
+  static constexpr int P = 2 * R + 1;           // ring depth
+};
+
+constexpr int kSepStages = 8;  // cp.async ring depth (rows in flight per CTA = NS-1)
+
+template <int R, int NT, int VEC>
+__global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
+  constexpr int NS = kSepStages;
+  constexpr int HP = SepGeom<R>::HP;
+  constexpr int P = SepGeom<R>::P;
+  constexpr int TW = 4 * NT;
+  constexpr int ROWLEN = TW + 2 * HP;
+  constexpr int NSLOT = ROWLEN / 4;
+  extern __shared__ __align__(16) float smem[];
+
+  const int tid = threadIdx.x;
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * TW;
+  const int ly0 = blockIdx.y * S;
+  const int ly1 = min(ly0 + S, p.dst.H);
+  const int g0 = p.dst.y0 + ly0;  // first output global row
+  const int NI = (ly1 - ly0) + 2 * R;
+  const int W = p.src.W;
+  const int Hg = p.src.Hg;
+  const bool clampb = p.src.border == kBorderClamp;
+  const bool edge = (x0 - HP < 0) || (x0 + TW + HP > W);
+
+  // Issue the loads of input row k (global row g0 - R + k) into its stage.
+  auto load_row = [&](int k) {
+    if (k >= NI) return;
+    float* st = smem + (k % NS) * ROWLEN;
+    int gi = g0 - R + k;
+    if (gi < 0 || gi >= Hg) {
+      if (!clampb) {  // constant border: a full row of c
+        for (int s = tid; s < NSLOT; s += NT)
+          reinterpret_cast<float4*>(st)[s] = make_float4(p.src.cval, p.src.cval, p.src.cval, p.src.cval);
+        return;
+      }
+      gi = clampi(gi, 0, Hg - 1);
+    }
+    const float* row = src_row(p.src, b, gi);
+    for (int s = tid; s < NSLOT; s += NT) {
+      const int xs = x0 - HP + 4 * s;
+      if (VEC == 4) {
+        int nb = (xs < 0) ? 0 : min(max(W - xs, 0), 4) * 4;
+        cp_async16(st + 4 * s, nb ? (const void*)(row + xs) : (const void*)row, nb);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int xe = xs + e;
+          const bool in = xe >= 0 && xe < W;
+          cp_async4(st + 4 * s + e, in ? (const void*)(row + xe) : (const void*)row, in ? 4 : 0);
+        }
+      }
+    }
+  };
+
+  // Prologue: NS-1 rows in flight.
+  for (int k = 0; k < NS - 1; ++k) {
+    load_row(k);
+    cp_async_commit();
+  }
+
+  float4 ring[P];
+  const int xc = x0 + 4 * tid;  // first of this thread's 4 columns
+
+  for (int kb = 0; kb < NI; kb += P) {
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      const int k = kb + u;
+      if (k < NI) {
+        cp_async_wait<NS - 2>();  // groups 0..k complete => row k has landed
+        __syncthreads();
+        float* st = smem + (k % NS) * ROWLEN;
+        if (edge) {
+          // Boundary fix-up of halo columns outside [0, W) (Fig. 3).
+          const float vl = st[HP - x0 >= 0 && HP - x0 < ROWLEN ? HP - x0 : 0];
+          const int ir = (W - 1) - x0 + HP;
+          const float vr = st[ir >= 0 && ir < ROWLEN ? ir : 0];
+          __syncthreads();
+          for (int s = tid; s < NSLOT; s += NT) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int xe = x0 - HP + 4 * s + e;
+              if (xe < 0) st[4 * s + e] = clampb ? vl : p.src.cval;
+              else if (xe >= W) st[4 * s + e] = clampb ? vr : p.src.cval;
+            }
+          }
+          __syncthreads();
+        }
+        load_row(k + NS - 1);
+        cp_async_commit();
+        // Row pass for 4 columns: window st[4*tid .. 4*tid + 4 + 2HP).
+        float v[4 + 2 * HP];
+#pragma unroll
+        for (int q = 0; q < (4 + 2 * HP) / 4; ++q) {
+          const float4 w = reinterpret_cast<const float4*>(st + 4 * tid)[q];
+          v[4 * q] = w.x; v[4 * q + 1] = w.y; v[4 * q + 2] = w.z; v[4 * q + 3] = w.w;
+        }
+        float t[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float a = 0.0f;
+#pragma unroll
+          for (int i = 0; i < P; ++i) a = __fmaf_rn(p.fx[i], v[HP - R + c + i], a);
+          t[c] = a;
+        }
+        ring[u] = make_float4(t[0], t[1], t[2], t[3]);
+        if (k >= 2 * R) {
+          float o[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+          for (int j = 0; j < P; ++j) {
+            const float4 rr = ring[(u + 1 + j) % P];
+            o[0] = __fmaf_rn(p.gy[j], rr.x, o[0]);
+            o[1] = __fmaf_rn(p.gy[j], rr.y, o[1]);
+            o[2] = __fmaf_rn(p.gy[j], rr.z, o[2]);
+            o[3] = __fmaf_rn(p.gy[j], rr.w, o[3]);
+          }
+          const int ly = ly0 + k - 2 * R;
+          float* drow = dst_row(p.dst, b, ly);
+          if (VEC == 4 && xc + 3 < W) {
+            st_cs4(drow + xc, make_float4(o[0], o[1], o[2], o[3]));
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (xc + c < W) drow[xc + c] = o[c];
+          }
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+// Pipeline invariant: before iteration k, NS-1+k groups are committed (one per
+// row, empty groups past the end), so wait_group(NS-2) completes row k while
+// rows k+1..k+NS-2 stay in flight; row k+NS-1 is issued into the stage row
+// k-1 used, which every thread released at this iteration's barrier.
+
+template <int R, int NT, int VEC>
+static inline cudaError_t launch_stream_R(const SepParams& p, int batch, int S, cudaStream_t s) {
+  constexpr int ROWLEN = 4 * NT + 2 * SepGeom<R>::HP;
+  const size_t smem = (size_t)kSepStages * ROWLEN * sizeof(float);
+  auto kern = sep_stream<R, NT, VEC>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grd((p.src.W + 4 * NT - 1) / (4 * NT), (p.dst.H + S - 1) / S, batch);
+  kern<<<grd, NT, smem, s>>>(p, S);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int NT, int VEC>
+cudaError_t dispatch_stream(const SepParams& p, int R, int batch, int S, cudaStream_t s) {
+  switch (R) {
+#define ICL_SEP_CASE(r) \
+  case r:               \
+    return launch_stream_R<r, NT, VEC>(p, batch, S, s);
+    ICL_SEP_CASE(0) ICL_SEP_CASE(1) ICL_SEP_CASE(2) ICL_SEP_CASE(3) ICL_SEP_CASE(4) ICL_SEP_CASE(5)
+    ICL_SEP_CASE(6) ICL_SEP_CASE(7) ICL_SEP_CASE(8) ICL_SEP_CASE(9) ICL_SEP_CASE(10) ICL_SEP_CASE(11)
+    ICL_SEP_CASE(12) ICL_SEP_CASE(13) ICL_SEP_CASE(14) ICL_SEP_CASE(15)
+#undef ICL_SEP_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+
+}  // namespace icl
