@@ -65,6 +65,14 @@ def ncu_traffic():
         return {}
 
 
+def _traffic(t, f, px):
+    """ncu DRAM bytes per launch of this bench's launch size (from profiles/ncu_traffic.json)."""
+    e = t.get(f)
+    if not e or "bytes_per_px" not in e:
+        return None
+    return e["bytes_per_px"] * px
+
+
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     """SM clock + throttle reasons sampled (NVML, every 10 ms) during the timed region."""
@@ -373,13 +381,13 @@ def run_suite(args):
         "nlm": {"bound": "alu", "achieved": nlm_flop_px * px_rank / (med["nlm"] * 1e-3) / 1e12,
                 "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "flop_per_px": nlm_flop_px,
                 "formulation": nlm_kind, "kernel": variants["nlm"],
-                "traffic": traffic.get("nlm")},
+                "traffic": _traffic(traffic, "nlm", px_rank)},
         "sepconv": {"bound": "hbm", "achieved": SEP_BYTES_PER_PX * px_rank / (med["sepconv"] * 1e-3) / 1e9,
                     "peak": hbm, "unit": "GB/s", "kernel": variants["sepconv"],
-                    "traffic": traffic.get("sepconv")},
+                    "traffic": _traffic(traffic, "sepconv", px_rank)},
         "harris": {"bound": "hbm", "achieved": HARRIS_BYTES_PER_PX * px_rank / (med["harris"] * 1e-3) / 1e9,
                    "peak": hbm, "unit": "GB/s", "kernel": variants["harris"],
-                   "traffic": traffic.get("harris")},
+                   "traffic": _traffic(traffic, "harris", px_rank)},
     }
     for r in roof.values():
         r["frac"] = r["achieved"] / r["peak"]
