@@ -30,6 +30,7 @@ bool nlm_tiled_supported(int P, int S);
 bool nlm_boxsum_supported(int P, int S);
 bool nlm_ox_supported(int P, int S);
 bool nlm_ws_supported(int P, int S);
+bool nlm_r8_supported(int P, int S);
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -132,7 +133,7 @@ static icl_status make_views(const icl_image* src, const icl_image* dst, const i
 }
 
 // ------------------------------------------------------------------ variants
-enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXOX, K_BOXWS };
+enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXOX, K_BOXWS, K_BOXR8 };
 struct Variant {
   const char* name;
   Kind kind;
@@ -158,6 +159,7 @@ static const Variant kNlmVariants[] = {
     {"boxsum_32x32", K_BOXSUM, 32, 0, 32},
     {"boxsum_oxwarp", K_BOXOX, 0, 0, 0},
     {"boxsum_ws", K_BOXWS, 0, 0, 0},
+    {"boxsum_r8", K_BOXR8, 0, 0, 0},
 };
 
 static const Variant* table(icl_filter f, int* n) {
@@ -199,6 +201,7 @@ static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXSUM && !nlm_boxsum_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXOX && !nlm_ox_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXWS && !nlm_ws_supported(pc.nlm.P, pc.nlm.S)) return false;
+  if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXR8 && !nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return false;
   return true;
 }
 
@@ -216,6 +219,7 @@ static cudaError_t run_variant(const Prepared& pc, const Variant& v, cudaStream_
       if (v.kind == K_TILED) return launch_nlm_tiled(pc.nlm, v.nt, v.S, s);
       if (v.kind == K_BOXOX) return launch_nlm_ox(pc.nlm, s);
       if (v.kind == K_BOXWS) return launch_nlm_ws(pc.nlm, s);
+      if (v.kind == K_BOXR8) return launch_nlm_r8(pc.nlm, s);
       return launch_nlm_boxsum(pc.nlm, 0, s);
   }
   return cudaErrorInvalidValue;
@@ -231,7 +235,7 @@ static int default_variant(const Prepared& pc) {
       if (!pc.a16) return 6;
       return pc.pixels < (1 << 20) ? 5 : 1;
     case ICL_FILTER_NLM:
-      if (nlm_ws_supported(pc.nlm.P, pc.nlm.S)) return 4;
+      if (nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return 5;
       if (nlm_ox_supported(pc.nlm.P, pc.nlm.S)) return 3;
       if (nlm_boxsum_supported(pc.nlm.P, pc.nlm.S)) return 2;
       return nlm_tiled_supported(pc.nlm.P, pc.nlm.S) ? 1 : 0;
