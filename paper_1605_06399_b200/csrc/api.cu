@@ -28,8 +28,6 @@ namespace icl {
 
 bool nlm_tiled_supported(int P, int S);
 bool nlm_boxsum_supported(int P, int S);
-bool nlm_ox_supported(int P, int S);
-bool nlm_ws_supported(int P, int S);
 bool nlm_r8_supported(int P, int S);
 
 static std::atomic<uint64_t> g_launches{0};
@@ -133,7 +131,7 @@ static icl_status make_views(const icl_image* src, const icl_image* dst, const i
 }
 
 // ------------------------------------------------------------------ variants
-enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXOX, K_BOXWS, K_BOXR8 };
+enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK };
 struct Variant {
   const char* name;
   Kind kind;
@@ -141,11 +139,21 @@ struct Variant {
 };
 
 static const Variant kSepVariants[] = {
-    {"naive_direct", K_NAIVE, 0, 0, 0},           {"naive_2pass", K_TWOPASS, 0, 0, 0},
-    {"stream_nt64_s64_v4", K_STREAM, 64, 4, 64},  {"stream_nt32_s32_v4", K_STREAM, 32, 4, 32},
-    {"stream_nt128_s64_v4", K_STREAM, 128, 4, 64}, {"stream_nt64_s128_v4", K_STREAM, 64, 4, 128},
-    {"stream_nt32_s16_v4", K_STREAM, 32, 4, 16},  {"stream_nt64_s256_v4", K_STREAM, 64, 4, 256},
+    {"naive_direct", K_NAIVE, 0, 0, 0},
+    {"naive_2pass", K_TWOPASS, 0, 0, 0},
+    {"stream_nt64_s16_v4", K_STREAM, 64, 4, 16},
+    {"stream_nt32_s16_v4", K_STREAM, 32, 4, 16},
+    {"stream_nt128_s16_v4", K_STREAM, 128, 4, 16},
+    {"stream_nt32_s8_v4", K_STREAM, 32, 4, 8},
+    {"stream_nt32_s32_v4", K_STREAM, 32, 4, 32},
+    {"stream_nt64_s32_v4", K_STREAM, 64, 4, 32},
+    {"stream_nt64_s64_v4", K_STREAM, 64, 4, 64},
+    {"stream_nt128_s64_v4", K_STREAM, 128, 4, 64},
+    {"stream_nt256_s16_v4", K_STREAM, 256, 4, 16},
     {"stream_nt64_s64_v1", K_STREAM, 64, 1, 64},
+    {"stream_nt64_s16_v1", K_STREAM, 64, 1, 16},
+    {"bulk_nt128_s64", K_BULK, 128, 4, 64},
+    {"bulk_nt64_s64", K_BULK, 64, 4, 64},
 };
 static const Variant kHarVariants[] = {
     {"naive_direct", K_NAIVE, 0, 0, 0},           {"stream_nt64_s64_v4", K_STREAM, 64, 4, 64},
@@ -157,8 +165,6 @@ static const Variant kNlmVariants[] = {
     {"naive_direct", K_NAIVE, 0, 0, 0},
     {"tiled_direct_32x8", K_TILED, 32, 0, 8},
     {"boxsum_32x32", K_BOXSUM, 32, 0, 32},
-    {"boxsum_oxwarp", K_BOXOX, 0, 0, 0},
-    {"boxsum_ws", K_BOXWS, 0, 0, 0},
     {"boxsum_r8", K_BOXR8, 0, 0, 0},
 };
 
@@ -189,7 +195,10 @@ struct Prepared {
 
 static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
   *why = ICL_ERR_UNSUPPORTED;
-  if (v.kind == K_STREAM && v.vec == 4 && !pc.a16) return false;
+  if ((v.kind == K_STREAM || v.kind == K_BULK) && v.vec == 4 && !pc.a16) return false;
+  if (pc.f == ICL_FILTER_SEPCONV && v.kind == K_STREAM &&
+      sep_stream_smem_bytes(v.nt, pc.sep.rx > pc.sep.ry ? pc.sep.rx : pc.sep.ry) > 227 * 1024)
+    return false;
   if (pc.f == ICL_FILTER_SEPCONV && v.kind == K_TWOPASS) {
     const size_t need = sep_2pass_workspace(pc.sep.src.W, pc.sep.dst.H, pc.sep.batch, pc.sep.ry);
     if (!pc.sep.workspace || pc.sep.workspace_bytes < need) {
@@ -199,8 +208,6 @@ static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
   }
   if (pc.f == ICL_FILTER_NLM && v.kind == K_TILED && !nlm_tiled_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXSUM && !nlm_boxsum_supported(pc.nlm.P, pc.nlm.S)) return false;
-  if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXOX && !nlm_ox_supported(pc.nlm.P, pc.nlm.S)) return false;
-  if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXWS && !nlm_ws_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXR8 && !nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return false;
   return true;
 }
@@ -210,6 +217,7 @@ static cudaError_t run_variant(const Prepared& pc, const Variant& v, cudaStream_
     case ICL_FILTER_SEPCONV:
       if (v.kind == K_NAIVE) return launch_sep_naive_direct(pc.sep, s);
       if (v.kind == K_TWOPASS) return launch_sep_naive_2pass(pc.sep, s);
+      if (v.kind == K_BULK) return launch_sep_bulk(pc.sep, v.nt, v.S, s);
       return launch_sep_stream(pc.sep, v.nt, v.vec, v.S, s);
     case ICL_FILTER_HARRIS:
       if (v.kind == K_NAIVE) return launch_harris_naive(pc.har, s);
@@ -217,28 +225,34 @@ static cudaError_t run_variant(const Prepared& pc, const Variant& v, cudaStream_
     case ICL_FILTER_NLM:
       if (v.kind == K_NAIVE) return launch_nlm_naive(pc.nlm, s);
       if (v.kind == K_TILED) return launch_nlm_tiled(pc.nlm, v.nt, v.S, s);
-      if (v.kind == K_BOXOX) return launch_nlm_ox(pc.nlm, s);
-      if (v.kind == K_BOXWS) return launch_nlm_ws(pc.nlm, s);
       if (v.kind == K_BOXR8) return launch_nlm_r8(pc.nlm, s);
       return launch_nlm_boxsum(pc.nlm, 0, s);
   }
   return cudaErrorInvalidValue;
 }
 
-// Default (untuned) choice: a heuristic per filter.
+static int variant_id(icl_filter f, const char* name) {
+  int n;
+  const Variant* vt = table(f, &n);
+  for (int i = 0; i < n; ++i)
+    if (!strcmp(vt[i].name, name)) return i;
+  return 0;
+}
+
+// Default (untuned) choice: a heuristic per filter (the measured winners of
+// tools/variant_sweep.py on B200 for large images; small images take the
+// narrowest CTA for more parallelism).
 static int default_variant(const Prepared& pc) {
   switch (pc.f) {
     case ICL_FILTER_SEPCONV:
-      if (!pc.a16) return 8;
-      return pc.pixels < (1 << 20) ? 6 : 2;
+      if (!pc.a16) return variant_id(pc.f, pc.pixels < (1 << 20) ? "stream_nt64_s16_v1" : "stream_nt64_s64_v1");
+      return variant_id(pc.f, pc.pixels < (1 << 20) ? "stream_nt32_s8_v4" : "stream_nt64_s16_v4");
     case ICL_FILTER_HARRIS:
-      if (!pc.a16) return 6;
-      return pc.pixels < (1 << 20) ? 5 : 1;
+      if (!pc.a16) return variant_id(pc.f, "stream_nt64_s64_v1");
+      return variant_id(pc.f, pc.pixels < (1 << 20) ? "stream_nt32_s16_v4" : "stream_nt64_s64_v4");
     case ICL_FILTER_NLM:
-      if (nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return 5;
-      if (nlm_ox_supported(pc.nlm.P, pc.nlm.S)) return 3;
-      if (nlm_boxsum_supported(pc.nlm.P, pc.nlm.S)) return 2;
-      return nlm_tiled_supported(pc.nlm.P, pc.nlm.S) ? 1 : 0;
+      if (nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return variant_id(pc.f, "boxsum_r8");
+      return nlm_tiled_supported(pc.nlm.P, pc.nlm.S) ? variant_id(pc.f, "tiled_direct_32x8") : 0;
   }
   return 0;
 }

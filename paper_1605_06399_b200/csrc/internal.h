@@ -47,6 +47,8 @@ cudaError_t launch_sep_naive_direct(const SepCall& c, cudaStream_t s);
 cudaError_t launch_sep_naive_2pass(const SepCall& c, cudaStream_t s);
 size_t sep_2pass_workspace(int64_t W, int64_t H, int64_t batch, int ry);
 cudaError_t launch_sep_stream(const SepCall& c, int nt, int vec, int S, cudaStream_t s);
+size_t sep_stream_smem_bytes(int nt, int R);
+cudaError_t launch_sep_bulk(const SepCall& c, int nt, int S, cudaStream_t s);
 
 // harris
 cudaError_t launch_harris_naive(const HarrisCall& c, cudaStream_t s);
@@ -56,8 +58,6 @@ cudaError_t launch_harris_stream(const HarrisCall& c, int nt, int vec, int S, cu
 cudaError_t launch_nlm_naive(const NlmCall& c, cudaStream_t s);
 cudaError_t launch_nlm_tiled(const NlmCall& c, int tw, int th, cudaStream_t s);
 cudaError_t launch_nlm_boxsum(const NlmCall& c, int variant, cudaStream_t s);
-cudaError_t launch_nlm_ox(const NlmCall& c, cudaStream_t s);
-cudaError_t launch_nlm_ws(const NlmCall& c, cudaStream_t s);
 cudaError_t launch_nlm_r8(const NlmCall& c, cudaStream_t s);
 
 // synthetic inputs

@@ -66,26 +66,8 @@ __global__ void __launch_bounds__(256) sep_col_pass(SepParams p, const float* __
 }
 
 // ----------------------------------------------------------------- launchers
-static SepParams make_params(const SepCall& c, bool pad) {
-  SepParams p;
-  p.src = c.src;
-  p.dst = c.dst;
-  p.rx = c.rx;
-  p.ry = c.ry;
-  for (int i = 0; i < 2 * kMaxRadius + 1; ++i) { p.fx[i] = 0.0f; p.gy[i] = 0.0f; }
-  if (pad) {
-    const int R = c.rx > c.ry ? c.rx : c.ry;
-    for (int i = 0; i < 2 * c.rx + 1; ++i) p.fx[R - c.rx + i] = c.fx[i];
-    for (int j = 0; j < 2 * c.ry + 1; ++j) p.gy[R - c.ry + j] = c.gy[j];
-  } else {
-    for (int i = 0; i < 2 * c.rx + 1; ++i) p.fx[i] = c.fx[i];
-    for (int j = 0; j < 2 * c.ry + 1; ++j) p.gy[j] = c.gy[j];
-  }
-  return p;
-}
-
 cudaError_t launch_sep_naive_direct(const SepCall& c, cudaStream_t s) {
-  SepParams p = make_params(c, false);
+  SepParams p = make_sep_params(c, false);
   dim3 blk(32, 8), grd((c.src.W + 31) / 32, (c.dst.H + 7) / 8, c.batch);
   sep_naive_direct<<<grd, blk, 0, s>>>(p);
   count_launch();
@@ -98,7 +80,7 @@ size_t sep_2pass_workspace(int64_t W, int64_t H, int64_t batch, int ry) {
 }
 
 cudaError_t launch_sep_naive_2pass(const SepCall& c, cudaStream_t s) {
-  SepParams p = make_params(c, false);
+  SepParams p = make_sep_params(c, false);
   const int64_t tpitch = ((int64_t)c.src.W + 31) / 32 * 32;
   const int trows = c.dst.H + 2 * c.ry;
   const int64_t tbstride = tpitch * trows;
@@ -119,14 +101,38 @@ extern template cudaError_t dispatch_stream<32, 4>(const SepParams&, int, int, i
 extern template cudaError_t dispatch_stream<64, 4>(const SepParams&, int, int, int, cudaStream_t);
 extern template cudaError_t dispatch_stream<128, 4>(const SepParams&, int, int, int, cudaStream_t);
 extern template cudaError_t dispatch_stream<64, 1>(const SepParams&, int, int, int, cudaStream_t);
+extern template cudaError_t dispatch_stream<256, 4>(const SepParams&, int, int, int, cudaStream_t);
+template <int NT>
+cudaError_t dispatch_bulk(const SepParams& p, int R, int batch, int S, cudaStream_t s);
+extern template cudaError_t dispatch_bulk<32>(const SepParams&, int, int, int, cudaStream_t);
+extern template cudaError_t dispatch_bulk<64>(const SepParams&, int, int, int, cudaStream_t);
+extern template cudaError_t dispatch_bulk<128>(const SepParams&, int, int, int, cudaStream_t);
+
+cudaError_t launch_sep_bulk(const SepCall& c, int nt, int S, cudaStream_t s) {
+  SepParams p = make_sep_params(c, true);
+  const int R = c.rx > c.ry ? c.rx : c.ry;
+  if (nt == 32) return dispatch_bulk<32>(p, R, c.batch, S, s);
+  if (nt == 64) return dispatch_bulk<64>(p, R, c.batch, S, s);
+  if (nt == 128) return dispatch_bulk<128>(p, R, c.batch, S, s);
+  return cudaErrorInvalidValue;
+}
+
+size_t sep_stream_smem_bytes(int nt, int R) {
+  const int P = 2 * R + 1;
+  const int RB = P * ((4 + P - 1) / P);
+  const int NSR = RB * (RB <= 8 ? 3 : 2);
+  const int HP = ((R + 3) / 4) * 4;
+  return (size_t)NSR * (size_t)(4 * nt + 2 * HP) * sizeof(float);
+}
 
 cudaError_t launch_sep_stream(const SepCall& c, int nt, int vec, int S, cudaStream_t s) {
-  SepParams p = make_params(c, true);
+  SepParams p = make_sep_params(c, true);
   const int R = c.rx > c.ry ? c.rx : c.ry;
   if (vec == 4) {
     if (nt == 32) return dispatch_stream<32, 4>(p, R, c.batch, S, s);
     if (nt == 64) return dispatch_stream<64, 4>(p, R, c.batch, S, s);
     if (nt == 128) return dispatch_stream<128, 4>(p, R, c.batch, S, s);
+    if (nt == 256) return dispatch_stream<256, 4>(p, R, c.batch, S, s);
   } else if (vec == 1 && nt == 64) {
     return dispatch_stream<64, 1>(p, R, c.batch, S, s);
   }

@@ -1,0 +1,7 @@
+// sepconv_nt256_v4.cu -- instantiation of the streaming sepconv kernel for
+// NT=256 threads per CTA, VEC=4 (separate TU for a parallel build).
+#include "sepconv_stream.cuh"
+
+namespace icl {
+template cudaError_t dispatch_stream<256, 4>(const SepParams& p, int R, int batch, int S, cudaStream_t s);
+}  // namespace icl

@@ -31,13 +31,21 @@ struct SepGeom {
   static constexpr int P = 2 * R + 1;           // ring depth
 };
 
-constexpr int kSepStages = 8;  // cp.async ring depth (rows in flight per CTA = NS-1)
+// Rows per pipeline block (a multiple of the ring period P, >= 4) and blocks
+// of shared memory (NBLK-1 blocks in flight while one is computed).
+template <int R>
+struct StreamGeom {
+  static constexpr int P = SepGeom<R>::P;
+  static constexpr int RB = P * ((4 + P - 1) / P);
+  static constexpr int NBLK = RB <= 8 ? 3 : 2;
+  static constexpr int NSR = RB * NBLK;  // rows of shared memory
+};
 
 template <int R, int NT, int VEC>
 __global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
-  constexpr int NS = kSepStages;
   constexpr int HP = SepGeom<R>::HP;
   constexpr int P = SepGeom<R>::P;
+  constexpr int RB = StreamGeom<R>::RB, NBLK = StreamGeom<R>::NBLK, NSR = StreamGeom<R>::NSR;
   constexpr int TW = 4 * NT;
   constexpr int ROWLEN = TW + 2 * HP;
   constexpr int NSLOT = ROWLEN / 4;
@@ -48,79 +56,113 @@ __global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
   const int x0 = blockIdx.x * TW;
   const int ly0 = blockIdx.y * S;
   const int ly1 = min(ly0 + S, p.dst.H);
-  const int g0 = p.dst.y0 + ly0;  // first output global row
+  const int g0 = p.dst.y0 + ly0;
   const int NI = (ly1 - ly0) + 2 * R;
+  const int NB = (NI + RB - 1) / RB;
   const int W = p.src.W;
   const int Hg = p.src.Hg;
   const bool clampb = p.src.border == kBorderClamp;
   const bool edge = (x0 - HP < 0) || (x0 + TW + HP > W);
+  const bool vint = (g0 - R >= 0) && (g0 - R + NI <= Hg);
+  const bool fast = !edge && vint && VEC == 4;  // no boundary work anywhere in this CTA
 
-  // Issue the loads of input row k (global row g0 - R + k) into its stage.
-  auto load_row = [&](int k) {
-    if (k >= NI) return;
-    float* st = smem + (k % NS) * ROWLEN;
-    int gi = g0 - R + k;
-    if (gi < 0 || gi >= Hg) {
-      if (!clampb) {  // constant border: a full row of c
-        for (int s = tid; s < NSLOT; s += NT)
-          reinterpret_cast<float4*>(st)[s] = make_float4(p.src.cval, p.src.cval, p.src.cval, p.src.cval);
-        return;
+  // fast-path copy descriptors (columns never change across rows)
+  const float* row0 = src_row(p.src, b, fast ? g0 - R : 0);  // row of input k = 0
+  const int s1 = tid + NT;
+  const int c0 = x0 - HP + 4 * tid, c1 = x0 - HP + 4 * s1;
+
+  // Issue the loads of rows [kb, kb + RB) into their smem rows (k % NSR).
+  auto load_block = [&](int kb) {
+    if (fast) {
+#pragma unroll
+      for (int u = 0; u < RB; ++u) {
+        const int k = kb + u;
+        if (k < NI) {
+          float* st = smem + (k % NSR) * ROWLEN;
+          const float* row = row0 + (int64_t)k * (p.src.pitch >> 2);
+          cp_async16(st + 4 * tid, row + c0, 16);
+          if (s1 < NSLOT) cp_async16(st + 4 * s1, row + c1, 16);
+        }
       }
-      gi = clampi(gi, 0, Hg - 1);
+      return;
     }
-    const float* row = src_row(p.src, b, gi);
-    for (int s = tid; s < NSLOT; s += NT) {
-      const int xs = x0 - HP + 4 * s;
-      if (VEC == 4) {
-        int nb = (xs < 0) ? 0 : min(max(W - xs, 0), 4) * 4;
-        cp_async16(st + 4 * s, nb ? (const void*)(row + xs) : (const void*)row, nb);
-      } else {
+    for (int u = 0; u < RB; ++u) {
+      const int k = kb + u;
+      if (k >= NI) break;
+      float* st = smem + (k % NSR) * ROWLEN;
+      int gi = g0 - R + k;
+      if (gi < 0 || gi >= Hg) {
+        if (!clampb) {  // constant border: a full row of c
+          for (int s = tid; s < NSLOT; s += NT)
+            reinterpret_cast<float4*>(st)[s] = make_float4(p.src.cval, p.src.cval, p.src.cval, p.src.cval);
+          continue;
+        }
+        gi = clampi(gi, 0, Hg - 1);
+      }
+      const float* row = src_row(p.src, b, gi);
+      for (int s = tid; s < NSLOT; s += NT) {
+        const int xs = x0 - HP + 4 * s;
+        if (VEC == 4) {
+          int nb = (xs < 0) ? 0 : min(max(W - xs, 0), 4) * 4;
+          cp_async16(st + 4 * s, nb ? (const void*)(row + xs) : (const void*)row, nb);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int xe = xs + e;
+            const bool in = xe >= 0 && xe < W;
+            cp_async4(st + 4 * s + e, in ? (const void*)(row + xe) : (const void*)row, in ? 4 : 0);
+          }
+        }
+      }
+    }
+  };
+  // Boundary fix-up of the halo columns outside [0, W) of rows [kb, kb+RB).
+  auto fix_block = [&](int kb) {
+    const int il = HP - x0;
+    const int ir = (W - 1) - x0 + HP;
+    for (int u = 0; u < RB; ++u) {
+      const int k = kb + u;
+      if (k >= NI) break;
+      float* st = smem + (k % NSR) * ROWLEN;
+      const float vl = st[il >= 0 && il < ROWLEN ? il : 0];
+      const float vr = st[ir >= 0 && ir < ROWLEN ? ir : 0];
+      for (int s = tid; s < NSLOT; s += NT) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int xe = xs + e;
-          const bool in = xe >= 0 && xe < W;
-          cp_async4(st + 4 * s + e, in ? (const void*)(row + xe) : (const void*)row, in ? 4 : 0);
+          const int xe = x0 - HP + 4 * s + e;
+          if (xe < 0) st[4 * s + e] = clampb ? vl : p.src.cval;
+          else if (xe >= W) st[4 * s + e] = clampb ? vr : p.src.cval;
         }
       }
     }
   };
 
-  // Prologue: NS-1 rows in flight.
-  for (int k = 0; k < NS - 1; ++k) {
-    load_row(k);
+  // Prologue: blocks 0 .. NBLK-2 in flight (one cp.async group per block).
+  for (int i = 0; i < NBLK - 1; ++i) {
+    if (i < NB) load_block(i * RB);
     cp_async_commit();
   }
 
   float4 ring[P];
-  const int xc = x0 + 4 * tid;  // first of this thread's 4 columns
+  const int xc = x0 + 4 * tid;
+  float* drow = dst_row(p.dst, b, ly0);
+  const int64_t dpitch = p.dst.pitch >> 2;
 
-  for (int kb = 0; kb < NI; kb += P) {
+#pragma unroll 1
+  for (int i = 0; i < NB; ++i) {
+    cp_async_wait<NBLK - 2>();  // block i complete
+    __syncthreads();            // ... for every thread; block i-1's rows are free
+    if (edge) {
+      fix_block(i * RB);
+      __syncthreads();
+    }
+    if (i + NBLK - 1 < NB) load_block((i + NBLK - 1) * RB);
+    cp_async_commit();
 #pragma unroll
-    for (int u = 0; u < P; ++u) {
-      const int k = kb + u;
+    for (int u = 0; u < RB; ++u) {
+      const int k = i * RB + u;
       if (k < NI) {
-        cp_async_wait<NS - 2>();  // groups 0..k complete => row k has landed
-        __syncthreads();
-        float* st = smem + (k % NS) * ROWLEN;
-        if (edge) {
-          // Boundary fix-up of halo columns outside [0, W) (Fig. 3).
-          const float vl = st[HP - x0 >= 0 && HP - x0 < ROWLEN ? HP - x0 : 0];
-          const int ir = (W - 1) - x0 + HP;
-          const float vr = st[ir >= 0 && ir < ROWLEN ? ir : 0];
-          __syncthreads();
-          for (int s = tid; s < NSLOT; s += NT) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int xe = x0 - HP + 4 * s + e;
-              if (xe < 0) st[4 * s + e] = clampb ? vl : p.src.cval;
-              else if (xe >= W) st[4 * s + e] = clampb ? vr : p.src.cval;
-            }
-          }
-          __syncthreads();
-        }
-        load_row(k + NS - 1);
-        cp_async_commit();
-        // Row pass for 4 columns: window st[4*tid .. 4*tid + 4 + 2HP).
+        const float* st = smem + (k % NSR) * ROWLEN;
         float v[4 + 2 * HP];
 #pragma unroll
         for (int q = 0; q < (4 + 2 * HP) / 4; ++q) {
@@ -132,10 +174,10 @@ __global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
         for (int c = 0; c < 4; ++c) {
           float a = 0.0f;
 #pragma unroll
-          for (int i = 0; i < P; ++i) a = __fmaf_rn(p.fx[i], v[HP - R + c + i], a);
+          for (int ii = 0; ii < P; ++ii) a = __fmaf_rn(p.fx[ii], v[HP - R + c + ii], a);
           t[c] = a;
         }
-        ring[u] = make_float4(t[0], t[1], t[2], t[3]);
+        ring[u % P] = make_float4(t[0], t[1], t[2], t[3]);
         if (k >= 2 * R) {
           float o[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
@@ -146,8 +188,6 @@ __global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
             o[2] = __fmaf_rn(p.gy[j], rr.z, o[2]);
             o[3] = __fmaf_rn(p.gy[j], rr.w, o[3]);
           }
-          const int ly = ly0 + k - 2 * R;
-          float* drow = dst_row(p.dst, b, ly);
           if (VEC == 4 && xc + 3 < W) {
             st_cs4(drow + xc, make_float4(o[0], o[1], o[2], o[3]));
           } else {
@@ -155,21 +195,23 @@ __global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
             for (int c = 0; c < 4; ++c)
               if (xc + c < W) drow[xc + c] = o[c];
           }
+          drow += dpitch;
         }
       }
     }
   }
   cp_async_wait<0>();
 }
-// Pipeline invariant: before iteration k, NS-1+k groups are committed (one per
-// row, empty groups past the end), so wait_group(NS-2) completes row k while
-// rows k+1..k+NS-2 stay in flight; row k+NS-1 is issued into the stage row
-// k-1 used, which every thread released at this iteration's barrier.
+// Pipeline invariant: before block i, NBLK-1+i cp.async groups are committed
+// (one per block, empty past the end), so wait_group(NBLK-2) completes block
+// i while block i+1 .. stays in flight; block i+NBLK-1 is issued into the
+// smem rows block i-1 used, which every thread released at this barrier.
+// RB is a multiple of P, so ring slot u % P == k % P (static indices).
 
 template <int R, int NT, int VEC>
 static inline cudaError_t launch_stream_R(const SepParams& p, int batch, int S, cudaStream_t s) {
   constexpr int ROWLEN = 4 * NT + 2 * SepGeom<R>::HP;
-  const size_t smem = (size_t)kSepStages * ROWLEN * sizeof(float);
+  const size_t smem = (size_t)StreamGeom<R>::NSR * ROWLEN * sizeof(float);
   auto kern = sep_stream<R, NT, VEC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -196,5 +238,23 @@ cudaError_t dispatch_stream(const SepParams& p, int R, int batch, int S, cudaStr
   }
 }
 
+
+static inline SepParams make_sep_params(const SepCall& c, bool pad) {
+  SepParams p;
+  p.src = c.src;
+  p.dst = c.dst;
+  p.rx = c.rx;
+  p.ry = c.ry;
+  for (int i = 0; i < 2 * kMaxRadius + 1; ++i) { p.fx[i] = 0.0f; p.gy[i] = 0.0f; }
+  if (pad) {
+    const int R = c.rx > c.ry ? c.rx : c.ry;
+    for (int i = 0; i < 2 * c.rx + 1; ++i) p.fx[R - c.rx + i] = c.fx[i];
+    for (int j = 0; j < 2 * c.ry + 1; ++j) p.gy[R - c.ry + j] = c.gy[j];
+  } else {
+    for (int i = 0; i < 2 * c.rx + 1; ++i) p.fx[i] = c.fx[i];
+    for (int j = 0; j < 2 * c.ry + 1; ++j) p.gy[j] = c.gy[j];
+  }
+  return p;
+}
 
 }  // namespace icl

@@ -46,6 +46,20 @@ def main():
         "harris": lambda: icl.harris(src, dst, 5, 0.04, "clamp", mask=mask, threshold=1.0),
         "nlm": lambda: icl.nlm(src, dst, 2, 5, 0.1, "clamp"),
     }
+    if "sepconv" in a.filters:  # HBM ceiling on the same buffers: torch copy (read + write)
+        ts = []
+        for _ in range(a.reps):
+            if flush is not None:
+                flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(src)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = statistics.median(ts)
+        print(json.dumps({"filter": "copy", "variant": "torch_copy", "ms": ms, "gbs": 8 * px / ms / 1e6,
+                          "frac_hbm": 8 * px / ms / 1e6 / hbm}), flush=True)
     for f in a.filters.split(","):
         for vid, name in enumerate(icl.variant_names(f)):
             if name.startswith("naive") and S * S * B > (1 << 24) and f == "nlm":
