@@ -35,8 +35,11 @@ __device__ __forceinline__ float harris_R(float sxx, float sxy, float syy, float
 // --------------------------------------------------------------------------
 constexpr int kHarStages = 10;
 
+// Border path: CTAs whose strip touches the left/right image edge or whose
+// rows touch the top/bottom (clamp/constant logic per H-row, one barrier per
+// input row).
 template <int B, int NT, int VEC>
-__global__ void __launch_bounds__(NT) harris_stream(HarrisParams p, int S) {
+__device__ __forceinline__ void harris_slow(const HarrisParams& p, int S, float* smem) {
   constexpr int NS = kHarStages;
   constexpr int A = B / 2;
   constexpr int BB = B - 1 - A;
@@ -45,7 +48,6 @@ __global__ void __launch_bounds__(NT) harris_stream(HarrisParams p, int S) {
   constexpr int ROWLEN = TW + 2 * HP;
   constexpr int NSLOT = ROWLEN / 4;
   constexpr int NC = 4 + B - 1;  // dx/dy columns per thread: xc-A .. xc+3+BB
-  extern __shared__ __align__(16) float smem[];
 
   const int tid = threadIdx.x;
   const int b = blockIdx.z;
@@ -238,10 +240,164 @@ __global__ void __launch_bounds__(NT) harris_stream(HarrisParams p, int S) {
   cp_async_wait<0>();
 }
 
+
+// --------------------------------------------------------------------------
+// Interior fast path: every input row and column the CTA touches is inside
+// the image, so r == yy for every H-row, no boundary logic runs, copy
+// addresses are fixed per thread (running row pointers), and one barrier
+// serves a block of RB H-rows (RB a multiple of B: static ring indices).
+// Identical fp32 operation order to the border path and the naive variant.
+// --------------------------------------------------------------------------
+template <int B>
+struct HarFastGeom {
+  static constexpr int RB = B * ((4 + B - 1) / B);
+  static constexpr int NBLKS = RB <= 8 ? 5 : 4;
+  static constexpr int NSR = RB * NBLKS;
+};
+
+template <int B, int NT>
+__device__ __forceinline__ void harris_fast(const HarrisParams& p, int S, float* smem) {
+  constexpr int A = B / 2;
+  constexpr int BB = B - 1 - A;
+  constexpr int HP = 4;
+  constexpr int TW = 4 * NT;
+  constexpr int ROWLEN = TW + 2 * HP;
+  constexpr int NSLOT = ROWLEN / 4;
+  constexpr int RB = HarFastGeom<B>::RB, NBLKS = HarFastGeom<B>::NBLKS, NSR = HarFastGeom<B>::NSR;
+  const int tid = threadIdx.x;
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * TW;
+  const int ly0 = blockIdx.y * S;
+  const int ly1 = min(ly0 + S, p.dst.H);
+  const int g0 = p.dst.y0 + ly0;
+  const int NY = (ly1 - ly0) + B - 1;  // H-rows: global g0-A .. g0-A+NY-1
+  const int NL = NY + 2;               // input rows: global g0-A-1 .. g0-A+NY
+  const int NBI = (NY + RB - 1) / RB;  // step blocks
+  const int NBL = (NL + RB - 1) / RB;  // load blocks
+  const float* row0 = src_row(p.src, b, g0 - A - 1) + (x0 - HP);
+  const int64_t spitch = p.src.pitch >> 2;
+  const int s1 = tid + NT;
+
+  auto load_block = [&](int m) {
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      const int kl = m * RB + u;
+      if (kl < NL) {
+        float* st = smem + (kl % NSR) * ROWLEN;
+        const float* row = row0 + (int64_t)kl * spitch;
+        cp_async16(st + 4 * tid, row + 4 * tid, 16);
+        if (s1 < NSLOT) cp_async16(st + 4 * s1, row + 4 * s1, 16);
+      }
+    }
+  };
+  for (int m = 0; m < NBLKS - 1; ++m) {
+    if (m < NBL) load_block(m);
+    cp_async_commit();
+  }
+
+  const int xc = x0 + 4 * tid;
+  // ring of the last B H-rows: (Hxx, Hyy) packed per column + Hxy
+  float2 hr2[B][4];
+  float hrxy[B][4];
+  float* drow = dst_row(p.dst, b, ly0);
+  const int64_t dpitch = p.dst.pitch >> 2;
+  char* mrow = p.mask ? p.mask + (int64_t)b * p.mbstride + (int64_t)ly0 * p.mpitch : nullptr;
+
+#pragma unroll 1
+  for (int i = 0; i < NBI; ++i) {
+    cp_async_wait<NBLKS - 3>();  // load blocks 0 .. i+1 complete
+    __syncthreads();             // ... for all threads; load block i-1 is free
+    if (i + NBLKS - 1 < NBL) load_block(i + NBLKS - 1);
+    cp_async_commit();
+    const int base = (i % NBLKS) * RB;  // smem row of load index i*RB
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      const int step = i * RB + u;
+      if (step < NY) {
+        float in[3][12];
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr) {
+          int sr = base + u + rr;
+          if (sr >= NSR) sr -= NSR;
+          const float* st = smem + sr * ROWLEN + 4 * tid;
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const float4 w = reinterpret_cast<const float4*>(st)[q];
+            in[rr][4 * q] = w.x; in[rr][4 * q + 1] = w.y; in[rr][4 * q + 2] = w.z; in[rr][4 * q + 3] = w.w;
+          }
+        }
+        float vd[12];
+#pragma unroll
+        for (int c = 3 - A; c <= 8 + BB; ++c) vd[c] = __fsub_rn(in[2][c], in[0][c]);
+        float2 g[12];  // (dx, dy) per column: operands of the packed products
+#pragma unroll
+        for (int c = 4 - A; c <= 7 + BB; ++c) {
+          const float h0 = __fsub_rn(in[0][c + 1], in[0][c - 1]);
+          const float h1 = __fsub_rn(in[1][c + 1], in[1][c - 1]);
+          const float h2 = __fsub_rn(in[2][c + 1], in[2][c - 1]);
+          g[c].x = __fmaf_rn(2.0f, h1, __fadd_rn(h0, h2));
+          g[c].y = __fmaf_rn(2.0f, vd[c], __fadd_rn(vd[c - 1], vd[c + 1]));
+        }
+        const int slot = u % B;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float2 hxxyy = make_float2(0.0f, 0.0f);
+          float hxy = 0.0f;
+#pragma unroll
+          for (int t = -A; t <= BB; ++t) {
+            const float2 gg = g[4 + q + t];
+            hxxyy = __ffma2_rn(gg, gg, hxxyy);  // (dx^2 + Hxx, dy^2 + Hyy): same rounding as 2 FFMA
+            hxy = __fmaf_rn(gg.x, gg.y, hxy);
+          }
+          hr2[slot][q] = hxxyy;
+          hrxy[slot][q] = hxy;
+        }
+        if (step >= B - 1) {
+          float R[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float2 s2 = hr2[(u + 1) % B][q];
+            float sxy = hrxy[(u + 1) % B][q];
+#pragma unroll
+            for (int j = 1; j < B; ++j) {
+              s2 = __fadd2_rn(s2, hr2[(u + 1 + j) % B][q]);
+              sxy = __fadd_rn(sxy, hrxy[(u + 1 + j) % B][q]);
+            }
+            R[q] = harris_R(s2.x, sxy, s2.y, p.k);
+          }
+          st_cs4(drow + xc, make_float4(R[0], R[1], R[2], R[3]));
+          drow += dpitch;
+          if (mrow) {
+            *reinterpret_cast<uchar4*>(mrow + xc) =
+                make_uchar4(R[0] > p.threshold, R[1] > p.threshold, R[2] > p.threshold, R[3] > p.threshold);
+            mrow += p.mpitch;
+          }
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
+template <int B, int NT, int VEC>
+__global__ void __launch_bounds__(NT) harris_stream(HarrisParams p, int S) {
+  extern __shared__ __align__(16) float smem[];
+  constexpr int A = B / 2, BB = B - 1 - A, TW = 4 * NT;
+  const int x0 = blockIdx.x * TW;
+  const int ly0 = blockIdx.y * S;
+  const int ly1 = min(ly0 + S, p.dst.H);
+  const int g0 = p.dst.y0 + ly0;
+  const bool fast = VEC == 4 && x0 - 4 >= 0 && x0 + TW + 4 <= p.src.W && g0 - A - 1 >= 0 &&
+                    g0 + (ly1 - ly0) + BB + 1 <= p.src.Hg;
+  if (fast) harris_fast<B, NT>(p, S, smem);
+  else harris_slow<B, NT, VEC>(p, S, smem);
+}
+
 template <int B, int NT, int VEC>
 static inline cudaError_t launch_hs(const HarrisParams& p, int batch, int S, cudaStream_t s) {
   constexpr int ROWLEN = 4 * NT + 8;
-  const size_t smem = (size_t)kHarStages * ROWLEN * sizeof(float);
+  const int rows = kHarStages > HarFastGeom<B>::NSR ? kHarStages : HarFastGeom<B>::NSR;
+  const size_t smem = (size_t)rows * ROWLEN * sizeof(float);
   auto kern = harris_stream<B, NT, VEC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
