@@ -432,13 +432,86 @@ def run_suite(args):
     return 0
 
 
+# ----------------------------------------------------------------------------- icl arm: row bands
+def run_sepconv_bands(args):
+    """BASELINE.json configs[3]: one S x S fp32 image, separable Gaussian radius r,
+    row-band sharded over the ranks with an NCCL halo exchange (dist.halo_exchange)
+    overlapped with the interior rows.  Strong scaling (the image is fixed)."""
+    import torch
+
+    import paper_1605_06399_b200 as icl
+    from paper_1605_06399_b200 import dist as icd
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = init_dist(ws, "nccl")
+    icl.load_library()
+    S, r = args.size, args.radius
+    band = icd.partition(S, ws, rank, r, r)
+    buf = torch.empty(band.buf_rows, S, device=dev)
+    # own rows from the device generator (synth.uniform_image stream), halos by exchange
+    icl.fill_uniform(buf[band.own_slice], 4, row0=band.r0)
+    out = torch.empty(band.rows, S, device=dev)
+    fx = synth.gaussian_taps(r)
+    stream = torch.cuda.current_stream(dev)
+    comm = torch.cuda.Stream(device=dev)
+
+    def call(src, dst, b, st):
+        icl.sepconv(src, dst, fx, fx, "constant", band=b, stream=st)
+
+    def step():
+        icd.run_band(call, buf, out, band, (lambda: icd.halo_exchange(buf, band)) if ws > 1 else (lambda: None),
+                     stream=stream, comm_stream=comm if ws > 1 else None)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    n0 = icl.launch_count()
+    with ClockSampler(local) as clk:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            step()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+    launches = icl.launch_count() - n0
+    if ws > 1:
+        dist.barrier()
+    step_ms = max_over_ranks(a.elapsed_time(b) / args.steps, ws, dev)
+    px = S * S
+    value = px / (step_ms * 1e-3) / 1e6
+    hbm, hbm_kind = measured_peaks()
+    achieved = 8 * px / ws / (step_ms * 1e-3) / 1e9  # per-GPU algorithmic GB/s
+    if rank == 0:
+        line = {
+            "metric": f"sepconv megapixels/s ({S}x{S} fp32, radius {r}, row-band sharded)",
+            "value": value, "unit": "Mpx/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "sepconv16k (BASELINE.json configs[3])", "size": [S, S], "radius": r,
+                       "border": "constant", "halo_rows": [band.up, band.down], "variant":
+                           icl.variant_names("sepconv")[icl.last_variant("sepconv")],
+                       "l2": "input 1 GiB >> L2; no flush"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None, "peak_kind": hbm_kind},
+            "gpu_launches": launches, "clocks": clk.summary(), "e2e": None, "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="icl", choices=["icl", "reference"])
-    ap.add_argument("--workload", default="suite", choices=["suite"])
+    ap.add_argument("--workload", default="suite", choices=["suite", "sepconv16k"])
+    ap.add_argument("--radius", type=int, default=2)
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--size", type=int, default=4096)
     ap.add_argument("--no-e2e", action="store_true")
@@ -449,6 +522,10 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "sepconv16k":
+        if args.size == 4096:
+            args.size = 16384
+        return run_sepconv_bands(args)
     return run_suite(args)
 
 
