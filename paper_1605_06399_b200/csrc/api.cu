@@ -149,6 +149,9 @@ static const Variant kSepVariants[] = {
     {"stream_nt64_s32_v4", K_STREAM, 64, 4, 32},
     {"stream_nt64_s64_v4", K_STREAM, 64, 4, 64},
     {"stream_nt128_s64_v4", K_STREAM, 128, 4, 64},
+    {"stream_nt64_s128_v4", K_STREAM, 64, 4, 128},
+    {"stream_nt32_s128_v4", K_STREAM, 32, 4, 128},
+    {"stream_nt128_s128_v4", K_STREAM, 128, 4, 128},
     {"stream_nt256_s16_v4", K_STREAM, 256, 4, 16},
     {"stream_nt64_s64_v1", K_STREAM, 64, 1, 64},
     {"stream_nt64_s16_v1", K_STREAM, 64, 1, 16},
@@ -246,7 +249,15 @@ static int default_variant(const Prepared& pc) {
   switch (pc.f) {
     case ICL_FILTER_SEPCONV:
       if (!pc.a16) return variant_id(pc.f, pc.pixels < (1 << 20) ? "stream_nt64_s16_v1" : "stream_nt64_s64_v1");
-      return variant_id(pc.f, pc.pixels < (1 << 20) ? "stream_nt32_s8_v4" : "stream_nt64_s16_v4");
+      if (pc.pixels < (1 << 20)) return variant_id(pc.f, "stream_nt32_s8_v4");
+      {
+        // the vertical halo 2R is re-read per S output rows: S grows with R
+        const int R = pc.sep.rx > pc.sep.ry ? pc.sep.rx : pc.sep.ry;
+        if (R <= 2) return variant_id(pc.f, "stream_nt64_s16_v4");
+        if (R <= 4) return variant_id(pc.f, "stream_nt64_s32_v4");
+        if (R <= 8) return variant_id(pc.f, "stream_nt64_s64_v4");
+        return variant_id(pc.f, "stream_nt64_s128_v4");
+      }
     case ICL_FILTER_HARRIS:
       if (!pc.a16) return variant_id(pc.f, "stream_nt64_s64_v1");
       return variant_id(pc.f, pc.pixels < (1 << 20) ? "stream_nt32_s16_v4" : "stream_nt64_s64_v4");
