@@ -29,6 +29,7 @@ namespace icl {
 bool nlm_tiled_supported(int P, int S);
 bool nlm_boxsum_supported(int P, int S);
 bool nlm_r8_supported(int P, int S);
+bool nlm_r16_supported(int P, int S);
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -131,7 +132,7 @@ static icl_status make_views(const icl_image* src, const icl_image* dst, const i
 }
 
 // ------------------------------------------------------------------ variants
-enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK };
+enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16 };
 struct Variant {
   const char* name;
   Kind kind;
@@ -169,6 +170,7 @@ static const Variant kNlmVariants[] = {
     {"tiled_direct_32x8", K_TILED, 32, 0, 8},
     {"boxsum_32x32", K_BOXSUM, 32, 0, 32},
     {"boxsum_r8", K_BOXR8, 0, 0, 0},
+    {"boxsum_r16", K_BOXR16, 0, 0, 0},
 };
 
 static const Variant* table(icl_filter f, int* n) {
@@ -212,6 +214,7 @@ static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
   if (pc.f == ICL_FILTER_NLM && v.kind == K_TILED && !nlm_tiled_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXSUM && !nlm_boxsum_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXR8 && !nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return false;
+  if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXR16 && !nlm_r16_supported(pc.nlm.P, pc.nlm.S)) return false;
   return true;
 }
 
@@ -229,6 +232,7 @@ static cudaError_t run_variant(const Prepared& pc, const Variant& v, cudaStream_
       if (v.kind == K_NAIVE) return launch_nlm_naive(pc.nlm, s);
       if (v.kind == K_TILED) return launch_nlm_tiled(pc.nlm, v.nt, v.S, s);
       if (v.kind == K_BOXR8) return launch_nlm_r8(pc.nlm, s);
+      if (v.kind == K_BOXR16) return launch_nlm_r16(pc.nlm, s);
       return launch_nlm_boxsum(pc.nlm, 0, s);
   }
   return cudaErrorInvalidValue;

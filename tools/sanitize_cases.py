@@ -1,0 +1,33 @@
+"""Small ragged cases exercising every variant of every filter once (for
+compute-sanitizer memcheck / racecheck / synccheck runs; see tools/sanitize.sh)."""
+import sys
+import torch
+sys.path.insert(0, '.')
+import paper_1605_06399_b200 as icl  # noqa: E402
+import synth  # noqa: E402
+
+dev = torch.device('cuda:0')
+for (h, w) in [(61, 53), (130, 517), (9, 300)]:
+    img = torch.from_numpy(synth.uniform_image(1, h, w)).to(dev)
+    out = torch.empty_like(img)
+    mask = torch.empty(h, w, dtype=torch.uint8, device=dev)
+    ws = torch.empty(icl.sepconv_workspace_bytes(w, h, 1, 15) // 4 + 1, device=dev)
+    for f in ("sepconv", "harris", "nlm"):
+        for vid, name in enumerate(icl.variant_names(f)):
+            icl.force_variant(f, vid)
+            for border in ("constant", "clamp"):
+                try:
+                    if f == "sepconv":
+                        for r in (0, 2, 7):
+                            fx = synth.gaussian_taps(r)
+                            icl.sepconv(img, out, fx, fx, border, 0.5, workspace=ws)
+                    elif f == "harris":
+                        icl.harris(img, out, 5, 0.04, border, 0.5, mask=mask, threshold=0.1)
+                    else:
+                        icl.nlm(img, out, 2, 5, 0.1, border, 0.5)
+                except icl.IclError as e:
+                    if e.status not in (3, 4):
+                        raise
+            torch.cuda.synchronize()
+        icl.force_variant(f, None)
+print("sanitize cases done")
