@@ -97,8 +97,8 @@ __device__ __forceinline__ void harris_slow(const HarrisParams& p, int S, float*
     float* st = smem + (kl % NS) * ROWLEN;
     const int il = HP - x0;
     const int ir = (W - 1) - x0 + HP;
-    const float vl = st[il >= 0 && il < ROWLEN ? il : 0];
-    const float vr = st[ir >= 0 && ir < ROWLEN ? ir : 0];
+    const float vl = (il >= 0 && il < ROWLEN) ? st[il] : 0.0f;  // column 0, if in this row
+    const float vr = (ir >= 0 && ir < ROWLEN) ? st[ir] : 0.0f;  // column W-1, if in this row
     for (int s = tid; s < NSLOT; s += NT) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {

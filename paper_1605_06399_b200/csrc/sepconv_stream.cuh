@@ -124,8 +124,8 @@ __global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
       const int k = kb + u;
       if (k >= NI) break;
       float* st = smem + (k % NSR) * ROWLEN;
-      const float vl = st[il >= 0 && il < ROWLEN ? il : 0];
-      const float vr = st[ir >= 0 && ir < ROWLEN ? ir : 0];
+      const float vl = (il >= 0 && il < ROWLEN) ? st[il] : 0.0f;  // column 0, if in this row
+      const float vr = (ir >= 0 && ir < ROWLEN) ? st[ir] : 0.0f;  // column W-1, if in this row
       for (int s = tid; s < NSLOT; s += NT) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
