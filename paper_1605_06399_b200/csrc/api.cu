@@ -132,7 +132,7 @@ static icl_status make_views(const icl_image* src, const icl_image* dst, const i
 }
 
 // ------------------------------------------------------------------ variants
-enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16 };
+enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL };
 struct Variant {
   const char* name;
   Kind kind;
@@ -164,6 +164,9 @@ static const Variant kHarVariants[] = {
     {"stream_nt32_s32_v4", K_STREAM, 32, 4, 32},  {"stream_nt128_s64_v4", K_STREAM, 128, 4, 64},
     {"stream_nt64_s128_v4", K_STREAM, 64, 4, 128}, {"stream_nt32_s16_v4", K_STREAM, 32, 4, 16},
     {"stream_nt64_s64_v1", K_STREAM, 64, 1, 64},
+    {"shfl_nw2_s64", K_SHFL, 2, 4, 64},           {"shfl_nw4_s64", K_SHFL, 4, 4, 64},
+    {"shfl_nw2_s32", K_SHFL, 2, 4, 32},           {"shfl_nw4_s32", K_SHFL, 4, 4, 32},
+    {"shfl_nw2_s128", K_SHFL, 2, 4, 128},
 };
 static const Variant kNlmVariants[] = {
     {"naive_direct", K_NAIVE, 0, 0, 0},
@@ -200,7 +203,8 @@ struct Prepared {
 
 static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
   *why = ICL_ERR_UNSUPPORTED;
-  if ((v.kind == K_STREAM || v.kind == K_BULK) && v.vec == 4 && !pc.a16) return false;
+  if ((v.kind == K_STREAM || v.kind == K_BULK || v.kind == K_SHFL) && v.vec == 4 && !pc.a16) return false;
+  if (v.kind == K_SHFL && pc.har.block > 5) return false;
   if (pc.f == ICL_FILTER_SEPCONV && v.kind == K_STREAM &&
       sep_stream_smem_bytes(v.nt, pc.sep.rx > pc.sep.ry ? pc.sep.rx : pc.sep.ry) > 227 * 1024)
     return false;
@@ -227,6 +231,7 @@ static cudaError_t run_variant(const Prepared& pc, const Variant& v, cudaStream_
       return launch_sep_stream(pc.sep, v.nt, v.vec, v.S, s);
     case ICL_FILTER_HARRIS:
       if (v.kind == K_NAIVE) return launch_harris_naive(pc.har, s);
+      if (v.kind == K_SHFL) return launch_harris_shfl(pc.har, v.nt, v.S, s);
       return launch_harris_stream(pc.har, v.nt, v.vec, v.S, s);
     case ICL_FILTER_NLM:
       if (v.kind == K_NAIVE) return launch_nlm_naive(pc.nlm, s);
@@ -264,7 +269,8 @@ static int default_variant(const Prepared& pc) {
       }
     case ICL_FILTER_HARRIS:
       if (!pc.a16) return variant_id(pc.f, "stream_nt64_s64_v1");
-      return variant_id(pc.f, pc.pixels < (1 << 20) ? "stream_nt32_s16_v4" : "stream_nt64_s64_v4");
+      if (pc.pixels < (1 << 20)) return variant_id(pc.f, "stream_nt32_s16_v4");
+      return variant_id(pc.f, pc.har.block <= 5 ? "shfl_nw2_s64" : "stream_nt64_s64_v4");
     case ICL_FILTER_NLM:
       if (nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return variant_id(pc.f, "boxsum_r8");
       return nlm_tiled_supported(pc.nlm.P, pc.nlm.S) ? variant_id(pc.f, "tiled_direct_32x8") : 0;

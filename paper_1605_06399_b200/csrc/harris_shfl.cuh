@@ -1,0 +1,217 @@
+// harris_shfl.cuh -- Harris variant family "shfl<B,NW>": the fused streaming
+// Harris kernel (§6; Tables 4-5) with the window halo
+// exchanged by warp shuffles instead of recomputed.
+//
+// Each lane computes (dx, dy) only for its own 4 columns (differences-first
+// Sobel, R19) and fetches the B-1 neighbour columns the window sums
+// need from lanes -1 / +1 (__shfl_up/down, 8 shuffles per H-row for B <= 5).
+// Warps overlap by one lane on each side: lanes 0 and 31 only supply halo
+// columns, lanes 1..30 emit outputs, so a warp produces 120 columns and a
+// CTA of NW warps a strip of TW = 120*NW columns.  The Sobel stage costs
+// ~34 FP32 ops per H-row instead of ~74 (no 2x halo recomputation); the rest
+// (FFMA2-packed (Sxx,Syy) window sums, ring of B H-rows, response, mask) is
+// the stream<> fast path.  Interior CTAs only; CTAs touching the image border
+// run harris_slow<> with the same strip geometry.  Same per-output fp32
+// operation order as every other Harris variant (bit-identical).
+#pragma once
+#include "harris_stream.cuh"
+
+namespace icl {
+
+template <int B, int NW>
+__device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, float* smem) {
+  constexpr int A = B / 2;
+  constexpr int BB = B - 1 - A;
+  static_assert(A <= 2 && BB <= 2, "shuffle halo covers windows up to 5x5");
+  constexpr int NT = 32 * NW;
+  constexpr int HP = 8;
+  constexpr int TW = 120 * NW;
+  constexpr int ROWLEN = TW + 2 * HP;
+  constexpr int NSLOT = ROWLEN / 4;
+  constexpr int RB = HarFastGeom<B>::RB, NBLKS = HarFastGeom<B>::NBLKS, NSR = HarFastGeom<B>::NSR;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * TW;
+  const int ly0 = blockIdx.y * S;
+  const int ly1 = min(ly0 + S, p.dst.H);
+  const int g0 = p.dst.y0 + ly0;
+  const int NY = (ly1 - ly0) + B - 1;
+  const int NL = NY + 2;
+  const int NBI = (NY + RB - 1) / RB;
+  const int NBL = (NL + RB - 1) / RB;
+  const float* row0 = src_row(p.src, b, g0 - A - 1) + (x0 - HP);
+  const int64_t spitch = p.src.pitch >> 2;
+
+  auto load_block = [&](int m) {
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      const int kl = m * RB + u;
+      if (kl < NL) {
+        float* st = smem + (kl % NSR) * ROWLEN;
+        const float* row = row0 + (int64_t)kl * spitch;
+        for (int s = tid; s < NSLOT; s += NT) cp_async16(st + 4 * s, row + 4 * s, 16);
+      }
+    }
+  };
+  for (int m = 0; m < NBLKS - 1; ++m) {
+    if (m < NBL) load_block(m);
+    cp_async_commit();
+  }
+
+  // own columns: xl .. xl+3, xl = x0 + 120*warp + 4*(lane-1); smem index of xl:
+  const int xl = x0 + 120 * warp + 4 * (lane - 1);
+  const int si = xl - (x0 - HP);
+  const bool emit = lane >= 1 && lane <= 30;
+  float2 hr2[B][4];
+  float hrxy[B][4];
+  float* drow = dst_row(p.dst, b, ly0);
+  const int64_t dpitch = p.dst.pitch >> 2;
+  char* mrow = p.mask ? p.mask + (int64_t)b * p.mbstride + (int64_t)ly0 * p.mpitch : nullptr;
+
+#pragma unroll 1
+  for (int i = 0; i < NBI; ++i) {
+    cp_async_wait<NBLKS - 3>();
+    __syncthreads();
+    if (i + NBLKS - 1 < NBL) load_block(i + NBLKS - 1);
+    cp_async_commit();
+    const int base = (i % NBLKS) * RB;
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      const int step = i * RB + u;
+      if (step < NY) {
+        // columns xl-1 .. xl+4 of the three input rows (index c+1 <-> column xl+c)
+        float in[3][6];
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr) {
+          int sr = base + u + rr;
+          if (sr >= NSR) sr -= NSR;
+          const float* st = smem + sr * ROWLEN + si;
+          const float4 w = *reinterpret_cast<const float4*>(st);
+          // columns xl-1 / xl+4 belong to lanes -1 / +1 (lanes 0 / 31 get junk there,
+          // which only feeds their own non-emitted, non-shared columns)
+          in[rr][0] = __shfl_up_sync(0xffffffffu, w.w, 1);
+          in[rr][1] = w.x; in[rr][2] = w.y; in[rr][3] = w.z; in[rr][4] = w.w;
+          in[rr][5] = __shfl_down_sync(0xffffffffu, w.x, 1);
+        }
+        float vd[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) vd[c] = __fsub_rn(in[2][c], in[0][c]);
+        // g[j] = (dx, dy) of column xl-2+j, j = 0..7 (own columns j = 2..5)
+        float2 g[8];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float h0 = __fsub_rn(in[0][c + 2], in[0][c]);
+          const float h1 = __fsub_rn(in[1][c + 2], in[1][c]);
+          const float h2 = __fsub_rn(in[2][c + 2], in[2][c]);
+          g[c + 2].x = __fmaf_rn(2.0f, h1, __fadd_rn(h0, h2));
+          g[c + 2].y = __fmaf_rn(2.0f, vd[c + 1], __fadd_rn(vd[c], vd[c + 2]));
+        }
+        g[0].x = __shfl_up_sync(0xffffffffu, g[4].x, 1);
+        g[0].y = __shfl_up_sync(0xffffffffu, g[4].y, 1);
+        g[1].x = __shfl_up_sync(0xffffffffu, g[5].x, 1);
+        g[1].y = __shfl_up_sync(0xffffffffu, g[5].y, 1);
+        g[6].x = __shfl_down_sync(0xffffffffu, g[2].x, 1);
+        g[6].y = __shfl_down_sync(0xffffffffu, g[2].y, 1);
+        g[7].x = __shfl_down_sync(0xffffffffu, g[3].x, 1);
+        g[7].y = __shfl_down_sync(0xffffffffu, g[3].y, 1);
+        const int slot = u % B;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float2 hxxyy = make_float2(0.0f, 0.0f);
+          float hxy = 0.0f;
+#pragma unroll
+          for (int t = -A; t <= BB; ++t) {
+            const float2 gg = g[2 + q + t];
+            hxxyy = __ffma2_rn(gg, gg, hxxyy);
+            hxy = __fmaf_rn(gg.x, gg.y, hxy);
+          }
+          hr2[slot][q] = hxxyy;
+          hrxy[slot][q] = hxy;
+        }
+        if (step >= B - 1) {
+          float R[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float2 s2 = hr2[(u + 1) % B][q];
+            float sxy = hrxy[(u + 1) % B][q];
+#pragma unroll
+            for (int j = 1; j < B; ++j) {
+              s2 = __fadd2_rn(s2, hr2[(u + 1 + j) % B][q]);
+              sxy = __fadd_rn(sxy, hrxy[(u + 1 + j) % B][q]);
+            }
+            R[q] = harris_R(s2.x, sxy, s2.y, p.k);
+          }
+          if (emit) {
+            st_cs4(drow + xl, make_float4(R[0], R[1], R[2], R[3]));
+            if (mrow)
+              *reinterpret_cast<uchar4*>(mrow + xl) =
+                  make_uchar4(R[0] > p.threshold, R[1] > p.threshold, R[2] > p.threshold, R[3] > p.threshold);
+          }
+          drow += dpitch;
+          if (mrow) mrow += p.mpitch;
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
+// Interior and border CTAs run as two launches over the same grid (each CTA
+// returns at once in the launch that is not its own): the hot interior kernel
+// then carries only its own code and registers.
+template <int B, int NW>
+__device__ __forceinline__ bool harris_shfl_is_fast(const HarrisParams& p, int S) {
+  constexpr int A = B / 2, BB = B - 1 - A, TW = 120 * NW;
+  const int x0 = blockIdx.x * TW;
+  const int ly0 = blockIdx.y * S;
+  const int ly1 = min(ly0 + S, p.dst.H);
+  const int g0 = p.dst.y0 + ly0;
+  return x0 - 8 >= 0 && x0 + TW + 8 <= p.src.W && g0 - A - 1 >= 0 && g0 + (ly1 - ly0) + BB + 1 <= p.src.Hg;
+}
+
+template <int B, int NW>
+__global__ void __launch_bounds__(32 * NW) harris_shfl(HarrisParams p, int S) {
+  extern __shared__ __align__(16) float smem[];
+  if (harris_shfl_is_fast<B, NW>(p, S)) harris_shfl_fast<B, NW>(p, S, smem);
+}
+
+template <int B, int NW>
+__global__ void __launch_bounds__(32 * NW) harris_shfl_border(HarrisParams p, int S) {
+  extern __shared__ __align__(16) float smem[];
+  if (!harris_shfl_is_fast<B, NW>(p, S)) harris_slow<B, 32 * NW, 4, 120 * NW, 8>(p, S, smem);
+}
+
+template <int B, int NW>
+static inline cudaError_t launch_hshfl(const HarrisParams& p, int batch, int S, cudaStream_t s) {
+  constexpr int TW = 120 * NW;
+  constexpr int ROWLEN = TW + 16;
+  const int rows = kHarStages > HarFastGeom<B>::NSR ? kHarStages : HarFastGeom<B>::NSR;
+  const size_t smem = (size_t)rows * ROWLEN * sizeof(float);
+  auto kern = harris_shfl<B, NW>;
+  auto kernb = harris_shfl_border<B, NW>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kernb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grd((p.src.W + TW - 1) / TW, (p.dst.H + S - 1) / S, batch);
+  kern<<<grd, 32 * NW, smem, s>>>(p, S);
+  count_launch();
+  kernb<<<grd, 32 * NW, smem, s>>>(p, S);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int NW>
+cudaError_t dispatch_hshfl(const HarrisParams& p, int batch, int S, cudaStream_t s) {
+  switch (p.block) {
+    case 1: return launch_hshfl<1, NW>(p, batch, S, s);
+    case 2: return launch_hshfl<2, NW>(p, batch, S, s);
+    case 3: return launch_hshfl<3, NW>(p, batch, S, s);
+    case 4: return launch_hshfl<4, NW>(p, batch, S, s);
+    case 5: return launch_hshfl<5, NW>(p, batch, S, s);
+    default: return cudaErrorInvalidValue;  // B = 6, 7 need a wider shuffle halo
+  }
+}
+
+}  // namespace icl

@@ -38,13 +38,16 @@ constexpr int kHarStages = 10;
 // Border path: CTAs whose strip touches the left/right image edge or whose
 // rows touch the top/bottom (clamp/constant logic per H-row, one barrier per
 // input row).
-template <int B, int NT, int VEC>
+// TW_/HP_: output columns per CTA and halo columns per side (the warp-shuffle
+// kernel of harris_shfl.cuh uses 120*NW and 8); threads with 4*tid >= TW only
+// help with the loads.
+template <int B, int NT, int VEC, int TW_ = 4 * NT, int HP_ = 4>
 __device__ __forceinline__ void harris_slow(const HarrisParams& p, int S, float* smem) {
   constexpr int NS = kHarStages;
   constexpr int A = B / 2;
   constexpr int BB = B - 1 - A;
-  constexpr int HP = 4;  // A + 1 <= 4 for B <= 7
-  constexpr int TW = 4 * NT;
+  constexpr int HP = HP_;  // >= A + 1 (4 suffices for B <= 7), multiple of 4
+  constexpr int TW = TW_;
   constexpr int ROWLEN = TW + 2 * HP;
   constexpr int NSLOT = ROWLEN / 4;
   constexpr int NC = 4 + B - 1;  // dx/dy columns per thread: xc-A .. xc+3+BB
@@ -116,7 +119,7 @@ __device__ __forceinline__ void harris_slow(const HarrisParams& p, int S, float*
   }
 
   const int xc = x0 + 4 * tid;
-  const bool active = xc < W;
+  const bool active = xc < W && 4 * tid < TW;
   float hring[B][12];  // [slot][ {xx[4], xy[4], yy[4]} ]
   int cidx = 0;        // load index of the current centre row (0 = none yet)
   const int NY = (ly1 - ly0) + B - 1;
@@ -150,7 +153,7 @@ __device__ __forceinline__ void harris_slow(const HarrisParams& p, int S, float*
           float in[3][12];
 #pragma unroll
           for (int rr = 0; rr < 3; ++rr) {
-            const float* st = smem + ((cidx - 1 + rr) % NS) * ROWLEN + 4 * tid;
+            const float* st = smem + ((cidx - 1 + rr) % NS) * ROWLEN + 4 * tid + (HP - 4);
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
               const float4 w = reinterpret_cast<const float4*>(st)[q];

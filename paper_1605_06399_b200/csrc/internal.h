@@ -53,6 +53,7 @@ cudaError_t launch_sep_bulk(const SepCall& c, int nt, int S, cudaStream_t s);
 // harris
 cudaError_t launch_harris_naive(const HarrisCall& c, cudaStream_t s);
 cudaError_t launch_harris_stream(const HarrisCall& c, int nt, int vec, int S, cudaStream_t s);
+cudaError_t launch_harris_shfl(const HarrisCall& c, int nw, int S, cudaStream_t s);
 
 // nlm
 cudaError_t launch_nlm_naive(const NlmCall& c, cudaStream_t s);
