@@ -10,9 +10,11 @@
 // CTA of NW warps a strip of TW = 120*NW columns.  The Sobel stage costs
 // ~34 FP32 ops per H-row instead of ~74 (no 2x halo recomputation); the rest
 // (FFMA2-packed (Sxx,Syy) window sums, ring of B H-rows, response, mask) is
-// the stream<> fast path.  Interior CTAs only; CTAs touching the image border
-// run harris_slow<> with the same strip geometry.  Same per-output fp32
-// operation order as every other Harris variant (bit-identical).
+// the stream<> fast path.  Image borders are handled in the same kernel:
+// left/right edges by per-element fix-ups (CTA-uniform flag), top/bottom by
+// loading clamped (or constant) rows and recomputing H at the clamped centre
+// row (== H(clamp(yy)), per-stage semantics).  Same per-output fp32 operation
+// order as every other Harris variant (bit-identical).
 #pragma once
 #include "harris_stream.cuh"
 
@@ -39,7 +41,12 @@ __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, f
   const int NL = NY + 2;
   const int NBI = (NY + RB - 1) / RB;
   const int NBL = (NL + RB - 1) / RB;
-  const float* row0 = src_row(p.src, b, g0 - A - 1) + (x0 - HP);
+  const int W = p.src.W;
+  const int Hg = p.src.Hg;
+  const bool clampb = p.src.border == kBorderClamp;
+  // left/right image edge inside this strip: per-element boundary work (uniform flag)
+  const bool edge = x0 - HP < 0 || x0 + TW + HP > W;
+  const float* rowb = src_row(p.src, b, g0 - A - 1);  // input row of load index 0, column 0
   const int64_t spitch = p.src.pitch >> 2;
 
   auto load_block = [&](int m) {
@@ -48,8 +55,40 @@ __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, f
       const int kl = m * RB + u;
       if (kl < NL) {
         float* st = smem + (kl % NSR) * ROWLEN;
-        const float* row = row0 + (int64_t)kl * spitch;
-        for (int s = tid; s < NSLOT; s += NT) cp_async16(st + 4 * s, row + 4 * s, 16);
+        int gi = g0 - A - 1 + kl;
+        if (gi < 0 || gi >= Hg) {  // input row outside the image (top / bottom segments only)
+          if (!clampb) {
+            for (int c = tid; c < ROWLEN; c += NT) st[c] = p.src.cval;
+            continue;
+          }
+          gi = clampi(gi, 0, Hg - 1);
+        }
+        const float* row = rowb + (int64_t)(gi - (g0 - A - 1)) * spitch;
+        for (int s = tid; s < NSLOT; s += NT) {
+          const int xs = x0 - HP + 4 * s;
+          if (!edge) {
+            cp_async16(st + 4 * s, row + xs, 16);
+          } else {  // zero-fill outside [0, W); fixed below (Fig. 3)
+            const int nb = (xs < 0) ? 0 : min(max(W - xs, 0), 4) * 4;
+            cp_async16(st + 4 * s, nb ? (const void*)(row + xs) : (const void*)row, nb);
+          }
+        }
+      }
+    }
+  };
+  // Input boundary of the halo columns outside [0, W) of load block m.
+  auto fix_block = [&](int m) {
+    for (int u = 0; u < RB; ++u) {
+      const int kl = m * RB + u;
+      if (kl >= NL) break;
+      float* st = smem + (kl % NSR) * ROWLEN;
+      const int il = HP - x0, ir = (W - 1) - x0 + HP;
+      const float vl = (il >= 0 && il < ROWLEN) ? st[il] : 0.0f;
+      const float vr = (ir >= 0 && ir < ROWLEN) ? st[ir] : 0.0f;
+      for (int c = tid; c < ROWLEN; c += NT) {
+        const int xe = x0 - HP + c;
+        if (xe < 0) st[c] = clampb ? vl : p.src.cval;
+        else if (xe >= W) st[c] = clampb ? vr : p.src.cval;
       }
     }
   };
@@ -61,7 +100,11 @@ __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, f
   // own columns: xl .. xl+3, xl = x0 + 120*warp + 4*(lane-1); smem index of xl:
   const int xl = x0 + 120 * warp + 4 * (lane - 1);
   const int si = xl - (x0 - HP);
-  const bool emit = lane >= 1 && lane <= 30;
+  const bool emit = lane >= 1 && lane <= 30 && xl < W;
+  // lanes of this warp owning image columns 0 and W-1 (for the dx/dy boundary)
+  const int xw = x0 + 120 * warp - 4;  // first column of lane 0
+  const int ll = (0 - xw) >> 2, el = (0 - xw) & 3;
+  const int lr = (W - 1 - xw) >> 2, er = (W - 1 - xw) & 3;
   float2 hr2[B][4];
   float hrxy[B][4];
   float* drow = dst_row(p.dst, b, ly0);
@@ -72,6 +115,11 @@ __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, f
   for (int i = 0; i < NBI; ++i) {
     cp_async_wait<NBLKS - 3>();
     __syncthreads();
+    if (edge) {  // rows of load blocks i (first time only) and i+1 become visible now
+      if (i == 0) fix_block(0);
+      if (i + 1 < NBL) fix_block(i + 1);
+      __syncthreads();
+    }
     if (i + NBLKS - 1 < NBL) load_block(i + NBLKS - 1);
     cp_async_commit();
     const int base = (i % NBLKS) * RB;
@@ -79,12 +127,17 @@ __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, f
     for (int u = 0; u < RB; ++u) {
       const int step = i * RB + u;
       if (step < NY) {
+        // H-row yy outside the image: clamp -> recompute H at r = clamp(yy) from the
+        // same smem rows (== H(clamp(yy)), per-stage semantics); constant -> 0 below.
+        const int yy = g0 - A + step;
+        const int dz = yy < 0 ? -yy : (yy >= Hg ? (Hg - 1) - yy : 0);
         // columns xl-1 .. xl+4 of the three input rows (index c+1 <-> column xl+c)
         float in[3][6];
 #pragma unroll
         for (int rr = 0; rr < 3; ++rr) {
-          int sr = base + u + rr;
+          int sr = base + u + rr + dz;
           if (sr >= NSR) sr -= NSR;
+          if (sr < 0) sr += NSR;
           const float* st = smem + sr * ROWLEN + si;
           const float4 w = *reinterpret_cast<const float4*>(st);
           // columns xl-1 / xl+4 belong to lanes -1 / +1 (lanes 0 / 31 get junk there,
@@ -105,6 +158,22 @@ __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, f
           const float h2 = __fsub_rn(in[2][c + 2], in[2][c]);
           g[c + 2].x = __fmaf_rn(2.0f, h1, __fadd_rn(h0, h2));
           g[c + 2].y = __fmaf_rn(2.0f, vd[c + 1], __fadd_rn(vd[c], vd[c + 2]));
+        }
+        if (edge) {  // per-stage boundary of dx/dy: outside [0, W) -> dx(clamp(q)) or 0
+          const float2 e0 = el == 0 ? g[2] : el == 1 ? g[3] : el == 2 ? g[4] : g[5];
+          const float2 e1 = er == 0 ? g[2] : er == 1 ? g[3] : er == 2 ? g[4] : g[5];
+          float2 gl, gr;
+          gl.x = __shfl_sync(0xffffffffu, e0.x, ll & 31);
+          gl.y = __shfl_sync(0xffffffffu, e0.y, ll & 31);
+          gr.x = __shfl_sync(0xffffffffu, e1.x, lr & 31);
+          gr.y = __shfl_sync(0xffffffffu, e1.y, lr & 31);
+          if (!clampb) gl = gr = make_float2(0.0f, 0.0f);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int xe = xl + c;
+            if (xe < 0) g[c + 2] = gl;
+            else if (xe >= W) g[c + 2] = gr;
+          }
         }
         g[0].x = __shfl_up_sync(0xffffffffu, g[4].x, 1);
         g[0].y = __shfl_up_sync(0xffffffffu, g[4].y, 1);
@@ -128,6 +197,13 @@ __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, f
           hr2[slot][q] = hxxyy;
           hrxy[slot][q] = hxy;
         }
+        if (dz != 0 && !clampb) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            hr2[slot][q] = make_float2(0.0f, 0.0f);
+            hrxy[slot][q] = 0.0f;
+          }
+        }
         if (step >= B - 1) {
           float R[4];
 #pragma unroll
@@ -142,10 +218,19 @@ __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, f
             R[q] = harris_R(s2.x, sxy, s2.y, p.k);
           }
           if (emit) {
-            st_cs4(drow + xl, make_float4(R[0], R[1], R[2], R[3]));
-            if (mrow)
-              *reinterpret_cast<uchar4*>(mrow + xl) =
-                  make_uchar4(R[0] > p.threshold, R[1] > p.threshold, R[2] > p.threshold, R[3] > p.threshold);
+            if (xl + 3 < W) {
+              st_cs4(drow + xl, make_float4(R[0], R[1], R[2], R[3]));
+              if (mrow)
+                *reinterpret_cast<uchar4*>(mrow + xl) =
+                    make_uchar4(R[0] > p.threshold, R[1] > p.threshold, R[2] > p.threshold, R[3] > p.threshold);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (xl + q < W) {
+                  drow[xl + q] = R[q];
+                  if (mrow) mrow[xl + q] = R[q] > p.threshold ? 1 : 0;
+                }
+            }
           }
           drow += dpitch;
           if (mrow) mrow += p.mpitch;
@@ -156,48 +241,24 @@ __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, f
   cp_async_wait<0>();
 }
 
-// Interior and border CTAs run as two launches over the same grid (each CTA
-// returns at once in the launch that is not its own): the hot interior kernel
-// then carries only its own code and registers.
-template <int B, int NW>
-__device__ __forceinline__ bool harris_shfl_is_fast(const HarrisParams& p, int S) {
-  constexpr int A = B / 2, BB = B - 1 - A, TW = 120 * NW;
-  const int x0 = blockIdx.x * TW;
-  const int ly0 = blockIdx.y * S;
-  const int ly1 = min(ly0 + S, p.dst.H);
-  const int g0 = p.dst.y0 + ly0;
-  return x0 - 8 >= 0 && x0 + TW + 8 <= p.src.W && g0 - A - 1 >= 0 && g0 + (ly1 - ly0) + BB + 1 <= p.src.Hg;
-}
-
 template <int B, int NW>
 __global__ void __launch_bounds__(32 * NW) harris_shfl(HarrisParams p, int S) {
   extern __shared__ __align__(16) float smem[];
-  if (harris_shfl_is_fast<B, NW>(p, S)) harris_shfl_fast<B, NW>(p, S, smem);
-}
-
-template <int B, int NW>
-__global__ void __launch_bounds__(32 * NW) harris_shfl_border(HarrisParams p, int S) {
-  extern __shared__ __align__(16) float smem[];
-  if (!harris_shfl_is_fast<B, NW>(p, S)) harris_slow<B, 32 * NW, 4, 120 * NW, 8>(p, S, smem);
+  harris_shfl_fast<B, NW>(p, S, smem);
 }
 
 template <int B, int NW>
 static inline cudaError_t launch_hshfl(const HarrisParams& p, int batch, int S, cudaStream_t s) {
   constexpr int TW = 120 * NW;
   constexpr int ROWLEN = TW + 16;
-  const int rows = kHarStages > HarFastGeom<B>::NSR ? kHarStages : HarFastGeom<B>::NSR;
-  const size_t smem = (size_t)rows * ROWLEN * sizeof(float);
+  const size_t smem = (size_t)HarFastGeom<B>::NSR * ROWLEN * sizeof(float);
   auto kern = harris_shfl<B, NW>;
-  auto kernb = harris_shfl_border<B, NW>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(kernb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   dim3 grd((p.src.W + TW - 1) / TW, (p.dst.H + S - 1) / S, batch);
   kern<<<grd, 32 * NW, smem, s>>>(p, S);
-  count_launch();
-  kernb<<<grd, 32 * NW, smem, s>>>(p, S);
   count_launch();
   return cudaGetLastError();
 }
