@@ -132,7 +132,7 @@ static icl_status make_views(const icl_image* src, const icl_image* dst, const i
 }
 
 // ------------------------------------------------------------------ variants
-enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL };
+enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL, K_TILE2 };
 struct Variant {
   const char* name;
   Kind kind;
@@ -158,6 +158,8 @@ static const Variant kSepVariants[] = {
     {"stream_nt64_s16_v1", K_STREAM, 64, 1, 16},
     {"bulk_nt128_s64", K_BULK, 128, 4, 64},
     {"bulk_nt64_s64", K_BULK, 64, 4, 64},
+    {"tile64_v4", K_TILE2, 256, 4, 64},
+    {"tile64p_v4", K_TILE2, 256, 4, 1},
 };
 static const Variant kHarVariants[] = {
     {"naive_direct", K_NAIVE, 0, 0, 0},           {"stream_nt64_s64_v4", K_STREAM, 64, 4, 64},
@@ -203,7 +205,8 @@ struct Prepared {
 
 static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
   *why = ICL_ERR_UNSUPPORTED;
-  if ((v.kind == K_STREAM || v.kind == K_BULK || v.kind == K_SHFL) && v.vec == 4 && !pc.a16) return false;
+  if ((v.kind == K_STREAM || v.kind == K_BULK || v.kind == K_SHFL || v.kind == K_TILE2) && v.vec == 4 && !pc.a16)
+    return false;
   if (v.kind == K_SHFL && pc.har.block > 5) return false;
   if (pc.f == ICL_FILTER_SEPCONV && v.kind == K_STREAM &&
       sep_stream_smem_bytes(v.nt, pc.sep.rx > pc.sep.ry ? pc.sep.rx : pc.sep.ry) > 227 * 1024)
@@ -228,6 +231,7 @@ static cudaError_t run_variant(const Prepared& pc, const Variant& v, cudaStream_
       if (v.kind == K_NAIVE) return launch_sep_naive_direct(pc.sep, s);
       if (v.kind == K_TWOPASS) return launch_sep_naive_2pass(pc.sep, s);
       if (v.kind == K_BULK) return launch_sep_bulk(pc.sep, v.nt, v.S, s);
+      if (v.kind == K_TILE2) return launch_sep_tile(pc.sep, v.S == 1, s);
       return launch_sep_stream(pc.sep, v.nt, v.vec, v.S, s);
     case ICL_FILTER_HARRIS:
       if (v.kind == K_NAIVE) return launch_harris_naive(pc.har, s);
@@ -260,12 +264,14 @@ static int default_variant(const Prepared& pc) {
       if (!pc.a16) return variant_id(pc.f, pc.pixels < (1 << 20) ? "stream_nt64_s16_v1" : "stream_nt64_s64_v1");
       if (pc.pixels < (1 << 20)) return variant_id(pc.f, "stream_nt32_s8_v4");
       {
-        // the vertical halo 2R is re-read per S output rows: S grows with R
+        // the vertical halo 2R is re-read per S output rows: S grows with R;
+        // from R = 7 the register ring of stream<R> limits occupancy and the
+        // shared-memory tile kernel wins (16384^2 sweep)
         const int R = pc.sep.rx > pc.sep.ry ? pc.sep.rx : pc.sep.ry;
         if (R <= 2) return variant_id(pc.f, "stream_nt64_s16_v4");
         if (R <= 4) return variant_id(pc.f, "stream_nt64_s32_v4");
-        if (R <= 8) return variant_id(pc.f, "stream_nt64_s64_v4");
-        return variant_id(pc.f, "stream_nt64_s128_v4");
+        if (R <= 6) return variant_id(pc.f, "stream_nt64_s64_v4");
+        return variant_id(pc.f, "tile64p_v4");
       }
     case ICL_FILTER_HARRIS:
       if (!pc.a16) return variant_id(pc.f, "stream_nt64_s64_v1");

@@ -162,6 +162,61 @@ def test_sepconv_config_512():
         check_sepconv(host(dst), img, fx, fx, border, 0.0)
 
 
+@pytest.mark.parametrize("r", [7, 15])
+@pytest.mark.parametrize("border,c", [("constant", 0.7), ("clamp", 0.0)])
+def test_sepconv_tile_persistent_vs_oracle(r, border, c):
+    """More 64x64 tiles (2 x 18 x 21 = 756) than the persistent grid (2 CTAs per
+    SM = 296), ragged right / bottom tiles and padded pitch: exercises the
+    cp.async prefetch of the next tile (interior and border) in tile64p_v4."""
+    b, h, w = 2, 1300, 1100 + 37
+    imgs = np.stack([synth.uniform_image(40 + r + i, h, w) for i in range(b)])
+    fx, gy = synth.gaussian_taps(r), synth.signed_taps(9, r)
+    pitch = ((w + 3) // 4) * 4 + 12
+    sbuf = torch.full((b, h, pitch), float("nan"), device=DEV)
+    sbuf[:, :, :w] = torch.from_numpy(imgs).to(DEV)
+    src = sbuf[:, :, :w]
+
+    def call():
+        dbuf = torch.full((b, h, pitch), float("nan"), device=DEV)
+        icl.sepconv(src, dbuf[:, :, :w], fx, gy, border, c)
+        full = host(dbuf)
+        assert np.isnan(full[:, :, w:]).all(), "padding was written"
+        return full[:, :, :w]
+    outs = run_all_variants("sepconv", call, skip=("naive_2pass",))
+    assert "tile64p_v4" in outs and "tile64_v4" in outs
+    for i in range(b):
+        check_sepconv(outs["naive_direct"][i], imgs[i], fx, gy, border, c)
+    for name, o in outs.items():
+        np.testing.assert_array_equal(o, outs["naive_direct"], err_msg=f"variant {name} not bit-identical")
+
+
+@pytest.mark.parametrize("border", ["constant", "clamp"])
+def test_sepconv_bands_bit_exact_all_variants_r9(border):
+    """Row bands through every variant (incl. the tile kernels' global-row logic)."""
+    H, W, r = 700, 333, 9
+    img = synth.uniform_image(18, H, W)
+    fx = synth.gaussian_taps(r)
+    P = 336  # 16-byte pitch: every variant eligible
+    full = empty_like_dev(H, W, pitch=P)
+    icl.sepconv(to_dev(img, pitch=P), full, fx, fx, border, 0.3)
+    ref = host(full)
+    cuts = [0, 5, 250, 251, 699, 700]
+    for vid, name in variants("sepconv"):
+        if name == "naive_2pass":  # needs a workspace; covered elsewhere
+            continue
+        icl.force_variant("sepconv", vid)
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            s0, s1 = max(0, a - r), min(H, b + r)
+            dst = empty_like_dev(b - a, W, pitch=P)
+            try:
+                icl.sepconv(to_dev(img[s0:s1], pitch=P), dst, fx, fx, border, 0.3, band=(H, s0, a))
+            except icl.IclError as e:
+                if e.status in (3, 4):  # not eligible for this call
+                    continue
+                raise
+            np.testing.assert_array_equal(host(dst), ref[a:b], err_msg=f"{name} band {a}:{b}")
+
+
 @pytest.mark.parametrize("border", ["constant", "clamp"])
 def test_sepconv_bands_bit_exact(border):
     """Row bands (icl_band) stitched == the unsharded call, bit for bit."""

@@ -30,4 +30,15 @@ for (h, w) in [(61, 53), (130, 517), (9, 300)]:
                         raise
             torch.cuda.synchronize()
         icl.force_variant(f, None)
+# more 64x64 tiles than the persistent grid: the tile kernel's cp.async prefetch path
+img = torch.from_numpy(synth.uniform_image(2, 1300, 1100)).to(dev)
+out = torch.empty_like(img)
+for name in ("tile64p_v4", "tile64_v4"):
+    icl.force_variant("sepconv", name)
+    for border in ("constant", "clamp"):
+        for r in (7, 15):
+            fx = synth.gaussian_taps(r)
+            icl.sepconv(img, out, fx, fx, border, 0.5)
+    torch.cuda.synchronize()
+icl.force_variant("sepconv", None)
 print("sanitize cases done")
