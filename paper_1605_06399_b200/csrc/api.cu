@@ -30,6 +30,7 @@ bool nlm_tiled_supported(int P, int S);
 bool nlm_boxsum_supported(int P, int S);
 bool nlm_r8_supported(int P, int S);
 bool nlm_r16_supported(int P, int S);
+bool nlm_x2_supported(int P, int S);
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -132,7 +133,7 @@ static icl_status make_views(const icl_image* src, const icl_image* dst, const i
 }
 
 // ------------------------------------------------------------------ variants
-enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL, K_TILE2 };
+enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL, K_TILE2, K_BOXX2 };
 struct Variant {
   const char* name;
   Kind kind;
@@ -176,6 +177,7 @@ static const Variant kNlmVariants[] = {
     {"boxsum_32x32", K_BOXSUM, 32, 0, 32},
     {"boxsum_r8", K_BOXR8, 0, 0, 0},
     {"boxsum_r16", K_BOXR16, 0, 0, 0},
+    {"boxsum_x2", K_BOXX2, 0, 0, 0},
 };
 
 static const Variant* table(icl_filter f, int* n) {
@@ -222,6 +224,7 @@ static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXSUM && !nlm_boxsum_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXR8 && !nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXR16 && !nlm_r16_supported(pc.nlm.P, pc.nlm.S)) return false;
+  if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXX2 && !nlm_x2_supported(pc.nlm.P, pc.nlm.S)) return false;
   return true;
 }
 
@@ -242,6 +245,7 @@ static cudaError_t run_variant(const Prepared& pc, const Variant& v, cudaStream_
       if (v.kind == K_TILED) return launch_nlm_tiled(pc.nlm, v.nt, v.S, s);
       if (v.kind == K_BOXR8) return launch_nlm_r8(pc.nlm, s);
       if (v.kind == K_BOXR16) return launch_nlm_r16(pc.nlm, s);
+      if (v.kind == K_BOXX2) return launch_nlm_x2(pc.nlm, s);
       return launch_nlm_boxsum(pc.nlm, 0, s);
   }
   return cudaErrorInvalidValue;
@@ -278,6 +282,7 @@ static int default_variant(const Prepared& pc) {
       if (pc.pixels < (1 << 20)) return variant_id(pc.f, "stream_nt32_s16_v4");
       return variant_id(pc.f, pc.har.block <= 5 ? "shfl_nw2_s64" : "stream_nt64_s64_v4");
     case ICL_FILTER_NLM:
+      if (nlm_x2_supported(pc.nlm.P, pc.nlm.S)) return variant_id(pc.f, "boxsum_x2");
       if (nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return variant_id(pc.f, "boxsum_r8");
       return nlm_tiled_supported(pc.nlm.P, pc.nlm.S) ? variant_id(pc.f, "tiled_direct_32x8") : 0;
   }

@@ -62,6 +62,7 @@ cudaError_t launch_nlm_tiled(const NlmCall& c, int tw, int th, cudaStream_t s);
 cudaError_t launch_nlm_boxsum(const NlmCall& c, int variant, cudaStream_t s);
 cudaError_t launch_nlm_r8(const NlmCall& c, cudaStream_t s);
 cudaError_t launch_nlm_r16(const NlmCall& c, cudaStream_t s);
+cudaError_t launch_nlm_x2(const NlmCall& c, cudaStream_t s);
 
 // synthetic inputs
 cudaError_t launch_fill_uniform(float* base, int64_t W, int64_t H, int64_t pitch, int64_t batch,

@@ -145,6 +145,40 @@ __global__ void k_lds128(float* out) {
   }
   if (s == 1234.5f) out[0] = s;
 }
+template <int ILP>
+__global__ void k_shfl(float* out) {  // independent SHFL.IDX chains
+  float r[ILP];
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) r[i] = threadIdx.x * 1e-3f + i;
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < ILP; ++i) r[i] = __shfl_down_sync(0xffffffffu, r[i], 1 + (i & 3));
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) s += r[i];
+  if (s == 1234.5f) out[0] = s;
+}
+// 4 SHFL + 4 conflict-free LDS.32 per iteration: do they share the LSU/MIO path?
+__global__ void k_shfl_lds(float* out) {
+  __shared__ float sm[4096];
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) sm[i] = i;
+  __syncthreads();
+  float r[4], s = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) r[i] = threadIdx.x * 1e-3f + i;
+  int idx = threadIdx.x;
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r[i] = __shfl_down_sync(0xffffffffu, r[i], 1 + i);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s += sm[(idx + k * 32) & 4095];
+    idx += 1;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) s += r[i];
+  if (s == 1234.5f) out[0] = s;
+}
 
 template <typename F>
 double run(F launch, double ops_per_thread_iter, int blocks, int threads) {
@@ -185,5 +219,9 @@ int main() {
   printf("LDS.32 (conflict-free)    : %7.2f Tinst/s  %6.1f words/clk/SM\n", r / 1e12, r / per_sm_clk);
   r = run([&] { k_lds128<<<B, T>>>(d); }, 8, B, T);
   printf("LDS.128 (conflict-free)   : %7.2f Tinst/s  %6.1f words/clk/SM\n", r / 1e12, 4 * r / per_sm_clk);
+  r = run([&] { k_shfl<8><<<B, T>>>(d); }, 8, B, T);
+  printf("SHFL.DOWN (independent)   : %7.2f Tinst/s  %6.1f lanes/clk/SM\n", r / 1e12, r / per_sm_clk);
+  r = run([&] { k_shfl_lds<<<B, T>>>(d); }, 8, B, T);
+  printf("4 SHFL + 4 LDS.32         : %7.2f Tinst/s  %6.1f lane-ops/clk/SM\n", r / 1e12, r / per_sm_clk);
   return 0;
 }

@@ -1,0 +1,40 @@
+"""Write profiles/ncu_traffic.json (DRAM bytes per pixel of each hot kernel) from
+`ncu --set full` reports of tools/ncu_capture.sh (bench.py --batch B, one
+B x 4096^2 launch per filter).  bench.py multiplies bytes_per_px by the pixels
+of its own launch to report roofline.traffic.
+
+  python tools/ncu_traffic.py --px 33554432 nlm=gpurun_out/ncu_r01c/full_nlm_box_x2.ncu-rep ...
+"""
+import argparse
+import csv
+import io
+import json
+import os
+import subprocess
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--px", type=int, required=True, help="pixels per captured launch")
+ap.add_argument("--tag", default="")
+ap.add_argument("reports", nargs="+", help="filter=path.ncu-rep")
+a = ap.parse_args()
+out = {"_note": ("dram__bytes_read.sum + dram__bytes_write.sum per pixel from one ncu --set full capture per "
+                 f"kernel ({a.tag}); bench.py scales by the pixels of its launch. Writes still dirty in L2 at "
+                 "kernel end are not counted, so traffic can read slightly below the algorithmic 8 / 9 B/px.")}
+for spec in a.reports:
+    f, path = spec.split("=", 1)
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, val = rows[0], rows[1], rows[2]
+    d = dict(zip(hdr, zip(val, units)))
+
+    def num(key):
+        v, u = d[key]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
+        return float(v.replace(",", "")) * scale
+    rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
+    out[f] = {"bytes_per_px": round((rd + wr) / a.px, 3), "kernel": d["Kernel Name"][0], "report": os.path.basename(path)}
+path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
+with open(path, "w") as fh:
+    json.dump(out, fh, indent=1)
+    fh.write("\n")
+print(json.dumps(out, indent=1))
