@@ -59,8 +59,18 @@ typedef enum { ICL_BORDER_CONSTANT = 0, ICL_BORDER_CLAMP = 1 } icl_border;
 
 typedef enum { ICL_FILTER_SEPCONV = 0, ICL_FILTER_HARRIS = 1, ICL_FILTER_NLM = 2 } icl_filter;
 
-/* A (batch of) 2-D image(s).  `data` is a device pointer (fp32 pixels for
- * images, uint8 for masks).  width, height >= 1 and < 2^31; pitch_bytes >=
+/* A (batch of) 2-D image(s).  `data` is a device pointer or a HOST pointer
+ * (fp32 pixels for images, uint8 for masks).  When any operand of
+ * icl_sepconv / icl_harris / icl_nlm is host memory (pinned, or pageable --
+ * pageable copies are staged synchronously by the driver), the call streams
+ * the batch through the GPU in row bands of ~16 MiB: H2D of a band's input
+ * rows (+ stencil halo) into library-owned device staging buffers, the filter
+ * on that band (icl_band semantics: results equal the device-resident call,
+ * bit for bit for sepconv and Harris), D2H of its output; the three stages of
+ * consecutive bands overlap on three library streams forked from and joined
+ * back into `stream`.  Host buffers must stay valid until `stream` reaches
+ * the call (icl_transfer_bytes counts the bytes moved).  Device-resident
+ * operands are used in place.  width, height >= 1 and < 2^31; pitch_bytes >=
  * width*elem_size and a multiple of elem_size; batch >= 1; when batch > 1,
  * batch_stride_bytes >= height*pitch_bytes (images must not overlap). */
 typedef struct {
@@ -179,6 +189,7 @@ typedef struct {
  * variant (bit-exact for sepconv, tolerance for Harris/NLM), cache the
  * fastest per problem key (ties within 0.5% -> lower id).  Synchronises.
  * Leaves the winner's result in dst. */
+/* (device-resident images only; host images -> ICL_ERR_INVALID_ARG) */
 icl_status icl_tune(const icl_problem* problem, unsigned flags, void* stream, icl_variant_info* chosen);
 
 /* Persist / restore the winner cache (JSON; keyed by device name, SM count
@@ -205,6 +216,10 @@ int icl_last_variant(icl_filter filter);
 /* Number of kernel launches this library issued on the calling process since
  * load (for the bench's gpu_launches claim). */
 uint64_t icl_launch_count(void);
+
+/* Cumulative host->device / device->host bytes the host-image path copied
+ * (either pointer may be NULL). */
+void icl_transfer_bytes(uint64_t* h2d, uint64_t* d2h);
 
 /* ------------------------------------------------------------------------
  * Misc

@@ -28,7 +28,7 @@ FILTER = {"sepconv": 0, "harris": 1, "nlm": 2}
 EXPORTS = ("icl_sepconv", "icl_sepconv_workspace_bytes", "icl_harris", "icl_nlm", "icl_tune",
            "icl_tune_cache_save", "icl_tune_cache_load", "icl_tune_cache_clear", "icl_tune_cache_size",
            "icl_variant_count", "icl_variant_name", "icl_force_variant", "icl_last_variant",
-           "icl_launch_count", "icl_last_error", "icl_version", "icl_fill_uniform")
+           "icl_launch_count", "icl_transfer_bytes", "icl_last_error", "icl_version", "icl_fill_uniform")
 
 
 class IclError(RuntimeError):
@@ -90,6 +90,7 @@ def load_library(path: str = LIB_PATH):
         "icl_force_variant": ([I, I], I),
         "icl_last_variant": ([I], I),
         "icl_launch_count": ([], ctypes.c_uint64),
+        "icl_transfer_bytes": ([ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)], None),
         "icl_last_error": ([], ctypes.c_char_p),
         "icl_version": ([], ctypes.c_char_p),
         "icl_fill_uniform": ([img, ctypes.c_uint64, I64, P], I),
@@ -108,13 +109,22 @@ def _check(status: int):
 
 
 # ----------------------------------------------------------------------------- marshalling
-def _image(t, elem: int = 4) -> icl_image:
-    """icl_image descriptor of a CUDA tensor (H, W) or (B, H, W)."""
+def _image(t, elem: int = 4, host_ok: bool = False) -> icl_image:
+    """icl_image descriptor of a tensor (H, W) or (B, H, W).
+
+    CUDA tensors are passed as device images.  With ``host_ok`` (the three
+    filter calls) a CPU tensor -- ideally pinned -- is passed as a HOST image:
+    the library streams it through the GPU in row bands (include/icl.h); the
+    computation always runs in the CUDA kernels, there is no CPU fallback."""
     import torch
     if not isinstance(t, torch.Tensor):
         raise TypeError("images are torch tensors")
     if not t.is_cuda:
-        raise ValueError("images must live on a CUDA device (no CPU fallback)")
+        if not host_ok:
+            raise ValueError("this call needs images on a CUDA device")
+        if not torch.cuda.is_available():
+            raise ValueError("host images are streamed through a CUDA device, and none is available "
+                             "(there is no CPU fallback)")
     if t.element_size() != elem:
         raise TypeError(f"expected element size {elem}, got {t.dtype}")
     if t.dim() not in (2, 3) or t.stride(-1) != 1:
@@ -155,7 +165,7 @@ def sepconv(src, dst, taps_x: Sequence[float], taps_y: Sequence[float], border: 
     """Separable convolution (icl_sepconv).  Returns dst."""
     lib = load_library()
     fx, gy = _taps(taps_x), _taps(taps_y)
-    s, d = _image(src), _image(dst)
+    s, d = _image(src, host_ok=True), _image(dst, host_ok=True)
     ws = workspace.data_ptr() if workspace is not None else None
     wsb = workspace.numel() * workspace.element_size() if workspace is not None else 0
     _check(lib.icl_sepconv(ctypes.byref(s), ctypes.byref(d), ctypes.cast(fx, ctypes.c_void_p), len(fx) // 2,
@@ -172,8 +182,8 @@ def harris(src, response, block: int = 5, k: float = 0.04, border: str = "clamp"
            mask=None, threshold: float = 0.0, band=None, stream=None):
     """Harris response (+ optional uint8 mask R > threshold) (icl_harris)."""
     lib = load_library()
-    s, r = _image(src), _image(response)
-    m = _image(mask, 1) if mask is not None else None
+    s, r = _image(src, host_ok=True), _image(response, host_ok=True)
+    m = _image(mask, 1, host_ok=True) if mask is not None else None
     _check(lib.icl_harris(ctypes.byref(s), ctypes.byref(r), block, k, BORDER[border], border_value, _ref(m),
                           threshold, _ref(_band(band)), _stream(stream)))
     return response
@@ -183,7 +193,7 @@ def nlm(src, dst, patch_radius: int = 2, search_radius: int = 5, h: float = 0.1,
         border_value: float = 0.0, band=None, stream=None):
     """Non-local means (icl_nlm; R11-R14)."""
     lib = load_library()
-    s, d = _image(src), _image(dst)
+    s, d = _image(src, host_ok=True), _image(dst, host_ok=True)
     _check(lib.icl_nlm(ctypes.byref(s), ctypes.byref(d), patch_radius, search_radius, h, BORDER[border],
                        border_value, _ref(_band(band)), _stream(stream)))
     return dst
@@ -265,6 +275,13 @@ def launch_count() -> int:
     return int(load_library().icl_launch_count())
 
 
+def transfer_bytes() -> tuple:
+    """Cumulative (host->device, device->host) bytes copied by the host-image path."""
+    h, d = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    load_library().icl_transfer_bytes(ctypes.byref(h), ctypes.byref(d))
+    return int(h.value), int(d.value)
+
+
 def version() -> str:
     return load_library().icl_version().decode()
 
@@ -287,6 +304,6 @@ def nlm_halo(patch_radius: int, search_radius: int):
 
 
 __all__ = ["sepconv", "harris", "nlm", "tune", "tune_cache_save", "tune_cache_load", "tune_cache_clear",
-           "tune_cache_size", "variant_names", "force_variant", "last_variant", "launch_count", "version",
+           "tune_cache_size", "variant_names", "force_variant", "last_variant", "launch_count", "transfer_bytes", "version",
            "fill_uniform", "load_library", "IclError", "sepconv_workspace_bytes", "harris_halo", "nlm_halo",
            "EXPORTS", "LIB_PATH"]

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <sstream>
@@ -609,6 +610,190 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
   return st;
 }
 
+// ------------------------------------------------------------------ host images
+// A call whose src / dst / mask data pointer is HOST memory (pinned or
+// pageable) streams the images through the GPU in row bands: band k's input
+// rows (plus the stencil halo) are copied H2D into one of NSET device staging
+// sets, the filter runs on that band through the icl_band path (so sepconv /
+// Harris results equal the device-resident call bit for bit), and the band's
+// output is copied D2H -- H2D of band k+1, compute of band k and D2H of band
+// k-1 overlap on three library streams.  The work forks from and joins back
+// into the caller's stream, so stream order and events on it bracket the
+// whole transfer + compute.  Device-resident operands are used in place.
+static std::atomic<uint64_t> g_h2d_bytes{0}, g_d2h_bytes{0};
+
+static bool is_host_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;  // unknown to CUDA: plain host memory
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
+}
+
+namespace {
+constexpr int kNSet = 3;
+struct Stager {
+  std::mutex mu;
+  cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+  cudaEvent_t in_ready[kNSet], comp_done[kNSet], out_done[kNSet], fork, join_c, join_d;
+  char* buf = nullptr;
+  size_t cap = 0;
+  bool init = false;
+};
+std::mutex g_stagers_mu;
+std::map<int, Stager*> g_stagers;
+}  // namespace
+
+static Stager* stager_for_current_device(icl_status* st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    *st = cuda_fail(e, "host path: cudaGetDevice");
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_stagers_mu);
+  Stager*& sg = g_stagers[dev];
+  if (!sg) sg = new Stager();
+  return sg;
+}
+
+static int64_t round16(int64_t b) { return (b + 15) / 16 * 16; }
+
+using ChunkCall = std::function<icl_status(const icl_image*, const icl_image*, const icl_image*, const icl_band*,
+                                           cudaStream_t)>;
+
+// src/dst/mask validated by the caller's prep_*; up/down = stencil rows.
+static icl_status run_host(const icl_image* src, const icl_image* dst, const icl_image* mask, const icl_band* band,
+                           int up, int down, const ChunkCall& call, cudaStream_t user) {
+  icl_status st = ICL_OK;
+  Stager* sg = stager_for_current_device(&st);
+  if (!sg) return st;
+  std::lock_guard<std::mutex> lk(sg->mu);
+  cudaError_t e = cudaSuccess;
+  if (!sg->init) {
+    const unsigned fl = cudaEventDisableTiming;
+    if ((e = cudaStreamCreateWithFlags(&sg->h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&sg->comp, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&sg->d2h, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "host path: stream create");
+    for (int i = 0; i < kNSet; ++i) {
+      if ((e = cudaEventCreateWithFlags(&sg->in_ready[i], fl)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&sg->comp_done[i], fl)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&sg->out_done[i], fl)) != cudaSuccess)
+        return cuda_fail(e, "host path: event create");
+    }
+    if ((e = cudaEventCreateWithFlags(&sg->fork, fl)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&sg->join_c, fl)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&sg->join_d, fl)) != cudaSuccess)
+      return cuda_fail(e, "host path: event create");
+    sg->init = true;
+  }
+  const bool src_h = is_host_ptr(src->data), dst_h = is_host_ptr(dst->data);
+  const bool msk_h = mask && mask->data && is_host_ptr(mask->data);
+  const int64_t W = src->width, B = src->batch;
+  const int64_t Hg = band ? band->global_height : src->height;
+  const int64_t sy0 = band ? band->src_y0 : 0, dy0 = band ? band->dst_y0 : 0;
+  const int64_t rows_out = dst->height;
+  // rows per band: ~16 MiB of output (ICL_HOST_CHUNK_ROWS overrides, for tests)
+  int64_t CH = std::max<int64_t>(1, (16ll << 20) / (W * 4));
+  if (const char* env = std::getenv("ICL_HOST_CHUNK_ROWS")) CH = std::max<int64_t>(1, std::atoll(env));
+  CH = std::min(CH, rows_out);
+  const int64_t spitch = round16(W * 4), dpitch = round16(W * 4), mpitch = round16(W);
+  const size_t in_bytes = src_h ? (size_t)(CH + up + down) * spitch : 0;
+  const size_t out_bytes = dst_h ? (size_t)CH * dpitch : 0;
+  const size_t m_bytes = msk_h ? (size_t)CH * mpitch : 0;
+  const size_t set_bytes = round16(in_bytes) + round16(out_bytes) + round16(m_bytes);
+  if (set_bytes * kNSet > sg->cap) {
+    // previous calls' copies may still read the old staging buffer
+    cudaStreamSynchronize(sg->h2d);
+    cudaStreamSynchronize(sg->comp);
+    cudaStreamSynchronize(sg->d2h);
+    if (sg->buf) cudaFree(sg->buf);
+    sg->buf = nullptr;
+    sg->cap = 0;
+    if ((e = cudaMalloc(&sg->buf, set_bytes * kNSet)) != cudaSuccess) return cuda_fail(e, "host path: staging");
+    sg->cap = set_bytes * kNSet;
+  }
+  auto set_in = [&](int k) { return sg->buf + k * set_bytes; };
+  auto set_out = [&](int k) { return sg->buf + k * set_bytes + round16(in_bytes); };
+  auto set_msk = [&](int k) { return sg->buf + k * set_bytes + round16(in_bytes) + round16(out_bytes); };
+  if ((e = cudaEventRecord(sg->fork, user)) != cudaSuccess) return cuda_fail(e, "host path: fork");
+  cudaStreamWaitEvent(sg->h2d, sg->fork, 0);
+  cudaStreamWaitEvent(sg->comp, sg->fork, 0);
+  cudaStreamWaitEvent(sg->d2h, sg->fork, 0);
+  const int64_t sb = src->batch > 1 ? src->batch_stride_bytes : 0;
+  const int64_t db = dst->batch > 1 ? dst->batch_stride_bytes : 0;
+  const int64_t mb = (mask && mask->batch > 1) ? mask->batch_stride_bytes : 0;
+  uint64_t h2d = 0, d2h = 0;
+  int64_t k = 0;
+  for (int64_t b = 0; b < B && st == ICL_OK; ++b) {
+    for (int64_t a = dy0; a < dy0 + rows_out && st == ICL_OK; a += CH, ++k) {
+      const int64_t ee = std::min(a + CH, dy0 + rows_out);
+      const int64_t lo = std::max(std::max<int64_t>(0, a - up), sy0);
+      const int64_t hi = std::min(std::min(Hg, ee + down), sy0 + src->height);
+      const int set = (int)(k % kNSet);
+      const bool reuse = k >= kNSet;
+      const char* sptr = static_cast<const char*>(src->data) + b * sb + (lo - sy0) * src->pitch_bytes;
+      char* dptr = static_cast<char*>(dst->data) + b * db + (a - dy0) * dst->pitch_bytes;
+      char* mptr = mask && mask->data ? static_cast<char*>(mask->data) + b * mb + (a - dy0) * mask->pitch_bytes
+                                      : nullptr;
+      icl_image iv{const_cast<char*>(sptr), W, hi - lo, src->pitch_bytes, 1, 0};
+      icl_image ov{dptr, W, ee - a, dst->pitch_bytes, 1, 0};
+      icl_image mv{mptr, W, ee - a, mask ? mask->pitch_bytes : 0, 1, 0};
+      if (src_h) {
+        if (reuse) cudaStreamWaitEvent(sg->h2d, sg->comp_done[set], 0);
+        e = cudaMemcpy2DAsync(set_in(set), spitch, sptr, src->pitch_bytes, W * 4, hi - lo, cudaMemcpyHostToDevice,
+                              sg->h2d);
+        if (e != cudaSuccess) { st = cuda_fail(e, "host path: H2D"); break; }
+        cudaEventRecord(sg->in_ready[set], sg->h2d);
+        cudaStreamWaitEvent(sg->comp, sg->in_ready[set], 0);
+        iv.data = set_in(set);
+        iv.pitch_bytes = spitch;
+        h2d += (uint64_t)(W * 4) * (hi - lo);
+      }
+      if ((dst_h || msk_h) && reuse) cudaStreamWaitEvent(sg->comp, sg->out_done[set], 0);
+      if (dst_h) { ov.data = set_out(set); ov.pitch_bytes = dpitch; }
+      if (msk_h) { mv.data = set_msk(set); mv.pitch_bytes = mpitch; }
+      const icl_band bc{Hg, lo, a};
+      st = call(&iv, &ov, mask && mask->data ? &mv : nullptr, &bc, sg->comp);
+      if (st != ICL_OK) break;
+      cudaEventRecord(sg->comp_done[set], sg->comp);
+      if (dst_h || msk_h) {
+        cudaStreamWaitEvent(sg->d2h, sg->comp_done[set], 0);
+        if (dst_h) {
+          e = cudaMemcpy2DAsync(dptr, dst->pitch_bytes, set_out(set), dpitch, W * 4, ee - a, cudaMemcpyDeviceToHost,
+                                sg->d2h);
+          if (e != cudaSuccess) { st = cuda_fail(e, "host path: D2H"); break; }
+          d2h += (uint64_t)(W * 4) * (ee - a);
+        }
+        if (msk_h) {
+          e = cudaMemcpy2DAsync(mptr, mask->pitch_bytes, set_msk(set), mpitch, W, ee - a, cudaMemcpyDeviceToHost,
+                                sg->d2h);
+          if (e != cudaSuccess) { st = cuda_fail(e, "host path: D2H mask"); break; }
+          d2h += (uint64_t)W * (ee - a);
+        }
+        cudaEventRecord(sg->out_done[set], sg->d2h);
+      }
+    }
+  }
+  // join (also on error: nothing of this call may outlive the caller's stream order)
+  cudaEventRecord(sg->join_c, sg->comp);
+  cudaEventRecord(sg->join_d, sg->d2h);
+  cudaStreamWaitEvent(sg->h2d, sg->join_c, 0);  // the h2d stream is drained by the compute it feeds
+  cudaStreamWaitEvent(user, sg->join_c, 0);
+  cudaStreamWaitEvent(user, sg->join_d, 0);
+  g_h2d_bytes.fetch_add(h2d);
+  g_d2h_bytes.fetch_add(d2h);
+  if (st == ICL_OK && (e = cudaGetLastError()) != cudaSuccess) st = cuda_fail(e, "host path");
+  return st;
+}
+
+static bool any_host(const icl_image* a, const icl_image* b, const icl_image* c) {
+  return (a && a->data && is_host_ptr(a->data)) || (b && b->data && is_host_ptr(b->data)) ||
+         (c && c->data && is_host_ptr(c->data));
+}
+
 }  // namespace icl
 
 using namespace icl;
@@ -623,6 +808,13 @@ icl_status icl_sepconv(const icl_image* src, const icl_image* dst, const float* 
   icl_status st = prep_sepconv(src, dst, taps_x, rx, taps_y, ry, border, border_value, band, workspace,
                                workspace_bytes, &pc);
   if (st != ICL_OK) return st;
+  if (any_host(src, dst, nullptr)) {
+    return run_host(src, dst, nullptr, band, ry, ry,
+                    [&](const icl_image* s, const icl_image* d, const icl_image*, const icl_band* b, cudaStream_t cs) {
+                      return icl_sepconv(s, d, taps_x, rx, taps_y, ry, border, border_value, b, nullptr, 0, cs);
+                    },
+                    static_cast<cudaStream_t>(stream));
+  }
   return dispatch(pc, static_cast<cudaStream_t>(stream));
 }
 
@@ -637,6 +829,14 @@ icl_status icl_harris(const icl_image* src, const icl_image* response, int block
   Prepared pc;
   icl_status st = prep_harris(src, response, block, k, border, border_value, mask, threshold, band, &pc);
   if (st != ICL_OK) return st;
+  if (any_host(src, response, mask)) {
+    const int a = block / 2, bb = block - 1 - a;
+    return run_host(src, response, mask, band, a + 1, bb + 1,
+                    [&](const icl_image* s, const icl_image* d, const icl_image* m, const icl_band* b, cudaStream_t cs) {
+                      return icl_harris(s, d, block, k, border, border_value, m, threshold, b, cs);
+                    },
+                    static_cast<cudaStream_t>(stream));
+  }
   return dispatch(pc, static_cast<cudaStream_t>(stream));
 }
 
@@ -645,11 +845,21 @@ icl_status icl_nlm(const icl_image* src, const icl_image* dst, int patch_radius,
   Prepared pc;
   icl_status st = prep_nlm(src, dst, patch_radius, search_radius, h, border, border_value, band, &pc);
   if (st != ICL_OK) return st;
+  if (any_host(src, dst, nullptr)) {
+    const int r = patch_radius + search_radius;
+    return run_host(src, dst, nullptr, band, r, r,
+                    [&](const icl_image* s, const icl_image* d, const icl_image*, const icl_band* b, cudaStream_t cs) {
+                      return icl_nlm(s, d, patch_radius, search_radius, h, border, border_value, b, cs);
+                    },
+                    static_cast<cudaStream_t>(stream));
+  }
   return dispatch(pc, static_cast<cudaStream_t>(stream));
 }
 
 icl_status icl_tune(const icl_problem* p, unsigned flags, void* stream, icl_variant_info* chosen) {
   if (!p) return fail(ICL_ERR_INVALID_ARG, "null problem");
+  if (any_host(&p->src, &p->dst, p->filter == ICL_FILTER_HARRIS ? &p->mask : nullptr))
+    return fail(ICL_ERR_INVALID_ARG, "icl_tune needs device-resident images");
   Prepared pc;
   icl_status st;
   switch (p->filter) {
@@ -754,6 +964,11 @@ int icl_last_variant(icl_filter filter) {
 
 uint64_t icl_launch_count(void) { return g_launches.load(); }
 
+void icl_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
+  if (h2d) *h2d = g_h2d_bytes.load();
+  if (d2h) *d2h = g_d2h_bytes.load();
+}
+
 const char* icl_last_error(void) { return t_err.c_str(); }
 
 const char* icl_version(void) { return ICL_VERSION_STRING; }
@@ -761,6 +976,7 @@ const char* icl_version(void) { return ICL_VERSION_STRING; }
 icl_status icl_fill_uniform(const icl_image* img, uint64_t seed, int64_t row0, void* stream) {
   icl_status st = check_image(img, 4, "img");
   if (st != ICL_OK) return st;
+  if (is_host_ptr(img->data)) return fail(ICL_ERR_INVALID_ARG, "icl_fill_uniform needs a device image");
   cudaError_t e = launch_fill_uniform(static_cast<float*>(img->data), img->width, img->height, img->pitch_bytes,
                                       img->batch, img->batch > 1 ? img->batch_stride_bytes : 0, seed, row0,
                                       static_cast<cudaStream_t>(stream));

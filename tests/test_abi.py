@@ -80,8 +80,14 @@ def test_invalid_arguments_fail_before_any_launch():
     assert st == 3  # radius > 15
 
 
-def test_cpu_tensors_are_rejected():
+def test_cpu_tensors_need_a_cuda_device():
+    """CPU tensors are host images streamed through the GPU; without a CUDA
+    device the binding refuses them (no CPU fallback)."""
     import torch
+    if torch.cuda.is_available():
+        pytest.skip("host-image path is exercised by tests/test_gpu_host.py")
     t = torch.zeros(8, 8)
     with pytest.raises(ValueError, match="CUDA"):
         icl.sepconv(t, t.clone(), [1.0], [1.0])
+    with pytest.raises(ValueError, match="CUDA"):
+        icl.fill_uniform(t, 1)
