@@ -639,6 +639,7 @@ struct Stager {
   cudaEvent_t in_ready[kNSet], comp_done[kNSet], out_done[kNSet], fork, join_c, join_d;
   char* buf = nullptr;
   size_t cap = 0;
+  uint64_t seq = 0;  // bands issued so far (all calls): staging set = seq % kNSet
   bool init = false;
 };
 std::mutex g_stagers_mu;
@@ -715,9 +716,12 @@ static icl_status run_host(const icl_image* src, const icl_image* dst, const icl
     if ((e = cudaMalloc(&sg->buf, set_bytes * kNSet)) != cudaSuccess) return cuda_fail(e, "host path: staging");
     sg->cap = set_bytes * kNSet;
   }
-  auto set_in = [&](int k) { return sg->buf + k * set_bytes; };
-  auto set_out = [&](int k) { return sg->buf + k * set_bytes + round16(in_bytes); };
-  auto set_msk = [&](int k) { return sg->buf + k * set_bytes + round16(in_bytes) + round16(out_bytes); };
+  // fixed set stride: a set's region never moves between calls, whatever
+  // their in/out/mask sizes, so the per-set events protect all of it
+  const size_t stride = sg->cap / kNSet;
+  auto set_in = [&](int k) { return sg->buf + k * stride; };
+  auto set_out = [&](int k) { return sg->buf + k * stride + round16(in_bytes); };
+  auto set_msk = [&](int k) { return sg->buf + k * stride + round16(in_bytes) + round16(out_bytes); };
   if ((e = cudaEventRecord(sg->fork, user)) != cudaSuccess) return cuda_fail(e, "host path: fork");
   cudaStreamWaitEvent(sg->h2d, sg->fork, 0);
   cudaStreamWaitEvent(sg->comp, sg->fork, 0);
@@ -726,14 +730,14 @@ static icl_status run_host(const icl_image* src, const icl_image* dst, const icl
   const int64_t db = dst->batch > 1 ? dst->batch_stride_bytes : 0;
   const int64_t mb = (mask && mask->batch > 1) ? mask->batch_stride_bytes : 0;
   uint64_t h2d = 0, d2h = 0;
-  int64_t k = 0;
   for (int64_t b = 0; b < B && st == ICL_OK; ++b) {
-    for (int64_t a = dy0; a < dy0 + rows_out && st == ICL_OK; a += CH, ++k) {
+    for (int64_t a = dy0; a < dy0 + rows_out && st == ICL_OK; a += CH) {
       const int64_t ee = std::min(a + CH, dy0 + rows_out);
       const int64_t lo = std::max(std::max<int64_t>(0, a - up), sy0);
       const int64_t hi = std::min(std::min(Hg, ee + down), sy0 + src->height);
-      const int set = (int)(k % kNSet);
-      const bool reuse = k >= kNSet;
+      // staging sets rotate across calls too (a call issued from another user
+      // stream may still be using them): always wait for the set's last users
+      const int set = (int)(sg->seq++ % kNSet);
       const char* sptr = static_cast<const char*>(src->data) + b * sb + (lo - sy0) * src->pitch_bytes;
       char* dptr = static_cast<char*>(dst->data) + b * db + (a - dy0) * dst->pitch_bytes;
       char* mptr = mask && mask->data ? static_cast<char*>(mask->data) + b * mb + (a - dy0) * mask->pitch_bytes
@@ -742,7 +746,9 @@ static icl_status run_host(const icl_image* src, const icl_image* dst, const icl
       icl_image ov{dptr, W, ee - a, dst->pitch_bytes, 1, 0};
       icl_image mv{mptr, W, ee - a, mask ? mask->pitch_bytes : 0, 1, 0};
       if (src_h) {
-        if (reuse) cudaStreamWaitEvent(sg->h2d, sg->comp_done[set], 0);
+        // the whole set must be free: its previous band's kernel and D2H
+        cudaStreamWaitEvent(sg->h2d, sg->comp_done[set], 0);
+        cudaStreamWaitEvent(sg->h2d, sg->out_done[set], 0);
         e = cudaMemcpy2DAsync(set_in(set), spitch, sptr, src->pitch_bytes, W * 4, hi - lo, cudaMemcpyHostToDevice,
                               sg->h2d);
         if (e != cudaSuccess) { st = cuda_fail(e, "host path: H2D"); break; }
@@ -752,7 +758,7 @@ static icl_status run_host(const icl_image* src, const icl_image* dst, const icl
         iv.pitch_bytes = spitch;
         h2d += (uint64_t)(W * 4) * (hi - lo);
       }
-      if ((dst_h || msk_h) && reuse) cudaStreamWaitEvent(sg->comp, sg->out_done[set], 0);
+      cudaStreamWaitEvent(sg->comp, sg->out_done[set], 0);  // set outputs drained by the previous D2H
       if (dst_h) { ov.data = set_out(set); ov.pitch_bytes = dpitch; }
       if (msk_h) { mv.data = set_msk(set); mv.pitch_bytes = mpitch; }
       const icl_band bc{Hg, lo, a};

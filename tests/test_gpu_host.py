@@ -133,3 +133,55 @@ def test_tune_rejects_host_images():
     t = host(np.zeros((16, 16), np.float32))
     with pytest.raises(ValueError):
         icl.tune("sepconv", t, t, taps_x=[1.0], taps_y=[1.0])
+
+
+def test_host_calls_from_several_streams(monkeypatch):
+    """Three host calls issued on three user streams share the library's
+    staging sets; their bands interleave on the copy / compute streams and
+    every result must still equal the device call (staging-set reuse waits
+    on the set's previous users across calls)."""
+    monkeypatch.setenv("ICL_HOST_CHUNK_ROWS", "16")
+    h, w = 300, 200
+    imgs = [synth.uniform_image(90 + i, h, w) for i in range(3)]
+    fx = synth.gaussian_taps(3)
+    refs = []
+    for im in imgs:
+        r = torch.empty(h, w, device=DEV)
+        icl.sepconv(torch.from_numpy(im).to(DEV), r, fx, fx, "clamp")
+        refs.append(r.cpu().numpy())
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    for rep in range(3):
+        srcs = [host(im) for im in imgs]
+        dsts = [host(np.full((h, w), np.nan, np.float32)) for _ in imgs]
+        for s, a, b in zip(streams, srcs, dsts):
+            icl.sepconv(a, b, fx, fx, "clamp", stream=s)
+        torch.cuda.synchronize()
+        for b, r in zip(dsts, refs):
+            np.testing.assert_array_equal(b.numpy(), r)
+
+
+def test_mixed_filters_from_several_streams(monkeypatch):
+    """sepconv / Harris+mask / NLM host calls on three streams: their staging
+    layouts differ (halo rows, mask region) yet share the rotating sets."""
+    monkeypatch.setenv("ICL_HOST_CHUNK_ROWS", "24")
+    h, w = 160, 180
+    a, b, c = (synth.rect_scene(95 + i, h, w, n_rect=12, noise=0.05) for i in range(3))
+    fx = synth.gaussian_taps(2)
+    ra, rb, rc = (torch.empty(h, w, device=DEV) for _ in range(3))
+    rm = torch.empty(h, w, dtype=torch.uint8, device=DEV)
+    icl.sepconv(torch.from_numpy(a).to(DEV), ra, fx, fx, "constant")
+    icl.harris(torch.from_numpy(b).to(DEV), rb, 5, 0.04, "clamp", mask=rm, threshold=0.2)
+    icl.nlm(torch.from_numpy(c).to(DEV), rc, 2, 5, 0.1, "clamp")
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    for rep in range(3):
+        oa, ob, oc = (host(np.full((h, w), np.nan, np.float32)) for _ in range(3))
+        om = torch.full((h, w), 9, dtype=torch.uint8).pin_memory()
+        ha, hb, hc = host(a), host(b), host(c)  # host inputs must outlive the asynchronous calls
+        icl.sepconv(ha, oa, fx, fx, "constant", stream=streams[0])
+        icl.harris(hb, ob, 5, 0.04, "clamp", mask=om, threshold=0.2, stream=streams[1])
+        icl.nlm(hc, oc, 2, 5, 0.1, "clamp", stream=streams[2])
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(oa.numpy(), ra.cpu().numpy())
+        np.testing.assert_array_equal(ob.numpy(), rb.cpu().numpy())
+        np.testing.assert_array_equal(om.numpy(), rm.cpu().numpy())
+        np.testing.assert_allclose(oc.numpy(), rc.cpu().numpy(), rtol=0, atol=2e-5)
