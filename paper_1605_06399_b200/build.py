@@ -46,7 +46,8 @@ def _deps_mtime():
 
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(BUILD, src[:-3] + ".o")
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+    extra = os.environ.get("ICL_NVCC_EXTRA", "").split()  # experiments only (e.g. -D tuning macros)
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -18,6 +18,10 @@
 #pragma once
 #include "harris_stream.cuh"
 
+#ifndef ICL_HSHFL_MINB
+#define ICL_HSHFL_MINB 1
+#endif
+
 namespace icl {
 
 template <int B, int NW>
@@ -241,17 +245,166 @@ __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, f
   cp_async_wait<0>();
 }
 
+// Interior CTAs (strip and all its input rows inside the image: no dz, no
+// edge fix-ups) -- the same FP32 operations as harris_shfl_fast with all
+// index work hoisted: the smem ring carries two mirror rows after its last
+// row (ring rows 0 and 1 are also written at NSR and NSR+1), so the three
+// input rows of a step are base + (u + rr) with compile-time offsets; the
+// loader walks a row pointer by the pitch; every emitting lane stores a full
+// float4.  Bit-identical to the general path.
 template <int B, int NW>
-__global__ void __launch_bounds__(32 * NW) harris_shfl(HarrisParams p, int S) {
+__device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int S, float* smem) {
+  constexpr int A = B / 2;
+  constexpr int BB = B - 1 - A;
+  constexpr int NT = 32 * NW;
+  constexpr int HP = 8;
+  constexpr int TW = 120 * NW;
+  constexpr int ROWLEN = TW + 2 * HP;
+  constexpr int NSLOT = ROWLEN / 4;
+  constexpr int RB = HarFastGeom<B>::RB, NBLKS = HarFastGeom<B>::NBLKS, NSR = HarFastGeom<B>::NSR;
+  static_assert(RB >= 2, "mirror rows cover the two rows a step reads past its block");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * TW;
+  const int ly0 = blockIdx.y * S;
+  const int ly1 = min(ly0 + S, p.dst.H);
+  const int g0 = p.dst.y0 + ly0;
+  const int NY = (ly1 - ly0) + B - 1;
+  const int NL = NY + 2;
+  const int NBI = (NY + RB - 1) / RB;
+  const int NBL = (NL + RB - 1) / RB;
+  const int64_t spitch = p.src.pitch >> 2;
+  const bool loader = tid < NSLOT;
+  const float* gsrc = src_row(p.src, b, g0 - A - 1) + (x0 - HP + 4 * tid);
+  float* sdst = smem + 4 * tid;
+
+  auto load_block = [&](int m) {
+    if (!loader) return;
+    const float* g = gsrc + (int64_t)(m * RB) * spitch;
+    const int r0 = (m % NBLKS) * RB;
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      if (m * RB + u < NL) {
+        cp_async16(sdst + (r0 + u) * ROWLEN, g, 16);
+        if (u < 2 && r0 == 0) cp_async16(sdst + (NSR + u) * ROWLEN, g, 16);  // mirror
+      }
+      g += spitch;
+    }
+  };
+  for (int m = 0; m < NBLKS - 1; ++m) {
+    if (m < NBL) load_block(m);
+    cp_async_commit();
+  }
+
+  const int xl = x0 + 120 * warp + 4 * (lane - 1);
+  const float* stb = smem + (xl - (x0 - HP));
+  const bool emit = lane >= 1 && lane <= 30;
+  float2 hr2[B][4];
+  float hrxy[B][4];
+  float* drow = dst_row(p.dst, b, ly0) + xl;
+  const int64_t dpitch = p.dst.pitch >> 2;
+  char* mrow = p.mask ? p.mask + (int64_t)b * p.mbstride + (int64_t)ly0 * p.mpitch + xl : nullptr;
+
+#pragma unroll 1
+  for (int i = 0; i < NBI; ++i) {
+    cp_async_wait<NBLKS - 3>();
+    __syncthreads();
+    if (i + NBLKS - 1 < NBL) load_block(i + NBLKS - 1);
+    cp_async_commit();
+    const float* sb = stb + (i % NBLKS) * RB * ROWLEN;
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      const int step = i * RB + u;
+      if (step < NY) {
+        float in[3][6];
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr) {
+          const float4 w = *reinterpret_cast<const float4*>(sb + (u + rr) * ROWLEN);
+          in[rr][0] = __shfl_up_sync(0xffffffffu, w.w, 1);
+          in[rr][1] = w.x; in[rr][2] = w.y; in[rr][3] = w.z; in[rr][4] = w.w;
+          in[rr][5] = __shfl_down_sync(0xffffffffu, w.x, 1);
+        }
+        float vd[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) vd[c] = __fsub_rn(in[2][c], in[0][c]);
+        float2 g[8];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float h0 = __fsub_rn(in[0][c + 2], in[0][c]);
+          const float h1 = __fsub_rn(in[1][c + 2], in[1][c]);
+          const float h2 = __fsub_rn(in[2][c + 2], in[2][c]);
+          g[c + 2].x = __fmaf_rn(2.0f, h1, __fadd_rn(h0, h2));
+          g[c + 2].y = __fmaf_rn(2.0f, vd[c + 1], __fadd_rn(vd[c], vd[c + 2]));
+        }
+        g[0].x = __shfl_up_sync(0xffffffffu, g[4].x, 1);
+        g[0].y = __shfl_up_sync(0xffffffffu, g[4].y, 1);
+        g[1].x = __shfl_up_sync(0xffffffffu, g[5].x, 1);
+        g[1].y = __shfl_up_sync(0xffffffffu, g[5].y, 1);
+        g[6].x = __shfl_down_sync(0xffffffffu, g[2].x, 1);
+        g[6].y = __shfl_down_sync(0xffffffffu, g[2].y, 1);
+        g[7].x = __shfl_down_sync(0xffffffffu, g[3].x, 1);
+        g[7].y = __shfl_down_sync(0xffffffffu, g[3].y, 1);
+        const int slot = u % B;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float2 hxxyy = make_float2(0.0f, 0.0f);
+          float hxy = 0.0f;
+#pragma unroll
+          for (int t = -A; t <= BB; ++t) {
+            const float2 gg = g[2 + q + t];
+            hxxyy = __ffma2_rn(gg, gg, hxxyy);
+            hxy = __fmaf_rn(gg.x, gg.y, hxy);
+          }
+          hr2[slot][q] = hxxyy;
+          hrxy[slot][q] = hxy;
+        }
+        if (step >= B - 1) {
+          float R[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float2 s2 = hr2[(u + 1) % B][q];
+            float sxy = hrxy[(u + 1) % B][q];
+#pragma unroll
+            for (int j = 1; j < B; ++j) {
+              s2 = __fadd2_rn(s2, hr2[(u + 1 + j) % B][q]);
+              sxy = __fadd_rn(sxy, hrxy[(u + 1 + j) % B][q]);
+            }
+            R[q] = harris_R(s2.x, sxy, s2.y, p.k);
+          }
+          if (emit) {
+            st_cs4(drow, make_float4(R[0], R[1], R[2], R[3]));
+            if (mrow)
+              *reinterpret_cast<uchar4*>(mrow) =
+                  make_uchar4(R[0] > p.threshold, R[1] > p.threshold, R[2] > p.threshold, R[3] > p.threshold);
+          }
+          drow += dpitch;
+          if (mrow) mrow += p.mpitch;
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
+template <int B, int NW>
+__global__ void __launch_bounds__(32 * NW, ICL_HSHFL_MINB) harris_shfl(HarrisParams p, int S) {
   extern __shared__ __align__(16) float smem[];
-  harris_shfl_fast<B, NW>(p, S, smem);
+  constexpr int TW = 120 * NW, HP = 8, A = B / 2, BB = B - 1 - A;
+  const int x0 = blockIdx.x * TW, ly0 = blockIdx.y * S;
+  const int ly1 = min(ly0 + S, p.dst.H);
+  const int g0 = p.dst.y0 + ly0;
+  // every input row (g0-A-1 .. last output row + BB + 1) and column inside the image
+  const bool interior = x0 - HP >= 0 && x0 + TW + HP <= p.src.W && g0 - A - 1 >= 0 &&
+                        p.dst.y0 + ly1 + BB + 1 <= p.src.Hg;
+  if (interior) harris_shfl_interior<B, NW>(p, S, smem);
+  else harris_shfl_fast<B, NW>(p, S, smem);
 }
 
 template <int B, int NW>
 static inline cudaError_t launch_hshfl(const HarrisParams& p, int batch, int S, cudaStream_t s) {
   constexpr int TW = 120 * NW;
   constexpr int ROWLEN = TW + 16;
-  const size_t smem = (size_t)HarFastGeom<B>::NSR * ROWLEN * sizeof(float);
+  const size_t smem = (size_t)(HarFastGeom<B>::NSR + 2) * ROWLEN * sizeof(float);  // + 2 mirror rows
   auto kern = harris_shfl<B, NW>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
