@@ -56,6 +56,11 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
+# variant -> kernel-name fragments (to attach ncu counters only to the kernel they were measured on)
+KERNEL_OF = {"boxsum_x2": ("nlm_box_x2",), "boxsum_r8": ("nlm_box_r8",), "stream_nt64_s16_v4": ("sep_stream<2, 64",),
+             "shfl_nw2_s64": ("harris_shfl<5, 2>",)}
+
+
 def ncu_traffic():
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
@@ -446,6 +451,15 @@ def run_suite(args):
     roof["harris"]["frac_of_8TBs_spec"] = roof["harris"]["achieved"] / 8000.0
     roof["sepconv"]["peak_kind"] = roof["harris"]["peak_kind"] = hbm_kind
     roof["nlm"]["peak_kind"] = "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz"
+    # ncu pipe counters of the profiled kernel (profiles/ncu_traffic.json), when it is the one timed here
+    for f in roof:
+        e = traffic.get(f) or {}
+        kname = e.get("kernel", "")
+        if e and any(k in kname for k in KERNEL_OF.get(roof[f]["kernel"], ())):
+            roof[f]["ncu"] = {k: e.get(k) for k in ("fma_pipe_cycles_pct", "issue_active_pct", "smem_wavefronts_pct",
+                                                    "mufu_pct")}
+    roof["nlm"]["limiter"] = ("shared-memory wavefronts (two-phase separable box sums: H round trip + "
+                              "accumulation loads, DESIGN.md §5)")
     dominant = max(med, key=med.get)
 
     cpu = None

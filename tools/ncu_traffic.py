@@ -32,7 +32,14 @@ for spec in a.reports:
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
         return float(v.replace(",", "")) * scale
     rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
-    out[f] = {"bytes_per_px": round((rd + wr) / a.px, 3), "kernel": d["Kernel Name"][0], "report": os.path.basename(path)}
+
+    def pct(key):
+        return round(float(d[key][0]), 1) if key in d else None
+    out[f] = {"bytes_per_px": round((rd + wr) / a.px, 3), "kernel": d["Kernel Name"][0], "report": os.path.basename(path),
+              "fma_pipe_cycles_pct": pct("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+              "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+              "smem_wavefronts_pct": pct("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+              "mufu_pct": pct("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active")}
 path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
 with open(path, "w") as fh:
     json.dump(out, fh, indent=1)
