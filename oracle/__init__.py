@@ -51,7 +51,8 @@ def _load():
         lib.oracle_sepconv.argtypes = [p, i64, i64, i64, p, i32, p, i32, i32, f32, p, p, i64, p, i32]
         lib.oracle_harris.argtypes = [p, i64, i64, i64, i32, f32, i32, f32, p, p, i64, p, p, i32]
         lib.oracle_nlm.argtypes = [p, i64, i64, i64, i32, i32, f32, i32, f32, p, p, i64, p, p, i32]
-        for fn in (lib.oracle_sepconv, lib.oracle_harris, lib.oracle_nlm):
+        lib.oracle_conv2d_u8.argtypes = [p, i64, i64, i64, p, i32, i32, f32, p, p, i64, p, i32]
+        for fn in (lib.oracle_sepconv, lib.oracle_harris, lib.oracle_nlm, lib.oracle_conv2d_u8):
             fn.restype = i32
         lib.oracle_nthreads_default.restype = i32
         _lib = lib
@@ -130,6 +131,24 @@ def nlm(img, patch_radius=2, search_radius=5, h=0.1, border="clamp", border_valu
     if rc:
         raise ValueError("oracle_nlm: invalid arguments")
     return (out, sc) if with_scale else out
+
+
+def conv2d_u8(img, filt, border="clamp", border_value=0.0, points=None, threads=0):
+    """out(x,y) = sum_j sum_i f[j+r][i+r] in_B(x+i, y+j) on an 8-bit image (§6,
+    Table 3): ``img`` (H, W) uint8 with contiguous rows, ``filt`` (2r+1, 2r+1) fp32."""
+    if img.dtype != np.uint8 or img.ndim != 2 or img.strides[1] != 1:
+        raise TypeError("conv2d_u8 images are 2-D uint8 arrays with contiguous rows")
+    f = np.ascontiguousarray(filt, dtype=np.float32)
+    assert f.ndim == 2 and f.shape[0] == f.shape[1] and f.shape[0] % 2 == 1
+    h, w = img.shape
+    xs, ys, n, shape = _points(img, points)
+    out = np.empty(shape, dtype=np.float64)
+    rc = _load().oracle_conv2d_u8(img.ctypes.data, w, h, img.strides[0], f.ctypes.data, f.shape[0] // 2,
+                                  _BORDERS[border], float(border_value), _ptr(xs), _ptr(ys), n,
+                                  out.ctypes.data, threads)
+    if rc:
+        raise ValueError("oracle_conv2d_u8: invalid arguments")
+    return out
 
 
 def harris_scale(S, k=0.04):

@@ -27,6 +27,12 @@
  *     (readings R6-R10): dx, dy are Images with their own boundary.
  *   Non-local means: NOT in PAPER.md (BASELINE.json north_star only);
  *     standard Buades-Coll-Morel form with the readings R11-R14 of DESIGN.md.
+ *   Non-separable convolution of an 8-bit image (§6, "a
+ *     8192x8192 image with pixels of type unsigned char, a 5x5 filter, and
+ *     clamped boundary condition"; filter values known only at run time,
+ *     PAPER.md:577-579; Table 3):
+ *       out(x,y) = sum_{j=-r..r} sum_{i=-r..r} f[j+r][i+r] * in_B(x+i, y+j)
+ *     (correlation, reading R1; real-valued output, reading R22).
  *
  * Threading: the point list is split into contiguous chunks, one pthread per
  * chunk; each output is computed independently in a fixed order, so results
@@ -172,9 +178,44 @@ static double nlm_px(const nlm_args* a, int64_t x, int64_t y, double* wmax) {
 }
 
 /* ------------------------------------------------------------------------ */
+/* Non-separable convolution of an 8-bit image:                                */
+/*   out(x,y) = sum_{j=-r..r} sum_{i=-r..r} f[j+r][i+r] * in_B(x+i, y+j)       */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    const uint8_t* u;
+    int64_t W, H, pitch; /* pitch in bytes == elements */
+    int border;
+    double c;
+} oimg8;
+
+/* in_B(x, y) of an 8-bit image: PAPER.md Fig. 3. */
+static double read_B8(const oimg8* im, int64_t x, int64_t y) {
+    if (x < 0 || x >= im->W || y < 0 || y >= im->H) {
+        if (im->border == OR_BORDER_CONSTANT) return im->c;
+        x = clampi(x, 0, im->W - 1);
+        y = clampi(y, 0, im->H - 1);
+    }
+    return (double)im->u[y * im->pitch + x];
+}
+
+typedef struct {
+    oimg8 im;
+    const double* f; /* (2r+1)^2, row j major */
+    int r;
+} conv2d_args;
+
+static double conv2d_px(const conv2d_args* a, int64_t x, int64_t y) {
+    const int r = a->r, n = 2 * r + 1;
+    double s = 0.0;
+    for (int j = -r; j <= r; ++j)
+        for (int i = -r; i <= r; ++i) s += a->f[(j + r) * n + (i + r)] * read_B8(&a->im, x + i, y + j);
+    return s;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Point-list driver + pthreads                                                */
 /* ------------------------------------------------------------------------ */
-enum { F_SEP = 0, F_HARRIS = 1, F_NLM = 2 };
+enum { F_SEP = 0, F_HARRIS = 1, F_NLM = 2, F_CONV2D = 3 };
 
 typedef struct {
     int filter;
@@ -193,6 +234,8 @@ static void* run_job(void* p) {
         int64_t y = jb->ys ? jb->ys[n] : n / jb->W;
         if (jb->filter == F_SEP) {
             jb->out[n] = sepconv_px((const sep_args*)jb->args, x, y);
+        } else if (jb->filter == F_CONV2D) {
+            jb->out[n] = conv2d_px((const conv2d_args*)jb->args, x, y);
         } else if (jb->filter == F_HARRIS) {
             double sxx, sxy, syy;
             jb->out[n] = harris_px((const harris_args*)jb->args, x, y, &sxx, &sxy, &syy);
@@ -278,6 +321,21 @@ int oracle_nlm(const float* in, int64_t W, int64_t H, int64_t pitch, int rho, in
     nlm_args a = {{in, W, H, pitch, border, (double)c}, rho, s, (double)h};
     int64_t npts = xs ? n : W * H;
     run_points(F_NLM, &a, W, npts, xs, ys, out, wmax, nthreads);
+    return 0;
+}
+
+int oracle_conv2d_u8(const uint8_t* in, int64_t W, int64_t H, int64_t pitch, const float* filt, int r,
+                     int border, float c, const int64_t* xs, const int64_t* ys, int64_t n, double* out,
+                     int nthreads) {
+    if (!in || W < 1 || H < 1 || pitch < W || r < 0 || !filt || !out) return -1;
+    if (border != OR_BORDER_CONSTANT && border != OR_BORDER_CLAMP) return -1;
+    const int nf = (2 * r + 1) * (2 * r + 1);
+    double* f = (double*)malloc(sizeof(double) * (size_t)nf);
+    for (int k = 0; k < nf; ++k) f[k] = (double)filt[k];
+    conv2d_args a = {{in, W, H, pitch, border, (double)c}, f, r};
+    int64_t npts = xs ? n : W * H;
+    run_points(F_CONV2D, &a, W, npts, xs, ys, out, NULL, nthreads);
+    free(f);
     return 0;
 }
 

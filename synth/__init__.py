@@ -14,6 +14,12 @@ Workload shapes follow BASELINE.json ``configs`` / SURVEY.md §8(d):
   0.5, axis-aligned rectangles of random intensity) plus uniform noise;
   the Harris (C2, noise +-0.01) and NLM (C3, sigma=0.05 -> +-0.0866)
   workloads.
+* ``uniform_u8``     -- i.i.d. uniform 8-bit pixels (the top 8 bits of the
+  same SplitMix64 draw); the non-separable uchar convolution workload
+  (8192^2 unsigned char, clamped boundary).
+* ``filter2d``       -- a seeded non-separable (2r+1)^2 filter, U(-1,1)
+  taps in fp32 (the paper's 5x5 filter is a run-time input whose values it
+  does not print).
 * ``gaussian_taps``  -- the separable Gaussian taps of SURVEY.md §8(c)
   reading #3 (OpenCV default sigma(r) = 0.3(r-1)+0.8, normalised in double,
   rounded once to fp32).  PAPER.md:588-589 (§6) fixes "a 5x5 filter" but
@@ -75,6 +81,28 @@ def uniform_image(seed: int, height: int, width: int, *, row0: int = 0,
         idx = np.arange(base, base + n * width, dtype=np.uint64)
         out[r:r + n] = u01(seed, idx).reshape(n, width).astype(np.float32)
     return out
+
+
+def uniform_u8(seed: int, height: int, width: int, *, row0: int = 0,
+               rows: int | None = None) -> np.ndarray:
+    """i.i.d. uniform uint8 image: pixel (x, y) = top 8 bits of splitmix64(key(seed) ^ (y*width + x))."""
+    rows = height - row0 if rows is None else rows
+    out = np.empty((rows, width), dtype=np.uint8)
+    chunk = max(1, (1 << 22) // max(width, 1))
+    for r in range(0, rows, chunk):
+        n = min(chunk, rows - r)
+        base = (row0 + r) * width
+        idx = np.arange(base, base + n * width, dtype=np.uint64)
+        z = splitmix64(idx ^ _stream_key(seed))
+        out[r:r + n] = (z >> np.uint64(56)).astype(np.uint8).reshape(n, width)
+    return out
+
+
+def filter2d(seed: int, radius: int) -> np.ndarray:
+    """Seeded non-separable (2r+1)x(2r+1) filter with U(-1,1) fp32 taps."""
+    n = 2 * radius + 1
+    idx = np.arange(n * n, dtype=np.uint64)
+    return (2.0 * u01(seed * 7 + 3, idx) - 1.0).astype(np.float32).reshape(n, n)
 
 
 def rect_scene(seed: int, height: int, width: int, *, n_rect: int = 256,

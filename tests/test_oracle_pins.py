@@ -232,3 +232,95 @@ def test_nlm_rejects_bad_h():
     for h in (0.0, -1.0, float("nan")):
         with pytest.raises(ValueError):
             oracle.nlm(img, 1, 1, h)
+
+
+# ============================================================================ conv2d_u8
+# Non-separable convolution of an 8-bit image (§6, Table 3).
+
+@pytest.mark.parametrize("r", [1, 2, 3])
+def test_conv2d_u8_delta_image(r):
+    """A single 255 pixel at (x0, y0), constant 0 border: out(x0-i, y0-j) = 255 f[j+r][i+r]
+    (correlation orientation, reading R1), zero elsewhere -- exact."""
+    H, W, x0, y0 = 15, 17, 8, 6
+    img = np.zeros((H, W), np.uint8)
+    img[y0, x0] = 255
+    f = synth.filter2d(3, r)
+    out = oracle.conv2d_u8(img, f, "constant", 0.0)
+    exp = np.zeros((H, W))
+    for j in range(-r, r + 1):
+        for i in range(-r, r + 1):
+            exp[y0 - j, x0 - i] = 255.0 * float(f[j + r, i + r])
+    np.testing.assert_array_equal(out, exp)
+
+
+@pytest.mark.parametrize("border,c", [("clamp", 0.0), ("constant", 77.0)])
+def test_conv2d_u8_constant_image(border, c):
+    img = np.full((9, 11), 77, np.uint8)
+    f = synth.filter2d(4, 2)
+    out = oracle.conv2d_u8(img, f, border, c)
+    np.testing.assert_allclose(out, 77.0 * f.astype(np.float64).sum(), rtol=1e-14)
+
+
+@pytest.mark.parametrize("border,c", [("clamp", 0.0), ("constant", 0.0), ("constant", 31.0)])
+def test_conv2d_u8_separable_filter_equals_sepconv_oracle(border, c):
+    """outer(g, f) filter == the separable oracle on the same (exactly fp32) pixel values."""
+    img = synth.uniform_u8(5, 23, 19)
+    fx, gy = synth.signed_taps(11, 2), synth.signed_taps(12, 2)
+    filt = np.outer(gy.astype(np.float64), fx.astype(np.float64))
+    # the product of two fp32 taps is exact in double but not in fp32: compare against the
+    # double outer product by building it from fp32 values the conv2d oracle then promotes
+    f32 = filt.astype(np.float32)
+    out = oracle.conv2d_u8(img, f32, border, c)
+    sep = oracle.sepconv(img.astype(np.float32), fx, gy, border, c)
+    scale = oracle.conv2d_u8(img, np.abs(f32), border, abs(c))
+    np.testing.assert_allclose(out, sep, rtol=0, atol=1e-6 * scale.max())  # f32 rounding of g_j f_i only
+
+
+@pytest.mark.parametrize("r", [0, 1, 2, 3])
+@pytest.mark.parametrize("border,c", [("clamp", 0.0), ("constant", 0.0), ("constant", 200.0)])
+def test_conv2d_u8_brute_force_scipy(r, border, c):
+    """scipy.ndimage.correlate (mode nearest == clamp, constant == constant c) on a 9x7 image
+    and a ragged 13x29 one: every border pixel included (SPEC.md §"Boundary semantics")."""
+    for shape in ((9, 7), (13, 29)):
+        img = synth.uniform_u8(6 + r, *shape)
+        f = synth.filter2d(7 + r, r)
+        out = oracle.conv2d_u8(img, f, border, c)
+        mode = "nearest" if border == "clamp" else "constant"
+        exp = ndi.correlate(img.astype(np.float64), f.astype(np.float64), mode=mode, cval=c)
+        np.testing.assert_allclose(out, exp, rtol=1e-13, atol=1e-10)
+
+
+def test_conv2d_u8_points_and_pitch():
+    full = synth.uniform_u8(8, 40, 33)
+    img = np.zeros((40, 48), np.uint8)
+    img[:, :33] = full
+    view = img[:, :33]  # row pitch 48 bytes
+    f = synth.filter2d(9, 2)
+    out = oracle.conv2d_u8(view, f, "clamp")
+    np.testing.assert_array_equal(out, oracle.conv2d_u8(full, f, "clamp"))
+    xs = np.array([0, 32, 5, 17, 0], np.int64)
+    ys = np.array([0, 39, 20, 3, 39], np.int64)
+    np.testing.assert_array_equal(oracle.conv2d_u8(full, f, "clamp", points=(xs, ys)), out[ys, xs])
+
+
+def test_conv2d_u8_linear_in_the_filter():
+    img = synth.uniform_u8(10, 12, 14)
+    f1, f2 = synth.filter2d(1, 2), synth.filter2d(2, 2)
+    a = oracle.conv2d_u8(img, f1) + oracle.conv2d_u8(img, f2)
+    b = oracle.conv2d_u8(img, f1.astype(np.float64) + f2.astype(np.float64))
+    np.testing.assert_allclose(a, b, rtol=1e-13, atol=1e-10)
+
+
+def test_conv2d_u8_rejects_bad_args():
+    with pytest.raises(TypeError):
+        oracle.conv2d_u8(np.zeros((3, 3), np.float32), synth.filter2d(1, 1))
+    with pytest.raises(KeyError):  # unknown border mode
+        oracle.conv2d_u8(np.zeros((3, 3), np.uint8), synth.filter2d(1, 1), "wrap")
+
+
+def test_uniform_u8_is_the_top_byte_of_the_u01_stream():
+    """uniform_u8 and uniform_image share one SplitMix64 draw: u8 = floor(256 * u01)."""
+    u = synth.uniform_image(13, 7, 9)
+    b = synth.uniform_u8(13, 7, 9)
+    np.testing.assert_array_equal(b, np.floor(u.astype(np.float64) * 256).astype(np.uint8))
+    np.testing.assert_array_equal(synth.uniform_u8(13, 7, 9, row0=3, rows=2), b[3:5])
