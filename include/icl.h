@@ -57,7 +57,7 @@ typedef enum {
 
 typedef enum { ICL_BORDER_CONSTANT = 0, ICL_BORDER_CLAMP = 1 } icl_border;
 
-typedef enum { ICL_FILTER_SEPCONV = 0, ICL_FILTER_HARRIS = 1, ICL_FILTER_NLM = 2 } icl_filter;
+typedef enum { ICL_FILTER_SEPCONV = 0, ICL_FILTER_HARRIS = 1, ICL_FILTER_NLM = 2, ICL_FILTER_CONV2D = 3 } icl_filter;
 
 /* A (batch of) 2-D image(s).  `data` is a device pointer or a HOST pointer
  * (fp32 pixels for images, uint8 for masks).  When any operand of
@@ -143,11 +143,30 @@ icl_status icl_nlm(const icl_image* src, const icl_image* dst, int patch_radius,
                    void* stream);
 
 /* ------------------------------------------------------------------------
+ * Non-separable 2-D convolution of an 8-bit image -- the paper's third
+ * benchmark (§6: "a 8192x8192 image with pixels of type
+ * unsigned char, a 5x5 filter, and clamped boundary condition"; the filter
+ * values are a run-time input; Table 3;
+ * SURVEY.md §8(f) row 1):
+ *     out(x,y) = sum_{j=-r..r} sum_{i=-r..r} filter[(j+r)*(2r+1) + (i+r)] * src_B(x+i, y+j)
+ * (correlation, R1; fp32 output, R22).  src: uint8 pixels
+ * (element size 1, own pitch); dst: fp32; same width / height / batch.
+ * radius r in [0, 3] (> 3 -> ICL_ERR_UNSUPPORTED); filter: HOST array of
+ * (2r+1)^2 finite floats, row j major, copied during the call (the
+ * constant-memory analog).  border_value: the constant-mode pixel value
+ * (any finite float).  Every variant evaluates, per output, one fp32 FMA
+ * chain over j = -r..r then i = -r..r starting from +0 with the pixel
+ * converted exactly to fp32, so variants and band splits are bit-identical.
+ * ---------------------------------------------------------------------- */
+icl_status icl_conv2d_u8(const icl_image* src, const icl_image* dst, const float* filter, int radius,
+                         icl_border border, float border_value, const icl_band* band, void* stream);
+
+/* ------------------------------------------------------------------------
  * Variant space + auto-tuner (§4, Table 1 lines
  * 364-393).
  * ---------------------------------------------------------------------- */
 
-/* Tagged union of the three calls' arguments. */
+/* Tagged union of the filter calls' arguments. */
 typedef struct {
     icl_filter filter;
     icl_image src;
@@ -170,6 +189,9 @@ typedef struct {
     int patch_radius;
     int search_radius;
     float h;
+    /* conv2d (src is the uint8 image) */
+    const float* filter2d;
+    int radius2d;
 } icl_problem;
 
 typedef struct {

@@ -22,10 +22,10 @@ ICL_OK = 0
 STATUS = {0: "ICL_OK", 1: "ICL_ERR_INVALID_ARG", 2: "ICL_ERR_ALIASING", 3: "ICL_ERR_UNSUPPORTED",
           4: "ICL_ERR_WORKSPACE", 5: "ICL_ERR_CUDA", 6: "ICL_ERR_NCCL", 7: "ICL_ERR_NOT_TUNED"}
 BORDER = {"constant": 0, "clamp": 1}
-FILTER = {"sepconv": 0, "harris": 1, "nlm": 2}
+FILTER = {"sepconv": 0, "harris": 1, "nlm": 2, "conv2d": 3}
 
 # Symbols include/icl.h declares (checked by tests/test_abi.py).
-EXPORTS = ("icl_sepconv", "icl_sepconv_workspace_bytes", "icl_harris", "icl_nlm", "icl_tune",
+EXPORTS = ("icl_sepconv", "icl_sepconv_workspace_bytes", "icl_harris", "icl_nlm", "icl_conv2d_u8", "icl_tune",
            "icl_tune_cache_save", "icl_tune_cache_load", "icl_tune_cache_clear", "icl_tune_cache_size",
            "icl_variant_count", "icl_variant_name", "icl_force_variant", "icl_last_variant",
            "icl_launch_count", "icl_transfer_bytes", "icl_last_error", "icl_version", "icl_fill_uniform")
@@ -53,7 +53,8 @@ class icl_problem(ctypes.Structure):
                 ("taps_y", ctypes.c_void_p), ("ry", ctypes.c_int), ("workspace", ctypes.c_void_p),
                 ("workspace_bytes", ctypes.c_size_t), ("block", ctypes.c_int), ("k", ctypes.c_float),
                 ("mask", icl_image), ("threshold", ctypes.c_float), ("patch_radius", ctypes.c_int),
-                ("search_radius", ctypes.c_int), ("h", ctypes.c_float)]
+                ("search_radius", ctypes.c_int), ("h", ctypes.c_float), ("filter2d", ctypes.c_void_p),
+                ("radius2d", ctypes.c_int)]
 
 
 class icl_variant_info(ctypes.Structure):
@@ -80,6 +81,7 @@ def load_library(path: str = LIB_PATH):
         "icl_sepconv_workspace_bytes": ([I64, I64, I64, I], ctypes.c_size_t),
         "icl_harris": ([img, img, I, F, I, F, img, F, band, P], I),
         "icl_nlm": ([img, img, I, I, F, I, F, band, P], I),
+        "icl_conv2d_u8": ([img, img, P, I, I, F, band, P], I),
         "icl_tune": ([ctypes.POINTER(icl_problem), U, P, ctypes.POINTER(icl_variant_info)], I),
         "icl_tune_cache_save": ([ctypes.c_char_p], I),
         "icl_tune_cache_load": ([ctypes.c_char_p], I),
@@ -199,13 +201,32 @@ def nlm(src, dst, patch_radius: int = 2, search_radius: int = 5, h: float = 0.1,
     return dst
 
 
+def _filter2d(filt):
+    import numpy as np
+    f = np.ascontiguousarray(np.asarray(filt.cpu() if hasattr(filt, "cpu") else filt, dtype=np.float32))
+    if f.ndim != 2 or f.shape[0] != f.shape[1] or f.shape[0] % 2 != 1:
+        raise ValueError("filter must be a square (2r+1) x (2r+1) array")
+    return (ctypes.c_float * f.size)(*f.ravel().tolist()), f.shape[0] // 2
+
+
+def conv2d_u8(src, dst, filt, border: str = "clamp", border_value: float = 0.0, band=None, stream=None):
+    """Non-separable convolution of a uint8 image into fp32 (icl_conv2d_u8).
+    ``filt`` is a (2r+1) x (2r+1) array of run-time taps.  Returns dst."""
+    lib = load_library()
+    f, r = _filter2d(filt)
+    s, d = _image(src, 1, host_ok=True), _image(dst, host_ok=True)
+    _check(lib.icl_conv2d_u8(ctypes.byref(s), ctypes.byref(d), ctypes.cast(f, ctypes.c_void_p), r, BORDER[border],
+                             border_value, _ref(_band(band)), _stream(stream)))
+    return dst
+
+
 # ----------------------------------------------------------------------------- tuner / registry
 def tune(filter: str, src, dst, *, force: bool = False, verify: bool = True, stream=None, **params) -> dict:
     """Auto-tune one problem (icl_tune).  ``params`` as for the filter call."""
     lib = load_library()
     p = icl_problem()
     p.filter = FILTER[filter]
-    p.src, p.dst = _image(src), _image(dst)
+    p.src, p.dst = _image(src, 1 if filter == "conv2d" else 4), _image(dst)
     p.border = BORDER[params.get("border", "constant" if filter == "sepconv" else "clamp")]
     p.border_value = params.get("border_value", 0.0)
     keep = []
@@ -222,6 +243,10 @@ def tune(filter: str, src, dst, *, force: bool = False, verify: bool = True, str
         if params.get("mask") is not None:
             p.mask = _image(params["mask"], 1)
         p.threshold = params.get("threshold", 0.0)
+    elif filter == "conv2d":
+        f2, r2 = _filter2d(params["filter2d"])
+        keep.append(f2)
+        p.filter2d, p.radius2d = ctypes.cast(f2, ctypes.c_void_p), r2
     else:
         p.patch_radius, p.search_radius = params.get("patch_radius", 2), params.get("search_radius", 5)
         p.h = params.get("h", 0.1)
@@ -303,7 +328,7 @@ def nlm_halo(patch_radius: int, search_radius: int):
     return r, r
 
 
-__all__ = ["sepconv", "harris", "nlm", "tune", "tune_cache_save", "tune_cache_load", "tune_cache_clear",
+__all__ = ["sepconv", "harris", "nlm", "conv2d_u8", "tune", "tune_cache_save", "tune_cache_load", "tune_cache_clear",
            "tune_cache_size", "variant_names", "force_variant", "last_variant", "launch_count", "transfer_bytes", "version",
            "fill_uniform", "load_library", "IclError", "sepconv_workspace_bytes", "harris_halo", "nlm_halo",
            "EXPORTS", "LIB_PATH"]

@@ -134,7 +134,7 @@ static icl_status make_views(const icl_image* src, const icl_image* dst, const i
 }
 
 // ------------------------------------------------------------------ variants
-enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL, K_TILE2, K_BOXX2 };
+enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL, K_TILE2, K_BOXX2, K_C2TILE };
 struct Variant {
   const char* name;
   Kind kind;
@@ -181,18 +181,26 @@ static const Variant kNlmVariants[] = {
     {"boxsum_x2", K_BOXX2, 0, 0, 0},
 };
 
+static const Variant kConvVariants[] = {
+    {"naive_direct", K_NAIVE, 0, 0, 0},
+    {"tile_c4r4", K_C2TILE, 256, 4, 4},
+    {"tile_c4r8", K_C2TILE, 256, 4, 8},
+};
+
 static const Variant* table(icl_filter f, int* n) {
   switch (f) {
     case ICL_FILTER_SEPCONV: *n = (int)(sizeof kSepVariants / sizeof *kSepVariants); return kSepVariants;
     case ICL_FILTER_HARRIS: *n = (int)(sizeof kHarVariants / sizeof *kHarVariants); return kHarVariants;
     case ICL_FILTER_NLM: *n = (int)(sizeof kNlmVariants / sizeof *kNlmVariants); return kNlmVariants;
+    case ICL_FILTER_CONV2D: *n = (int)(sizeof kConvVariants / sizeof *kConvVariants); return kConvVariants;
   }
   *n = 0;
   return nullptr;
 }
 
-static thread_local int t_force[3] = {-1, -1, -1};
-static thread_local int t_last[3] = {-1, -1, -1};
+constexpr int kNFilters = 4;
+static thread_local int t_force[kNFilters] = {-1, -1, -1, -1};
+static thread_local int t_last[kNFilters] = {-1, -1, -1, -1};
 
 // Prepared call of any filter (what a variant launcher needs).
 struct Prepared {
@@ -200,6 +208,7 @@ struct Prepared {
   SepCall sep;
   HarrisCall har;
   NlmCall nlm;
+  Conv2dCall c2d;
   bool a16;       // src/dst (and mask) 16B-aligned
   int64_t pixels; // W * H * batch
   size_t dst_bytes_compact;
@@ -208,7 +217,8 @@ struct Prepared {
 
 static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
   *why = ICL_ERR_UNSUPPORTED;
-  if ((v.kind == K_STREAM || v.kind == K_BULK || v.kind == K_SHFL || v.kind == K_TILE2) && v.vec == 4 && !pc.a16)
+  if ((v.kind == K_STREAM || v.kind == K_BULK || v.kind == K_SHFL || v.kind == K_TILE2 || v.kind == K_C2TILE) &&
+      v.vec == 4 && !pc.a16)
     return false;
   if (v.kind == K_SHFL && pc.har.block > 5) return false;
   if (pc.f == ICL_FILTER_SEPCONV && v.kind == K_STREAM &&
@@ -248,6 +258,9 @@ static cudaError_t run_variant(const Prepared& pc, const Variant& v, cudaStream_
       if (v.kind == K_BOXR16) return launch_nlm_r16(pc.nlm, s);
       if (v.kind == K_BOXX2) return launch_nlm_x2(pc.nlm, s);
       return launch_nlm_boxsum(pc.nlm, 0, s);
+    case ICL_FILTER_CONV2D:
+      if (v.kind == K_NAIVE) return launch_conv2d_naive(pc.c2d, s);
+      return launch_conv2d_tile(pc.c2d, v.S, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -286,6 +299,9 @@ static int default_variant(const Prepared& pc) {
       if (nlm_x2_supported(pc.nlm.P, pc.nlm.S)) return variant_id(pc.f, "boxsum_x2");
       if (nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return variant_id(pc.f, "boxsum_r8");
       return nlm_tiled_supported(pc.nlm.P, pc.nlm.S) ? variant_id(pc.f, "tiled_direct_32x8") : 0;
+    case ICL_FILTER_CONV2D:
+      if (!pc.a16) return 0;
+      return variant_id(pc.f, pc.pixels < (1 << 22) ? "tile_c4r4" : "tile_c4r8");
   }
   return 0;
 }
@@ -461,6 +477,32 @@ static icl_status prep_nlm(const icl_image* src, const icl_image* dst, int P, in
   return ICL_OK;
 }
 
+static icl_status prep_conv2d(const icl_image* src, const icl_image* dst, const float* filt, int r,
+                              icl_border border, float cval, const icl_band* band, Prepared* pc) {
+  icl_status st;
+  if ((st = check_image(src, 1, "src")) || (st = check_image(dst, 4, "dst"))) return st;
+  if (r < 0) return fail(ICL_ERR_INVALID_ARG, "radius must be >= 0");
+  if (r > 3) return fail(ICL_ERR_UNSUPPORTED, "radius %d > 3", r);
+  if (!filt) return fail(ICL_ERR_INVALID_ARG, "null filter");
+  if (!std::isfinite(cval)) return fail(ICL_ERR_INVALID_ARG, "border_value must be finite");
+  const int nf = (2 * r + 1) * (2 * r + 1);
+  for (int k = 0; k < nf; ++k)
+    if (!std::isfinite(filt[k])) return fail(ICL_ERR_INVALID_ARG, "filter tap %d is not finite", k);
+  if (overlap(byte_range(src, 1), byte_range(dst, 4))) return fail(ICL_ERR_ALIASING, "src and dst overlap");
+  pc->f = ICL_FILTER_CONV2D;
+  if ((st = make_views(src, dst, band, border, cval, r, r, &pc->c2d.src, &pc->c2d.dst))) return st;
+  pc->c2d.batch = (int)src->batch;
+  pc->c2d.r = r;
+  for (int k = 0; k < 49; ++k) pc->c2d.f[k] = k < nf ? filt[k] : 0.0f;
+  pc->a16 = aligned16(src) && aligned16(dst);
+  pc->pixels = src->width * dst->height * src->batch;
+  pc->dst_bytes_compact = (size_t)pc->pixels * 4;
+  std::ostringstream ps;
+  ps << "r" << r << ":bd" << (int)border;
+  pc->key = fmt_key("conv2d_u8", dst, pc->a16, ps.str());
+  return ICL_OK;
+}
+
 // ------------------------------------------------------------------ tuner
 __global__ void compare_kernel(const char* a, int64_t apitch, int64_t abstride, const float* ref, int W, int H,
                                unsigned long long* out) {
@@ -503,8 +545,14 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
     }
   }
   // Views of the real destination (the problem's dst).
-  const DstView real_dst = pc.f == ICL_FILTER_SEPCONV ? pc.sep.dst : (pc.f == ICL_FILTER_HARRIS ? pc.har.dst : pc.nlm.dst);
-  const int W = pc.f == ICL_FILTER_SEPCONV ? pc.sep.src.W : (pc.f == ICL_FILTER_HARRIS ? pc.har.src.W : pc.nlm.src.W);
+  const DstView real_dst = pc.f == ICL_FILTER_SEPCONV ? pc.sep.dst
+                           : pc.f == ICL_FILTER_HARRIS ? pc.har.dst
+                           : pc.f == ICL_FILTER_NLM    ? pc.nlm.dst
+                                                       : pc.c2d.dst;
+  const int W = pc.f == ICL_FILTER_SEPCONV ? pc.sep.src.W
+                : pc.f == ICL_FILTER_HARRIS ? pc.har.src.W
+                : pc.f == ICL_FILTER_NLM    ? pc.nlm.src.W
+                                            : pc.c2d.src.W;
   const int H = real_dst.H;
   const int batch = (int)(pc.pixels / ((int64_t)W * H));
   float* ref = nullptr;
@@ -533,7 +581,8 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
   DstView cdst{reinterpret_cast<char*>(ref), (int64_t)W * 4, (int64_t)W * H * 4, H, real_dst.y0};
   if (pc.f == ICL_FILTER_SEPCONV) pref.sep.dst = cdst;
   else if (pc.f == ICL_FILTER_HARRIS) { pref.har.dst = cdst; pref.har.mask = nullptr; }
-  else pref.nlm.dst = cdst;
+  else if (pc.f == ICL_FILTER_NLM) pref.nlm.dst = cdst;
+  else pref.c2d.dst = cdst;
   if ((e = run_variant(pref, vt[0], s)) != cudaSuccess) {
     cudaFree(ref);
     cudaFree(cmp);
@@ -560,7 +609,9 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
       unsigned int b1 = (unsigned int)hc[1], b2 = (unsigned int)hc[2];
       memcpy(&md, &b1, 4);
       memcpy(&mr, &b2, 4);
-      const bool ok = pc.f == ICL_FILTER_SEPCONV ? hc[0] == 0 : md <= 1e-4f * std::max(mr, 1e-30f);
+      // sepconv / conv2d variants share one fp32 order per output: bit-identical or rejected
+      const bool exact = pc.f == ICL_FILTER_SEPCONV || pc.f == ICL_FILTER_CONV2D;
+      const bool ok = exact ? hc[0] == 0 : md <= 1e-4f * std::max(mr, 1e-30f);
       if (!ok) { ++nrej; continue; }
     }
     // warm-up then timed reps (median)
@@ -666,7 +717,7 @@ using ChunkCall = std::function<icl_status(const icl_image*, const icl_image*, c
 
 // src/dst/mask validated by the caller's prep_*; up/down = stencil rows.
 static icl_status run_host(const icl_image* src, const icl_image* dst, const icl_image* mask, const icl_band* band,
-                           int up, int down, const ChunkCall& call, cudaStream_t user) {
+                           int up, int down, const ChunkCall& call, cudaStream_t user, int src_elem = 4) {
   icl_status st = ICL_OK;
   Stager* sg = stager_for_current_device(&st);
   if (!sg) return st;
@@ -700,7 +751,7 @@ static icl_status run_host(const icl_image* src, const icl_image* dst, const icl
   int64_t CH = std::max<int64_t>(1, (16ll << 20) / (W * 4));
   if (const char* env = std::getenv("ICL_HOST_CHUNK_ROWS")) CH = std::max<int64_t>(1, std::atoll(env));
   CH = std::min(CH, rows_out);
-  const int64_t spitch = round16(W * 4), dpitch = round16(W * 4), mpitch = round16(W);
+  const int64_t spitch = round16(W * src_elem), dpitch = round16(W * 4), mpitch = round16(W);
   const size_t in_bytes = src_h ? (size_t)(CH + up + down) * spitch : 0;
   const size_t out_bytes = dst_h ? (size_t)CH * dpitch : 0;
   const size_t m_bytes = msk_h ? (size_t)CH * mpitch : 0;
@@ -749,14 +800,14 @@ static icl_status run_host(const icl_image* src, const icl_image* dst, const icl
         // the whole set must be free: its previous band's kernel and D2H
         cudaStreamWaitEvent(sg->h2d, sg->comp_done[set], 0);
         cudaStreamWaitEvent(sg->h2d, sg->out_done[set], 0);
-        e = cudaMemcpy2DAsync(set_in(set), spitch, sptr, src->pitch_bytes, W * 4, hi - lo, cudaMemcpyHostToDevice,
-                              sg->h2d);
+        e = cudaMemcpy2DAsync(set_in(set), spitch, sptr, src->pitch_bytes, W * src_elem, hi - lo,
+                              cudaMemcpyHostToDevice, sg->h2d);
         if (e != cudaSuccess) { st = cuda_fail(e, "host path: H2D"); break; }
         cudaEventRecord(sg->in_ready[set], sg->h2d);
         cudaStreamWaitEvent(sg->comp, sg->in_ready[set], 0);
         iv.data = set_in(set);
         iv.pitch_bytes = spitch;
-        h2d += (uint64_t)(W * 4) * (hi - lo);
+        h2d += (uint64_t)(W * src_elem) * (hi - lo);
       }
       cudaStreamWaitEvent(sg->comp, sg->out_done[set], 0);  // set outputs drained by the previous D2H
       if (dst_h) { ov.data = set_out(set); ov.pitch_bytes = dpitch; }
@@ -862,6 +913,21 @@ icl_status icl_nlm(const icl_image* src, const icl_image* dst, int patch_radius,
   return dispatch(pc, static_cast<cudaStream_t>(stream));
 }
 
+icl_status icl_conv2d_u8(const icl_image* src, const icl_image* dst, const float* filter, int radius,
+                         icl_border border, float border_value, const icl_band* band, void* stream) {
+  Prepared pc;
+  icl_status st = prep_conv2d(src, dst, filter, radius, border, border_value, band, &pc);
+  if (st != ICL_OK) return st;
+  if (any_host(src, dst, nullptr)) {
+    return run_host(src, dst, nullptr, band, radius, radius,
+                    [&](const icl_image* s, const icl_image* d, const icl_image*, const icl_band* b, cudaStream_t cs) {
+                      return icl_conv2d_u8(s, d, filter, radius, border, border_value, b, cs);
+                    },
+                    static_cast<cudaStream_t>(stream), 1);
+  }
+  return dispatch(pc, static_cast<cudaStream_t>(stream));
+}
+
 icl_status icl_tune(const icl_problem* p, unsigned flags, void* stream, icl_variant_info* chosen) {
   if (!p) return fail(ICL_ERR_INVALID_ARG, "null problem");
   if (any_host(&p->src, &p->dst, p->filter == ICL_FILTER_HARRIS ? &p->mask : nullptr))
@@ -872,6 +938,9 @@ icl_status icl_tune(const icl_problem* p, unsigned flags, void* stream, icl_vari
     case ICL_FILTER_SEPCONV:
       st = prep_sepconv(&p->src, &p->dst, p->taps_x, p->rx, p->taps_y, p->ry, p->border, p->border_value, nullptr,
                         p->workspace, p->workspace_bytes, &pc);
+      break;
+    case ICL_FILTER_CONV2D:
+      st = prep_conv2d(&p->src, &p->dst, p->filter2d, p->radius2d, p->border, p->border_value, nullptr, &pc);
       break;
     case ICL_FILTER_HARRIS:
       st = prep_harris(&p->src, &p->dst, p->block, p->k, p->border, p->border_value, &p->mask, p->threshold,
@@ -964,7 +1033,7 @@ icl_status icl_force_variant(icl_filter filter, int id) {
 }
 
 int icl_last_variant(icl_filter filter) {
-  if (filter < 0 || filter > 2) return -1;
+  if (filter < 0 || filter >= kNFilters) return -1;
   return t_last[filter];
 }
 

@@ -42,6 +42,15 @@ struct NlmCall {
   float coef; // log2(e) / ((2P+1)^2 h^2), 0 when h = +inf
 };
 
+// non-separable convolution of an 8-bit image (src views bytes)
+struct Conv2dCall {
+  SrcView src;  // uint8 pixels: base / pitch / bstride in bytes
+  DstView dst;  // fp32
+  int batch;
+  int r;        // radius, 0..3
+  float f[49];  // (2r+1)^2 taps, row j major
+};
+
 // sepconv
 cudaError_t launch_sep_naive_direct(const SepCall& c, cudaStream_t s);
 cudaError_t launch_sep_naive_2pass(const SepCall& c, cudaStream_t s);
@@ -63,6 +72,9 @@ cudaError_t launch_nlm_boxsum(const NlmCall& c, int variant, cudaStream_t s);
 cudaError_t launch_nlm_r8(const NlmCall& c, cudaStream_t s);
 cudaError_t launch_nlm_r16(const NlmCall& c, cudaStream_t s);
 cudaError_t launch_nlm_x2(const NlmCall& c, cudaStream_t s);
+// conv2d (u8)
+cudaError_t launch_conv2d_naive(const Conv2dCall& c, cudaStream_t s);
+cudaError_t launch_conv2d_tile(const Conv2dCall& c, int rows_per_thread, cudaStream_t s);
 
 // synthetic inputs
 cudaError_t launch_fill_uniform(float* base, int64_t W, int64_t H, int64_t pitch, int64_t batch,

@@ -47,3 +47,15 @@ def check_nlm(got, img, P, S, h, border, c, points=None, tol=NLM_TOL):
     bad = np.where(scale > 0, err > tol * scale, err != 0)
     assert not bad.any(), f"nlm: {bad.sum()} pixels out of tolerance; max rel {np.max(err / np.maximum(scale, 1e-300))}"
     return float(np.max(err / np.maximum(scale, 1e-300))) if err.size else 0.0
+
+
+def check_conv2d(got, img, filt, border, c, points=None, tol=SEP_TOL):
+    """Non-separable uchar convolution (R22): |y - y^| <= 1e-5 (|f| * |x|)(p), exact 0 where the
+    scale is 0 -- the sepconv bar (north_star's 1e-5 for convolution)."""
+    ref = oracle.conv2d_u8(img, filt, border, c, points=points)
+    scale = oracle.conv2d_u8(img, np.abs(np.asarray(filt, np.float32)), border, abs(c), points=points)
+    got = np.asarray(got, dtype=np.float64)
+    err = np.abs(got - ref)
+    bad = np.where(scale > 0, err > tol * scale, err != 0)
+    assert not bad.any(), f"conv2d: {bad.sum()} pixels out of tolerance; max rel {np.max(err / np.maximum(scale, 1e-300))}"
+    return float(np.max(err / np.maximum(scale, 1e-300))) if err.size else 0.0
