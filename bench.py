@@ -2,7 +2,7 @@
 """bench.py -- megapixels/s of the ImageCL hot path on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl icl|reference]
-                    [--workload suite|sepconv16k] [--batch B] [--size S] [--radius R]
+                    [--workload suite|sepconv16k|conv2d8k] [--batch B] [--size S] [--radius R]
 
 Default workload ("suite", BASELINE.json configs[4] per GPU): every rank
 processes its own batch of B (default 8) synthetic 4096x4096 fp32 images
@@ -569,13 +569,119 @@ def run_sepconv_bands(args):
     return 0
 
 
+def run_conv2d(args):
+    """the paper's third benchmark: non-separable
+    (2r+1)^2 convolution of an 8192^2 unsigned-char image with a run-time filter, clamped
+    boundary, fp32 output (DESIGN.md R22).  One image per rank (image-parallel, weak scaling);
+    two input/output pairs alternate so consecutive steps never hit L2 (2 x 320 MB)."""
+    import numpy as np
+    import torch
+
+    import paper_1605_06399_b200 as icl
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = init_dist(ws, "nccl")
+    icl.load_library()
+    S, r = args.size, args.radius
+    filt = synth.filter2d(8, r)
+    imgs_h = [synth.uniform_u8(1000 * rank + k, S, S) for k in range(2)]
+    imgs = [torch.from_numpy(a).to(dev) for a in imgs_h]
+    outs = [torch.empty(S, S, device=dev) for _ in range(2)]
+    stream = torch.cuda.current_stream(dev)
+    if not args.no_tune:
+        icl.tune("conv2d", imgs[0], outs[0], filter2d=filt, border="clamp", stream=stream)
+
+    def step(k):
+        icl.conv2d_u8(imgs[k & 1], outs[k & 1], filt, "clamp", stream=stream)
+
+    for k in range(max(3, args.warmup)):
+        step(k)
+    torch.cuda.synchronize(dev)
+    variant = icl.variant_names("conv2d")[icl.last_variant("conv2d")]
+    if ws > 1:
+        dist.barrier()
+    n0 = icl.launch_count()
+    with ClockSampler(local) as clk:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for k in range(args.steps):
+            step(k)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+    launches = icl.launch_count() - n0
+    if ws > 1:
+        dist.barrier()
+    step_ms = max_over_ranks(a.elapsed_time(b) / args.steps, ws, dev)
+    px = S * S
+    value = ws * px / (step_ms * 1e-3) / 1e6
+    hbm, hbm_kind = measured_peaks()
+    n = 2 * r + 1
+    gbs = 5 * px / (step_ms * 1e-3) / 1e9
+    tfs = 2 * n * n * px / (step_ms * 1e-3) / 1e12
+    roof = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "traffic": None,
+            "peak_kind": hbm_kind, "bytes_per_px": 5}
+    roof_alu = {"bound": "alu", "achieved": tfs, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": tfs / FP32_PEAK_TFLOPS, "flop_per_px": 2 * n * n}
+    # e2e: the same call with pinned HOST buffers (the library's banded H2D/compute/D2H pipeline)
+    e2e = None
+    if not args.no_e2e:
+        hin = torch.from_numpy(imgs_h[0]).pin_memory()
+        hout = torch.empty(S, S).pin_memory()
+        ke = max(1, min(args.steps, 5))
+        icl.conv2d_u8(hin, hout, filt, "clamp", stream=stream)
+        stream.synchronize()
+        if ws > 1:
+            dist.barrier()
+        x0 = icl.transfer_bytes()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        for _ in range(ke):
+            icl.conv2d_u8(hin, hout, filt, "clamp", stream=stream)
+        eb.record(stream)
+        stream.synchronize()
+        x1 = icl.transfer_bytes()
+        e_ms = max_over_ranks(ea.elapsed_time(eb) / ke, ws, dev)
+        ok = bool(np.array_equal(hout.numpy()[::1021], outs[0].cpu().numpy()[::1021]))
+        e2e = {"value": ws * px / (e_ms * 1e-3) / 1e6, "unit": "Mpx/s", "h2d_bytes_per_step": (x1[0] - x0[0]) // ke,
+               "d2h_bytes_per_step": (x1[1] - x0[1]) // ke, "ms_per_step": e_ms, "steps": ke,
+               "path": "C ABI with pinned host buffers", "matches_device_outputs": ok}
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        import oracle
+        rng = np.random.default_rng(0)
+        npts = 4_000_000
+        xs, ys = rng.integers(0, S, npts), rng.integers(0, S, npts)
+        t0 = time.perf_counter()
+        oracle.conv2d_u8(imgs_h[0], filt, "clamp", points=(xs, ys))
+        dt = time.perf_counter() - t0
+        cpu = {"value": npts / dt / 1e6, "unit": "Mpx/s", "cores": oracle.default_threads(), "kind": "oracle",
+               "sample": f"{npts} random pixels of one {S}x{S} uchar image (f64 oracle, {dt:.1f} s)"}
+    if rank == 0:
+        line = {
+            "metric": f"conv2d_u8 megapixels/s ({S}x{S} uchar, {n}x{n} run-time filter, clamp)",
+            "value": value, "unit": "Mpx/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "conv2d8k (PAPER.md:594-598; SURVEY.md §8(f) row 1)", "size": [S, S],
+                       "radius": r, "border": "clamp", "variant": variant, "images_per_gpu": 1,
+                       "l2": "two input/output pairs alternate (2 x 320 MB > L2)"},
+            "roofline": roof, "rooflines": {"conv2d_hbm": roof, "conv2d_fp32": roof_alu},
+            "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="icl", choices=["icl", "reference"])
-    ap.add_argument("--workload", default="suite", choices=["suite", "sepconv16k"])
+    ap.add_argument("--workload", default="suite", choices=["suite", "sepconv16k", "conv2d8k"])
     ap.add_argument("--radius", type=int, default=2)
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--size", type=int, default=4096)
@@ -587,6 +693,10 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "conv2d8k":
+        if args.size == 4096:
+            args.size = 8192
+        return run_conv2d(args)
     if args.workload == "sepconv16k":
         if args.size == 4096:
             args.size = 16384

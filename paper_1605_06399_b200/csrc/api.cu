@@ -185,6 +185,8 @@ static const Variant kConvVariants[] = {
     {"naive_direct", K_NAIVE, 0, 0, 0},
     {"tile_c4r4", K_C2TILE, 256, 4, 4},
     {"tile_c4r8", K_C2TILE, 256, 4, 8},
+    {"tile_c4r4p", K_C2TILE, 1, 4, 4},
+    {"tile_c4r8p", K_C2TILE, 1, 4, 8},
 };
 
 static const Variant* table(icl_filter f, int* n) {
@@ -260,7 +262,7 @@ static cudaError_t run_variant(const Prepared& pc, const Variant& v, cudaStream_
       return launch_nlm_boxsum(pc.nlm, 0, s);
     case ICL_FILTER_CONV2D:
       if (v.kind == K_NAIVE) return launch_conv2d_naive(pc.c2d, s);
-      return launch_conv2d_tile(pc.c2d, v.S, s);
+      return launch_conv2d_tile(pc.c2d, v.S, v.nt == 1, s);
   }
   return cudaErrorInvalidValue;
 }

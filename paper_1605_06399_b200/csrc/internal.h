@@ -74,7 +74,7 @@ cudaError_t launch_nlm_r16(const NlmCall& c, cudaStream_t s);
 cudaError_t launch_nlm_x2(const NlmCall& c, cudaStream_t s);
 // conv2d (u8)
 cudaError_t launch_conv2d_naive(const Conv2dCall& c, cudaStream_t s);
-cudaError_t launch_conv2d_tile(const Conv2dCall& c, int rows_per_thread, cudaStream_t s);
+cudaError_t launch_conv2d_tile(const Conv2dCall& c, int rows_per_thread, bool persistent, cudaStream_t s);
 
 // synthetic inputs
 cudaError_t launch_fill_uniform(float* base, int64_t W, int64_t H, int64_t pitch, int64_t batch,
