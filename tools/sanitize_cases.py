@@ -41,4 +41,30 @@ for name in ("tile64p_v4", "tile64_v4"):
             icl.sepconv(img, out, fx, fx, border, 0.5)
     torch.cuda.synchronize()
 icl.force_variant("sepconv", None)
+# non-separable uchar convolution: every variant, ragged sizes, both borders, several tiles
+for (h, w) in [(61, 53), (130, 517), (300, 200)]:
+    u8 = torch.from_numpy(synth.uniform_u8(3, h, w)).to(dev)
+    out = torch.empty(h, w, device=dev)
+    for vid, name in enumerate(icl.variant_names("conv2d")):
+        icl.force_variant("conv2d", vid)
+        for border in ("constant", "clamp"):
+            for r in (0, 2, 3):
+                try:
+                    icl.conv2d_u8(u8, out, synth.filter2d(1, r), border, 5.0)
+                except icl.IclError as e:
+                    if e.status not in (3, 4):
+                        raise
+        torch.cuda.synchronize()
+    icl.force_variant("conv2d", None)
+# host-image path (pinned), small bands
+import os  # noqa: E402
+os.environ["ICL_HOST_CHUNK_ROWS"] = "16"
+hs = torch.from_numpy(synth.uniform_image(5, 100, 96)).pin_memory()
+hd = torch.empty(100, 96).pin_memory()
+icl.sepconv(hs, hd, synth.gaussian_taps(2), synth.gaussian_taps(2), "clamp")
+hm = torch.empty(100, 96, dtype=torch.uint8).pin_memory()
+icl.harris(hs, hd, 5, 0.04, "clamp", mask=hm, threshold=0.1)
+icl.nlm(hs, hd, 2, 5, 0.1, "clamp")
+torch.cuda.synchronize()
+del os.environ["ICL_HOST_CHUNK_ROWS"]
 print("sanitize cases done")
