@@ -524,7 +524,13 @@ def run_sepconv_bands(args):
     def call(src, dst, b, st):
         icl.sepconv(src, dst, fx, fx, "constant", band=b, stream=st)
 
+    native = ws > 1 and not args.torch_comm
+    ncomm = icl.Comm(ws, rank) if native else None  # icl_sepconv_sharded: NCCL halo exchange in libicl.so
+
     def step():
+        if native:
+            ncomm.sepconv(buf, out, S, fx, fx, "constant", stream=stream)
+            return
         icd.run_band(call, buf, out, band, (lambda: icd.halo_exchange(buf, band)) if ws > 1 else (lambda: None),
                      stream=stream, comm_stream=comm if ws > 1 else None)
 
@@ -556,7 +562,10 @@ def run_sepconv_bands(args):
             "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": "sepconv16k (BASELINE.json configs[3])", "size": [S, S], "radius": r,
-                       "border": "constant", "halo_rows": [band.up, band.down], "variant":
+                       "border": "constant", "halo_rows": [band.up, band.down],
+                       "exchange": ("icl_sepconv_sharded (NCCL in libicl.so)" if native else
+                                    "torch.distributed batch_isend_irecv" if ws > 1 else "none"),
+                       "variant":
                            icl.variant_names("sepconv")[icl.last_variant("sepconv")],
                        "l2": "input 1 GiB >> L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -564,6 +573,8 @@ def run_sepconv_bands(args):
             "gpu_launches": launches, "clocks": clk.summary(), "e2e": None, "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
+    if ncomm is not None:
+        ncomm.close()
     if ws > 1:
         dist.destroy_process_group()
     return 0
@@ -688,6 +699,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tune", action="store_true")
+    ap.add_argument("--torch-comm", action="store_true", help="sepconv16k: exchange halos via torch.distributed")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

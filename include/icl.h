@@ -162,6 +162,55 @@ icl_status icl_conv2d_u8(const icl_image* src, const icl_image* dst, const float
                          icl_border border, float border_value, const icl_band* band, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Row-band sharding of one large image over the GPUs of a node (SURVEY.md
+ * §8(b) "icl_comm_init / icl_*_sharded", §8(e); BASELINE.json configs[3]).
+ * Rank k of N owns global rows [r0, r1) = [k*ceil(H/N), min(r0+ceil(H/N), H))
+ * and keeps them in a BAND BUFFER holding rows [s0, s1) = [max(0, r0-up),
+ * min(H, r1+down)), where up/down are the filter's stencil rows
+ * (icl_halo_rows).  A sharded call exchanges the halo rows [s0, r0) and
+ * [r1, s1) with ranks k-1 / k+1 by one grouped ncclSend / ncclRecv per
+ * neighbour on the comm's stream, computes the rows that need no halo on
+ * `stream` meanwhile, and the edge rows after the join.  The filter runs on
+ * the band through icl_band (boundary in global coordinates), so the stitched
+ * result equals the unsharded call (bit for bit for sepconv, Harris and
+ * conv2d).  Collective: every rank calls with the same parameters.
+ * NCCL is loaded at run time (libnccl.so.2; the copy torch mapped, if any).
+ * ---------------------------------------------------------------------- */
+typedef struct icl_comm icl_comm;
+
+/* Stencil rows above / below an output row: sepconv p0 = ry; Harris p0 =
+ * block (floor(B/2)+1 above, B-floor(B/2) below); NLM p0 = patch, p1 =
+ * search radius (P+S each side); conv2d p0 = radius. */
+icl_status icl_halo_rows(icl_filter filter, int p0, int p1, int* up, int* down);
+/* out = {r0, r1, s0, s1} of `rank`; ICL_ERR_INVALID_ARG when N > 1 and a
+ * band is thinner than max(up, down) (out is still filled). */
+icl_status icl_shard_band(int64_t global_height, int nranks, int rank, int up, int down, int64_t out[4]);
+/* The rank's exchange: *n <= 2 entries {peer, send_row0, send_row1,
+ * recv_row0, recv_row1} (global rows), symmetric between neighbours. */
+icl_status icl_shard_plan(int64_t global_height, int nranks, int rank, int up, int down, int64_t plan[10], int* n);
+/* 128-byte NCCL unique id (rank 0 creates it; the caller broadcasts it). */
+icl_status icl_comm_unique_id(void* id128);
+icl_status icl_comm_init(icl_comm** comm, int nranks, int rank, const void* id128);
+icl_status icl_comm_destroy(icl_comm* comm);
+/* buf: the rank's band buffer (rows [s0, s1) of the global image, own rows
+ * filled by the caller, halo rows filled by the call; device memory, batch
+ * allowed); dst (and Harris mask): the rank's rows [r0, r1).  Shapes that do
+ * not match the partition -> ICL_ERR_INVALID_ARG; NCCL failures ->
+ * ICL_ERR_NCCL.  Ordered on `stream` (events on it bracket the exchange). */
+icl_status icl_sepconv_sharded(icl_comm* comm, const icl_image* buf, const icl_image* dst, int64_t global_height,
+                               const float* taps_x, int rx, const float* taps_y, int ry, icl_border border,
+                               float border_value, void* stream);
+icl_status icl_harris_sharded(icl_comm* comm, const icl_image* buf, const icl_image* response, int64_t global_height,
+                              int block, float k, icl_border border, float border_value, const icl_image* mask,
+                              float threshold, void* stream);
+icl_status icl_nlm_sharded(icl_comm* comm, const icl_image* buf, const icl_image* dst, int64_t global_height,
+                           int patch_radius, int search_radius, float h, icl_border border, float border_value,
+                           void* stream);
+icl_status icl_conv2d_u8_sharded(icl_comm* comm, const icl_image* buf, const icl_image* dst, int64_t global_height,
+                                 const float* filter, int radius, icl_border border, float border_value,
+                                 void* stream);
+
+/* ------------------------------------------------------------------------
  * Variant space + auto-tuner (§4, Table 1 lines
  * 364-393).
  * ---------------------------------------------------------------------- */

@@ -28,7 +28,9 @@ FILTER = {"sepconv": 0, "harris": 1, "nlm": 2, "conv2d": 3}
 EXPORTS = ("icl_sepconv", "icl_sepconv_workspace_bytes", "icl_harris", "icl_nlm", "icl_conv2d_u8", "icl_tune",
            "icl_tune_cache_save", "icl_tune_cache_load", "icl_tune_cache_clear", "icl_tune_cache_size",
            "icl_variant_count", "icl_variant_name", "icl_force_variant", "icl_last_variant",
-           "icl_launch_count", "icl_transfer_bytes", "icl_last_error", "icl_version", "icl_fill_uniform")
+           "icl_launch_count", "icl_transfer_bytes", "icl_last_error", "icl_version", "icl_fill_uniform",
+           "icl_halo_rows", "icl_shard_band", "icl_shard_plan", "icl_comm_unique_id", "icl_comm_init",
+           "icl_comm_destroy", "icl_sepconv_sharded", "icl_harris_sharded", "icl_nlm_sharded", "icl_conv2d_u8_sharded")
 
 
 class IclError(RuntimeError):
@@ -96,6 +98,16 @@ def load_library(path: str = LIB_PATH):
         "icl_last_error": ([], ctypes.c_char_p),
         "icl_version": ([], ctypes.c_char_p),
         "icl_fill_uniform": ([img, ctypes.c_uint64, I64, P], I),
+        "icl_halo_rows": ([I, I, I, ctypes.POINTER(I), ctypes.POINTER(I)], I),
+        "icl_shard_band": ([I64, I, I, I, I, ctypes.POINTER(I64)], I),
+        "icl_shard_plan": ([I64, I, I, I, I, ctypes.POINTER(I64), ctypes.POINTER(I)], I),
+        "icl_comm_unique_id": ([P], I),
+        "icl_comm_init": ([ctypes.POINTER(P), I, I, P], I),
+        "icl_comm_destroy": ([P], I),
+        "icl_sepconv_sharded": ([P, img, img, I64, P, I, P, I, I, F, P], I),
+        "icl_harris_sharded": ([P, img, img, I64, I, F, I, F, img, F, P], I),
+        "icl_nlm_sharded": ([P, img, img, I64, I, I, F, I, F, P], I),
+        "icl_conv2d_u8_sharded": ([P, img, img, I64, P, I, I, F, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -220,6 +232,92 @@ def conv2d_u8(src, dst, filt, border: str = "clamp", border_value: float = 0.0, 
     return dst
 
 
+# ----------------------------------------------------------------------------- row-band sharding (native NCCL)
+def halo_rows_of(filter: str, p0: int, p1: int = 0) -> tuple:
+    """(up, down) stencil rows of a filter (icl_halo_rows)."""
+    u, d = ctypes.c_int(0), ctypes.c_int(0)
+    _check(load_library().icl_halo_rows(FILTER[filter], p0, p1, ctypes.byref(u), ctypes.byref(d)))
+    return u.value, d.value
+
+
+def shard_band(height: int, nranks: int, rank: int, up: int, down: int) -> tuple:
+    """(r0, r1, s0, s1) of `rank` (icl_shard_band)."""
+    out = (ctypes.c_int64 * 4)()
+    _check(load_library().icl_shard_band(height, nranks, rank, up, down, out))
+    return tuple(out)
+
+
+def shard_plan(height: int, nranks: int, rank: int, up: int, down: int) -> list:
+    """[(peer, (send0, send1), (recv0, recv1))] global rows (icl_shard_plan)."""
+    buf, n = (ctypes.c_int64 * 10)(), ctypes.c_int(0)
+    _check(load_library().icl_shard_plan(height, nranks, rank, up, down, buf, ctypes.byref(n)))
+    return [(int(buf[5 * q]), (int(buf[5 * q + 1]), int(buf[5 * q + 2])), (int(buf[5 * q + 3]), int(buf[5 * q + 4])))
+            for q in range(n.value)]
+
+
+class Comm:
+    """Native row-band communicator (icl_comm over NCCL).  With a torch process group the
+    128-byte NCCL id is created on rank 0 and broadcast through it (plumbing only)."""
+
+    def __init__(self, nranks: int = 1, rank: int = 0, group=None):
+        lib = load_library()
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _check(lib.icl_comm_unique_id(uid))
+        if nranks > 1:
+            import torch.distributed as dist
+            obj = [bytes(uid.raw) if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = ctypes.create_string_buffer(obj[0], 128)
+        self._c = ctypes.c_void_p()
+        _check(lib.icl_comm_init(ctypes.byref(self._c), nranks, rank, uid))
+        self.nranks, self.rank = nranks, rank
+
+    def close(self):
+        if self._c:
+            _check(load_library().icl_comm_destroy(self._c))
+            self._c = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def band(self, height: int, up: int, down: int) -> tuple:
+        return shard_band(height, self.nranks, self.rank, up, down)
+
+    def sepconv(self, buf, dst, height, taps_x, taps_y, border="constant", border_value=0.0, stream=None):
+        fx, gy = _taps(taps_x), _taps(taps_y)
+        _check(load_library().icl_sepconv_sharded(self._c, ctypes.byref(_image(buf)), ctypes.byref(_image(dst)),
+                                                  height, ctypes.cast(fx, ctypes.c_void_p), len(fx) // 2,
+                                                  ctypes.cast(gy, ctypes.c_void_p), len(gy) // 2, BORDER[border],
+                                                  border_value, _stream(stream)))
+        return dst
+
+    def harris(self, buf, response, height, block=5, k=0.04, border="clamp", border_value=0.0, mask=None,
+               threshold=0.0, stream=None):
+        m = _image(mask, 1) if mask is not None else None
+        _check(load_library().icl_harris_sharded(self._c, ctypes.byref(_image(buf)), ctypes.byref(_image(response)),
+                                                 height, block, k, BORDER[border], border_value, _ref(m), threshold,
+                                                 _stream(stream)))
+        return response
+
+    def nlm(self, buf, dst, height, patch_radius=2, search_radius=5, h=0.1, border="clamp", border_value=0.0,
+            stream=None):
+        _check(load_library().icl_nlm_sharded(self._c, ctypes.byref(_image(buf)), ctypes.byref(_image(dst)), height,
+                                              patch_radius, search_radius, h, BORDER[border], border_value,
+                                              _stream(stream)))
+        return dst
+
+    def conv2d_u8(self, buf, dst, height, filt, border="clamp", border_value=0.0, stream=None):
+        f, r = _filter2d(filt)
+        _check(load_library().icl_conv2d_u8_sharded(self._c, ctypes.byref(_image(buf, 1)), ctypes.byref(_image(dst)),
+                                                    height, ctypes.cast(f, ctypes.c_void_p), r, BORDER[border],
+                                                    border_value, _stream(stream)))
+        return dst
+
+
 # ----------------------------------------------------------------------------- tuner / registry
 def tune(filter: str, src, dst, *, force: bool = False, verify: bool = True, stream=None, **params) -> dict:
     """Auto-tune one problem (icl_tune).  ``params`` as for the filter call."""
@@ -328,7 +426,7 @@ def nlm_halo(patch_radius: int, search_radius: int):
     return r, r
 
 
-__all__ = ["sepconv", "harris", "nlm", "conv2d_u8", "tune", "tune_cache_save", "tune_cache_load", "tune_cache_clear",
+__all__ = ["sepconv", "harris", "nlm", "conv2d_u8", "Comm", "shard_band", "shard_plan", "halo_rows_of", "tune", "tune_cache_save", "tune_cache_load", "tune_cache_clear",
            "tune_cache_size", "variant_names", "force_variant", "last_variant", "launch_count", "transfer_bytes", "version",
            "fill_uniform", "load_library", "IclError", "sepconv_workspace_bytes", "harris_halo", "nlm_halo",
            "EXPORTS", "LIB_PATH"]

@@ -47,6 +47,9 @@ static icl_status fail(icl_status st, const char* fmt, ...) {
   t_err = buf;
   return st;
 }
+// for the other translation units of the library (comm.cu): report an error status + message
+icl_status report_error(icl_status st, const char* msg) { return fail(st, "%s", msg); }
+
 static icl_status cuda_fail(cudaError_t e, const char* what) {
   return fail(ICL_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/icl.h"
 #include "common.cuh"
 
 namespace icl {
@@ -50,6 +51,9 @@ struct Conv2dCall {
   int r;        // radius, 0..3
   float f[49];  // (2r+1)^2 taps, row j major
 };
+
+// error reporting shared by the library's translation units (api.cu)
+icl_status report_error(icl_status st, const char* msg);
 
 // sepconv
 cudaError_t launch_sep_naive_direct(const SepCall& c, cudaStream_t s);
