@@ -137,7 +137,7 @@ static icl_status make_views(const icl_image* src, const icl_image* dst, const i
 }
 
 // ------------------------------------------------------------------ variants
-enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL, K_TILE2, K_BOXX2, K_C2TILE };
+enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL, K_TILE2, K_BOXX2, K_C2TILE, K_TEX };
 struct Variant {
   const char* name;
   Kind kind;
@@ -165,6 +165,7 @@ static const Variant kSepVariants[] = {
     {"bulk_nt64_s64", K_BULK, 64, 4, 64},
     {"tile64_v4", K_TILE2, 256, 4, 64},
     {"tile64p_v4", K_TILE2, 256, 4, 1},
+    {"tex_c4s16", K_TEX, 128, 4, 16},
 };
 static const Variant kHarVariants[] = {
     {"naive_direct", K_NAIVE, 0, 0, 0},           {"stream_nt64_s64_v4", K_STREAM, 64, 4, 64},
@@ -190,6 +191,7 @@ static const Variant kConvVariants[] = {
     {"tile_c4r8", K_C2TILE, 256, 4, 8},
     {"tile_c4r4p", K_C2TILE, 1, 4, 4},
     {"tile_c4r8p", K_C2TILE, 1, 4, 8},
+    {"tex_c4r4", K_TEX, 128, 4, 4},
 };
 
 static const Variant* table(icl_filter f, int* n) {
@@ -226,6 +228,13 @@ static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
       v.vec == 4 && !pc.a16)
     return false;
   if (v.kind == K_SHFL && pc.har.block > 5) return false;
+  if (v.kind == K_TEX) {  // hardware boundary: clamp, or constant 0 (border addressing)
+    const SrcView& sv = pc.f == ICL_FILTER_SEPCONV ? pc.sep.src : pc.c2d.src;
+    const int bt = pc.f == ICL_FILTER_SEPCONV ? pc.sep.batch : pc.c2d.batch;
+    if (pc.f == ICL_FILTER_SEPCONV && (pc.sep.rx > 8 || pc.sep.ry > 8)) return false;
+    const bool ok_border = sv.border == kBorderClamp || sv.cval == 0.0f;
+    if (!tex_eligible(sv, sv.Hg - sv.y0, bt, pc.f == ICL_FILTER_CONV2D ? 1 : 4, ok_border)) return false;
+  }
   if (pc.f == ICL_FILTER_SEPCONV && v.kind == K_STREAM &&
       sep_stream_smem_bytes(v.nt, pc.sep.rx > pc.sep.ry ? pc.sep.rx : pc.sep.ry) > 227 * 1024)
     return false;
@@ -251,6 +260,7 @@ static cudaError_t run_variant(const Prepared& pc, const Variant& v, cudaStream_
       if (v.kind == K_TWOPASS) return launch_sep_naive_2pass(pc.sep, s);
       if (v.kind == K_BULK) return launch_sep_bulk(pc.sep, v.nt, v.S, s);
       if (v.kind == K_TILE2) return launch_sep_tile(pc.sep, v.S == 1, s);
+      if (v.kind == K_TEX) return launch_sep_tex(pc.sep, s);
       return launch_sep_stream(pc.sep, v.nt, v.vec, v.S, s);
     case ICL_FILTER_HARRIS:
       if (v.kind == K_NAIVE) return launch_harris_naive(pc.har, s);
@@ -265,6 +275,7 @@ static cudaError_t run_variant(const Prepared& pc, const Variant& v, cudaStream_
       return launch_nlm_boxsum(pc.nlm, 0, s);
     case ICL_FILTER_CONV2D:
       if (v.kind == K_NAIVE) return launch_conv2d_naive(pc.c2d, s);
+      if (v.kind == K_TEX) return launch_conv2d_tex(pc.c2d, s);
       return launch_conv2d_tile(pc.c2d, v.S, v.nt == 1, s);
   }
   return cudaErrorInvalidValue;

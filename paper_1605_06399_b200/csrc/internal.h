@@ -55,6 +55,11 @@ struct Conv2dCall {
 // error reporting shared by the library's translation units (api.cu)
 icl_status report_error(icl_status st, const char* msg);
 
+// texture ("image memory") variants, tex.cu
+bool tex_eligible(const SrcView& s, int64_t rows, int batch, int elem, bool clamp_or_zero);
+cudaError_t launch_sep_tex(const SepCall& c, cudaStream_t s);
+cudaError_t launch_conv2d_tex(const Conv2dCall& c, cudaStream_t s);
+
 // sepconv
 cudaError_t launch_sep_naive_direct(const SepCall& c, cudaStream_t s);
 cudaError_t launch_sep_naive_2pass(const SepCall& c, cudaStream_t s);
