@@ -88,3 +88,41 @@ def test_suite_batch_sampled():
         sel = slice(0, 2500)  # NLM oracle is ~10x costlier per pixel
         check_nlm(o_nlm[i][iy[sel], ix[sel]].cpu().numpy(), ns_h[i], c["nlm_P"], c["nlm_S"], c["nlm_h"],
                   c["nlm_border"], 0.0, points=(xs[sel], ys[sel]))
+
+
+def test_batches_beyond_2gib_use_64bit_offsets():
+    """offsets are int64 (a 64 x 4096^2 batch is 4 GiB).  A 40 x 4096^2 fp32 batch
+    (2.5 GiB) through sepconv / Harris+mask / NLM and a 140 x 4096^2 uint8 batch (2.2 GiB) through
+    conv2d: sampled pixels of the LAST image (byte offsets > 2^31) against the oracle."""
+    B, S = 40, 4096
+    big = torch.empty(B, S, S, device=DEV)
+    icl.fill_uniform(big, 90)
+    last = big[B - 1].cpu().numpy()  # fill_uniform == synth.uniform_image(90 + b) (test_fill_uniform_matches_synth)
+    rng = np.random.default_rng(5)
+    xs = np.concatenate([rng.integers(0, S, 3000), [0, S - 1, 0, S - 1]])
+    ys = np.concatenate([rng.integers(0, S, 3000), [0, 0, S - 1, S - 1]])
+    ix, iy = torch.from_numpy(xs).to(DEV), torch.from_numpy(ys).to(DEV)
+    out = torch.empty_like(big)
+    fx = synth.gaussian_taps(2)
+    icl.sepconv(big, out, fx, fx, "constant")
+    check_sepconv(out[B - 1][iy, ix].cpu().numpy(), last, fx, fx, "constant", 0.0, points=(xs, ys))
+    mask = torch.empty(B, S, S, dtype=torch.uint8, device=DEV)
+    icl.harris(big, out, 5, 0.04, "clamp", mask=mask, threshold=1.0)
+    check_harris(out[B - 1][iy, ix].cpu().numpy(), mask[B - 1][iy, ix].cpu().numpy(), last, 5, 0.04, "clamp", 0.0,
+                 1.0, points=(xs, ys))
+    icl.nlm(big, out, 2, 5, 0.1, "clamp")
+    sel = slice(0, 1000)
+    check_nlm(out[B - 1][iy[sel], ix[sel]].cpu().numpy(), last, 2, 5, 0.1, "clamp", 0.0, points=(xs[sel], ys[sel]))
+    del big, out, mask
+    torch.cuda.empty_cache()
+    Bu = 140
+    u8 = torch.zeros(Bu, S, S, dtype=torch.uint8, device=DEV)
+    img = synth.uniform_u8(91, S, S)
+    u8[Bu - 1] = torch.from_numpy(img).to(DEV)
+    o8 = torch.empty(Bu, S, S, device=DEV)
+    f = synth.filter2d(91, 2)
+    icl.conv2d_u8(u8, o8, f, "clamp")
+    from tests._tol import check_conv2d
+    check_conv2d(o8[Bu - 1][iy, ix].cpu().numpy(), img, f, "clamp", 0.0, points=(xs, ys))
+    del u8, o8
+    torch.cuda.empty_cache()
