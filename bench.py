@@ -491,6 +491,8 @@ def run_suite(args):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if not args.no_small:
+            line["small_configs"] = small_configs(dev)
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -498,6 +500,59 @@ def run_suite(args):
 
 
 # ----------------------------------------------------------------------------- icl arm: row bands
+def small_configs(dev):
+    """BASELINE.json configs[0..2] on one GPU: 512^2 sepconv r=2, 2048^2 Harris B=5 (+mask), 1024^2
+    NLM 5x5/11x11 -- latency-bound sizes, timed per call eagerly and as a replayed CUDA graph of 20
+    calls (the calls only enqueue on the stream, so they capture).  Inputs are L2-resident at these
+    sizes (stated; the %HBM roofline is not meaningful here)."""
+    import torch
+
+    import paper_1605_06399_b200 as icl
+    st = torch.cuda.Stream(device=dev)
+    a = torch.from_numpy(synth.uniform_image(1, 512, 512)).to(dev)
+    h = torch.from_numpy(synth.rect_scene(2, 2048, 2048, noise=0.01)).to(dev)
+    n = torch.from_numpy(synth.rect_scene(3, 1024, 1024, noise=0.0866)).to(dev)
+    fx = synth.gaussian_taps(2)
+    oa, oh, on = torch.empty_like(a), torch.empty_like(h), torch.empty_like(n)
+    mk = torch.empty(2048, 2048, dtype=torch.uint8, device=dev)
+    calls = {
+        "sepconv_512_r2": (lambda: icl.sepconv(a, oa, fx, fx, "constant", stream=st), 512 * 512, "sepconv"),
+        "harris_2048_b5": (lambda: icl.harris(h, oh, 5, 0.04, "clamp", mask=mk, threshold=1.0, stream=st),
+                           2048 * 2048, "harris"),
+        "nlm_1024_5x5_11x11": (lambda: icl.nlm(n, on, 2, 5, 0.1, "clamp", stream=st), 1024 * 1024, "nlm"),
+    }
+    out = {}
+    reps = 20
+    for name, (fn, px, f) in calls.items():
+        with torch.cuda.stream(st):
+            for _ in range(3):
+                fn()
+        st.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        with torch.cuda.stream(st):
+            for _ in range(reps):
+                fn()
+        e1.record(st)
+        st.synchronize()
+        eager_us = e0.elapsed_time(e1) * 1000 / reps
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(reps):
+                fn()
+        g.replay()
+        torch.cuda.synchronize(dev)
+        e0.record(st)
+        with torch.cuda.stream(st):
+            g.replay()
+        e1.record(st)
+        st.synchronize()
+        graph_us = e0.elapsed_time(e1) * 1000 / reps
+        out[name] = {"us_per_call_eager": round(eager_us, 2), "us_per_call_graph": round(graph_us, 2),
+                     "mpx_s_graph": px / graph_us, "variant": icl.variant_names(f)[icl.last_variant(f)]}
+    return out
+
+
 def run_sepconv_bands(args):
     """BASELINE.json configs[3]: one S x S fp32 image, separable Gaussian radius r,
     row-band sharded over the ranks with an NCCL halo exchange (dist.halo_exchange)
@@ -699,6 +754,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tune", action="store_true")
+    ap.add_argument("--no-small", action="store_true", help="suite: skip the configs[0..2] latency block")
     ap.add_argument("--torch-comm", action="store_true", help="sepconv16k: exchange halos via torch.distributed")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -174,7 +174,7 @@ static const Variant kHarVariants[] = {
     {"stream_nt64_s64_v1", K_STREAM, 64, 1, 64},
     {"shfl_nw2_s64", K_SHFL, 2, 4, 64},           {"shfl_nw4_s64", K_SHFL, 4, 4, 64},
     {"shfl_nw2_s32", K_SHFL, 2, 4, 32},           {"shfl_nw4_s32", K_SHFL, 4, 4, 32},
-    {"shfl_nw2_s128", K_SHFL, 2, 4, 128},
+    {"shfl_nw2_s128", K_SHFL, 2, 4, 128},         {"shfl_nw2_s16", K_SHFL, 2, 4, 16},
 };
 static const Variant kNlmVariants[] = {
     {"naive_direct", K_NAIVE, 0, 0, 0},
@@ -309,8 +309,11 @@ static int default_variant(const Prepared& pc) {
       }
     case ICL_FILTER_HARRIS:
       if (!pc.a16) return variant_id(pc.f, "stream_nt64_s64_v1");
-      if (pc.pixels < (1 << 20)) return variant_id(pc.f, "stream_nt32_s16_v4");
-      return variant_id(pc.f, pc.har.block <= 5 ? "shfl_nw2_s64" : "stream_nt64_s64_v4");
+      if (pc.har.block > 5) return variant_id(pc.f, pc.pixels < (1 << 20) ? "stream_nt32_s16_v4" : "stream_nt64_s64_v4");
+      if (pc.pixels < (1 << 16)) return variant_id(pc.f, "stream_nt32_s16_v4");
+      // 240-column strips: short row segments keep enough CTAs in flight up to one 4096^2 image
+      // (1024^2 24.5 vs 34.8 us, 2048^2 30.7 vs 66 us, 4096^2 76 vs 90 us; 8 x 4096^2 prefers s64)
+      return variant_id(pc.f, pc.pixels <= (1 << 25) ? "shfl_nw2_s16" : "shfl_nw2_s64");
     case ICL_FILTER_NLM:
       if (nlm_x2_supported(pc.nlm.P, pc.nlm.S)) return variant_id(pc.f, "boxsum_x2");
       if (nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return variant_id(pc.f, "boxsum_r8");

@@ -7,7 +7,7 @@ set -u
 TAG=${1:-r01}; shift || true
 OUT=gpurun_out/ncu_$TAG
 mkdir -p $OUT
-BENCH="python bench.py --steps 2 --warmup 3 --batch 2 --no-e2e --no-cpu-baseline --no-tune"
+BENCH="python bench.py --steps 2 --warmup 3 --batch 2 --no-e2e --no-cpu-baseline --no-tune --no-small"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $BENCH > $OUT/launches_bench.log 2>&1
 echo "launch list rc=$?"
 REGEXES=("$@")
