@@ -12,6 +12,9 @@ struct SepParams {
   int rx, ry;
   float fx[2 * kMaxRadius + 1];
   float gy[2 * kMaxRadius + 1];
+  // tap pairs (fx[i], fx[i-1]) for two adjacent outputs fed by one input element (FFMA2 with a
+  // broadcast input); i = 1..2R used -- the first / last element of a pair runs as scalar FFMA
+  float2 fxp[2 * kMaxRadius + 2];
 };
 
 // --------------------------------------------------------------------------
@@ -254,6 +257,8 @@ static inline SepParams make_sep_params(const SepCall& c, bool pad) {
     for (int i = 0; i < 2 * c.rx + 1; ++i) p.fx[i] = c.fx[i];
     for (int j = 0; j < 2 * c.ry + 1; ++j) p.gy[j] = c.gy[j];
   }
+  for (int i = 0; i < 2 * kMaxRadius + 2; ++i)
+    p.fxp[i] = make_float2(i < 2 * kMaxRadius + 1 ? p.fx[i] : 0.0f, i >= 1 ? p.fx[i - 1] : 0.0f);
   return p;
 }
 

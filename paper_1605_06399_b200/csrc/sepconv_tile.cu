@@ -225,14 +225,24 @@ __global__ void __launch_bounds__(256, 2) sep_tile_p(SepParams p, int ntx, int n
           const float4 w = reinterpret_cast<const float4*>(src)[q];
           v[4 * q] = w.x; v[4 * q + 1] = w.y; v[4 * q + 2] = w.z; v[4 * q + 3] = w.w;
         }
-        float tt[8];
+        // output columns (2m, 2m+1) share FFMA2 lanes: input element e feeds column 2m with tap
+        // i = e - (HP-R) - 2m and column 2m+1 with tap i-1 -> (fx[i], fx[i-1]) x broadcast(v[e]);
+        // the pair's first / last element feeds one column only (scalar FFMA).  Each lane runs
+        // its own output's chain over i in order: bit-identical.
+        float2 tp[4];
 #pragma unroll
-        for (int o = 0; o < 8; ++o) {
-          float a = 0.0f;
+        for (int m = 0; m < 4; ++m) {
+          float2 a = make_float2(0.0f, 0.0f);
 #pragma unroll
-          for (int i = 0; i < P; ++i) a = __fmaf_rn(p.fx[i], v[HP - R + o + i], a);
-          tt[o] = a;
+          for (int i = 0; i <= P; ++i) {
+            const float ve = v[HP - R + 2 * m + i];
+            if (i == 0) a.x = __fmaf_rn(p.fx[0], ve, a.x);
+            else if (i == P) a.y = __fmaf_rn(p.fx[P - 1], ve, a.y);
+            else a = __ffma2_rn(make_float2(ve, ve), p.fxp[i], a);
+          }
+          tp[m] = a;
         }
+        const float tt[8] = {tp[0].x, tp[0].y, tp[1].x, tp[1].y, tp[2].x, tp[2].y, tp[3].x, tp[3].y};
         float* dst = T + hout[k];
         reinterpret_cast<float4*>(dst)[0] = make_float4(tt[0], tt[1], tt[2], tt[3]);
         reinterpret_cast<float4*>(dst)[1] = make_float4(tt[4], tt[5], tt[6], tt[7]);
