@@ -1,0 +1,126 @@
+"""Randomised parity sweep (seeded, reproducible): many small odd shapes
+(1..70 x 1..300, including 1-row / 1-column images), random radii / windows /
+patch+search sizes, random border modes and constants, padded and unpadded
+pitches -- every eligible variant against the oracle, and the variants of
+sepconv / Harris / conv2d against each other bit for bit."""
+import numpy as np
+import pytest
+
+import synth
+from tests._tol import check_conv2d, check_harris, check_nlm, check_sepconv
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1605_06399_b200 as icl  # noqa: E402
+
+DEV = torch.device("cuda:0")
+CASES = 64
+
+
+def dev_img(a, pad):
+    h, w = a.shape
+    p = w + pad
+    buf = torch.zeros((h, p), dtype=torch.from_numpy(a).dtype, device=DEV)
+    buf[:, :w] = torch.from_numpy(a).to(DEV)
+    return buf[:, :w]
+
+
+def each_variant(f, call):
+    outs = {}
+    for vid, name in enumerate(icl.variant_names(f)):
+        icl.force_variant(f, vid)
+        try:
+            outs[name] = call()
+        except icl.IclError as e:
+            if e.status not in (3, 4):
+                raise
+    icl.force_variant(f, None)
+    return outs
+
+
+def case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    h, w = int(rng.integers(1, 71)), int(rng.integers(1, 301))
+    border = "clamp" if rng.random() < 0.5 else "constant"
+    c = 0.0 if border == "clamp" or rng.random() < 0.4 else float(np.float32(rng.uniform(-1, 2)))
+    pad = int(rng.choice([0, 4, 12]))
+    return rng, h, w, border, c, pad
+
+
+@pytest.mark.parametrize("seed", range(CASES))
+def test_random_sepconv(seed):
+    rng, h, w, border, c, pad = case(seed)
+    rx, ry = int(rng.integers(0, 16)), int(rng.integers(0, 16))
+    img = synth.uniform_image(seed, h, w)
+    fx, gy = synth.signed_taps(seed, rx), synth.gaussian_taps(ry)
+    src = dev_img(img, pad)
+    ws = torch.empty(icl.sepconv_workspace_bytes(w, h, 1, ry) // 4 + 1, device=DEV)
+
+    def call():
+        d = dev_img(np.zeros((h, w), np.float32), pad)
+        icl.sepconv(src, d, fx, gy, border, c, workspace=ws)
+        return d.cpu().numpy()
+    outs = each_variant("sepconv", call)
+    check_sepconv(outs["naive_direct"], img, fx, gy, border, c)
+    for n, o in outs.items():
+        np.testing.assert_array_equal(o, outs["naive_direct"], err_msg=n)
+
+
+@pytest.mark.parametrize("seed", range(CASES))
+def test_random_harris(seed):
+    rng, h, w, border, c, pad = case(seed)
+    block = int(rng.integers(1, 8))
+    img = synth.rect_scene(seed, h, w, n_rect=6, noise=0.01)
+    src = dev_img(img, pad)
+    thr = 0.05
+
+    def call():
+        d = dev_img(np.zeros((h, w), np.float32), pad)
+        m = dev_img(np.zeros((h, w), np.uint8), pad)
+        icl.harris(src, d, block, 0.04, border, c, mask=m, threshold=thr)
+        return d.cpu().numpy(), m.cpu().numpy()
+    outs = each_variant("harris", call)
+    R, M = outs["naive_direct"]
+    check_harris(R, M, img, block, 0.04, border, c, thr)
+    for n, (r, m) in outs.items():
+        np.testing.assert_array_equal(r, R, err_msg=n)
+        np.testing.assert_array_equal(m, M, err_msg=n)
+
+
+@pytest.mark.parametrize("seed", range(CASES // 2))
+def test_random_nlm(seed):
+    rng, h, w, border, c, pad = case(seed)
+    h, w = min(h, 40), min(w, 90)
+    P, S = int(rng.integers(0, 4)), int(rng.integers(0, 8))
+    hh = float(rng.choice([0.05, 0.1, 0.3]))
+    img = synth.rect_scene(seed, h, w, n_rect=5, noise=0.0866)
+    src = dev_img(img, pad)
+
+    def call():
+        d = dev_img(np.zeros((h, w), np.float32), pad)
+        icl.nlm(src, d, P, S, hh, border, c)
+        return d.cpu().numpy()
+    for n, o in each_variant("nlm", call).items():
+        check_nlm(o, img, P, S, hh, border, c)
+
+
+@pytest.mark.parametrize("seed", range(CASES))
+def test_random_conv2d(seed):
+    rng, h, w, border, c, pad = case(seed)
+    r = int(rng.integers(0, 4))
+    img = synth.uniform_u8(seed, h, w)
+    f = synth.filter2d(seed, r)
+    c8 = float(np.float32(abs(c) * 100))
+    src = dev_img(img, pad)
+
+    def call():
+        d = dev_img(np.zeros((h, w), np.float32), pad)
+        icl.conv2d_u8(src, d, f, border, c8)
+        return d.cpu().numpy()
+    outs = each_variant("conv2d", call)
+    check_conv2d(outs["naive_direct"], img, f, border, c8)
+    for n, o in outs.items():
+        np.testing.assert_array_equal(o, outs["naive_direct"], err_msg=n)
