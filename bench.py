@@ -238,6 +238,18 @@ def cpu_oracle_sample(inputs, size, target_s=8.0, threads=0):
     return n, t, tot
 
 
+def cpu_model() -> str:
+    """Host CPU model (record it beside the oracle baseline)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
     ws, rank, _ = dist_env()
@@ -277,7 +289,8 @@ def run_reference(args):
         "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": "suite", "images_per_gpu": args.batch, "size": [size, size], **SUITE},
-        "cpu_baseline": {"value": value, "unit": "Mpx/s", "cores": threads, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "Mpx/s", "cores": threads, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "Mpx/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -466,7 +479,9 @@ def run_suite(args):
     if rank == 0 and not args.no_cpu_baseline:
         import oracle
         n, t, tot = cpu_oracle_sample((u_h[:1], hs_h[:1], ns_h[:1]), S)
+        n1, _, tot1 = cpu_oracle_sample((u_h[:1], hs_h[:1], ns_h[:1]), S, target_s=2.0, threads=1)
         cpu = {"value": n / tot / 1e6, "unit": "Mpx/s", "cores": oracle.default_threads(), "kind": "oracle",
+               "cpu_model": cpu_model(), "value_1_thread": n1 / tot1 / 1e6,
                "sample": f"{n} random pixels of one {S}x{S} image through sepconv+Harris+NLM (f64 oracle); "
                          f"per-filter s: " + ", ".join(f"{k}={v:.2f}" for k, v in t.items())}
 
@@ -722,6 +737,7 @@ def run_conv2d(args):
         oracle.conv2d_u8(imgs_h[0], filt, "clamp", points=(xs, ys))
         dt = time.perf_counter() - t0
         cpu = {"value": npts / dt / 1e6, "unit": "Mpx/s", "cores": oracle.default_threads(), "kind": "oracle",
+               "cpu_model": cpu_model(),
                "sample": f"{npts} random pixels of one {S}x{S} uchar image (f64 oracle, {dt:.1f} s)"}
     if rank == 0:
         line = {
