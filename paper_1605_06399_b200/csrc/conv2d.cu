@@ -60,15 +60,17 @@ template <int R>
 __global__ void __launch_bounds__(128) c2_naive(C2Params p) {
   constexpr int N = 2 * R + 1;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int ly = blockIdx.y, b = blockIdx.z;
+  const int b = blockIdx.z;
   if (x >= p.src.W) return;
-  const int gy = p.dst.y0 + ly;
-  float acc = 0.0f;
+  for (int ly = blockIdx.y; ly < p.dst.H; ly += gridDim.y) {  // grid-stride: any height
+    const int gy = p.dst.y0 + ly;
+    float acc = 0.0f;
 #pragma unroll
-  for (int j = -R; j <= R; ++j)
+    for (int j = -R; j <= R; ++j)
 #pragma unroll
-    for (int i = -R; i <= R; ++i) acc = __fmaf_rn(p.f[(j + R) * N + (i + R)], read_B8(p.src, b, x + i, gy + j), acc);
-  dst_row(p.dst, b, ly)[x] = acc;
+      for (int i = -R; i <= R; ++i) acc = __fmaf_rn(p.f[(j + R) * N + (i + R)], read_B8(p.src, b, x + i, gy + j), acc);
+    dst_row(p.dst, b, ly)[x] = acc;
+  }
 }
 
 // ---------------------------------------------------------------- tile_c4r<RPT>
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(256) c2_tile_p(C2Params p, int ntx, int nty, i
 // ---------------------------------------------------------------- launchers
 template <int R>
 static cudaError_t launch_naive_R(const C2Params& p, int batch, cudaStream_t s) {
-  dim3 grd((p.src.W + 127) / 128, p.dst.H, batch);
+  dim3 grd((p.src.W + 127) / 128, p.dst.H < 65535 ? p.dst.H : 65535, batch);
   c2_naive<R><<<grd, 128, 0, s>>>(p);
   count_launch();
   return cudaGetLastError();

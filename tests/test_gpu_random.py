@@ -124,3 +124,30 @@ def test_random_conv2d(seed):
     check_conv2d(outs["naive_direct"], img, f, border, c8)
     for n, o in outs.items():
         np.testing.assert_array_equal(o, outs["naive_direct"], err_msg=n)
+
+
+def test_tall_images_beyond_65535_rows():
+    """gridDim.y is capped at 65535: every filter's default dispatch (and conv2d's row-per-CTA
+    naive kernel, the only path for unaligned byte images) must still cover 70001-row images."""
+    H, W = 70001, 40
+    img = synth.uniform_image(7, H, W)
+    u8 = synth.uniform_u8(7, H, W)
+    src, src8 = torch.from_numpy(img).to(DEV), torch.from_numpy(u8).to(DEV)
+    out = torch.empty(H, W, device=DEV)
+    mask = torch.empty(H, W, dtype=torch.uint8, device=DEV)
+    rng = np.random.default_rng(7)
+    ys = np.concatenate([rng.integers(0, H, 1500), [0, H - 1, 65535, 65536]])
+    xs = np.concatenate([rng.integers(0, W, 1500), [0, W - 1, 3, 5]])
+    ix, iy = torch.from_numpy(xs).to(DEV), torch.from_numpy(ys).to(DEV)
+    fx = synth.gaussian_taps(2)
+    icl.sepconv(src, out, fx, fx, "clamp")
+    check_sepconv(out[iy, ix].cpu().numpy(), img, fx, fx, "clamp", 0.0, points=(xs, ys))
+    icl.harris(src, out, 5, 0.04, "clamp", mask=mask, threshold=0.1)
+    check_harris(out[iy, ix].cpu().numpy(), mask[iy, ix].cpu().numpy(), img, 5, 0.04, "clamp", 0.0, 0.1,
+                 points=(xs, ys))
+    icl.nlm(src, out, 2, 5, 0.1, "clamp")
+    check_nlm(out[iy, ix].cpu().numpy(), img, 2, 5, 0.1, "clamp", 0.0, points=(xs, ys))
+    f = synth.filter2d(7, 2)
+    icl.conv2d_u8(src8, out, f, "clamp")  # W = 40 bytes: not 16-byte aligned -> naive_direct
+    assert icl.variant_names("conv2d")[icl.last_variant("conv2d")] == "naive_direct"
+    check_conv2d(out[iy, ix].cpu().numpy(), u8, f, "clamp", 0.0, points=(xs, ys))
