@@ -71,7 +71,7 @@ typedef enum { ICL_FILTER_SEPCONV = 0, ICL_FILTER_HARRIS = 1, ICL_FILTER_NLM = 2
  * back into `stream`.  Host buffers must stay valid until `stream` reaches
  * the call (icl_transfer_bytes counts the bytes moved).  Device-resident
  * operands are used in place.  width, height >= 1 and < 2^31; pitch_bytes >=
- * width*elem_size and a multiple of elem_size; batch >= 1; when batch > 1,
+ * width*elem_size and a multiple of elem_size; 1 <= batch < 2^31; when batch > 1,
  * batch_stride_bytes >= height*pitch_bytes (images must not overlap). */
 typedef struct {
     void* data;

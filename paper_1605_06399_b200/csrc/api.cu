@@ -60,7 +60,7 @@ static icl_status check_image(const icl_image* im, int64_t elem, const char* nam
   if (!im->data) return fail(ICL_ERR_INVALID_ARG, "%s: null data pointer", name);
   if (im->width < 1 || im->height < 1 || im->batch < 1)
     return fail(ICL_ERR_INVALID_ARG, "%s: width/height/batch must be >= 1", name);
-  if (im->width >= (1ll << 31) || im->height >= (1ll << 31) || im->batch > 65535)
+  if (im->width >= (1ll << 31) || im->height >= (1ll << 31) || im->batch >= (1ll << 31))
     return fail(ICL_ERR_INVALID_ARG, "%s: size out of range", name);
   if (im->pitch_bytes < im->width * elem || im->pitch_bytes % elem)
     return fail(ICL_ERR_INVALID_ARG, "%s: pitch_bytes must be >= width*%lld and a multiple of %lld", name,
@@ -253,7 +253,41 @@ static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
   return true;
 }
 
+static cudaError_t run_variant_1(const Prepared& pc, const Variant& v, cudaStream_t s);
+
+// gridDim.z (the batch axis of most launchers) is capped at 65535: larger batches run as chunks
+// of images, each a view offset by whole images (per-pixel results do not depend on the split).
 static cudaError_t run_variant(const Prepared& pc, const Variant& v, cudaStream_t s) {
+  constexpr int kMaxZ = 65535;
+  const int batch = pc.f == ICL_FILTER_SEPCONV ? pc.sep.batch
+                    : pc.f == ICL_FILTER_HARRIS ? pc.har.batch
+                    : pc.f == ICL_FILTER_NLM    ? pc.nlm.batch
+                                                : pc.c2d.batch;
+  if (batch <= kMaxZ) return run_variant_1(pc, v, s);
+  for (int b0 = 0; b0 < batch; b0 += kMaxZ) {
+    Prepared c = pc;
+    const int nb = std::min(kMaxZ, batch - b0);
+    auto shift = [&](SrcView& sv, DstView& dv, int& bt) {
+      sv.base += (int64_t)b0 * sv.bstride;
+      dv.base += (int64_t)b0 * dv.bstride;
+      bt = nb;
+    };
+    switch (c.f) {
+      case ICL_FILTER_SEPCONV: shift(c.sep.src, c.sep.dst, c.sep.batch); break;
+      case ICL_FILTER_HARRIS:
+        shift(c.har.src, c.har.dst, c.har.batch);
+        if (c.har.mask) c.har.mask += (int64_t)b0 * c.har.mbstride;
+        break;
+      case ICL_FILTER_NLM: shift(c.nlm.src, c.nlm.dst, c.nlm.batch); break;
+      case ICL_FILTER_CONV2D: shift(c.c2d.src, c.c2d.dst, c.c2d.batch); break;
+    }
+    cudaError_t e = run_variant_1(c, v, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+static cudaError_t run_variant_1(const Prepared& pc, const Variant& v, cudaStream_t s) {
   switch (pc.f) {
     case ICL_FILTER_SEPCONV:
       if (v.kind == K_NAIVE) return launch_sep_naive_direct(pc.sep, s);
@@ -524,19 +558,20 @@ static icl_status prep_conv2d(const icl_image* src, const icl_image* dst, const 
 
 // ------------------------------------------------------------------ tuner
 __global__ void compare_kernel(const char* a, int64_t apitch, int64_t abstride, const float* ref, int W, int H,
-                               unsigned long long* out) {
+                               int64_t nb, unsigned long long* out) {
   // out[0] = #unequal, out[1] = max|a-ref| (float bits), out[2] = max|ref| (float bits)
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y;
-  const int b = blockIdx.z;
   if (x >= W) return;
-  const float va = reinterpret_cast<const float*>(a + (int64_t)b * abstride + (int64_t)y * apitch)[x];
-  const float vr = ref[((int64_t)b * H + y) * W + x];
-  const bool eq = (va == vr) || (va != va && vr != vr);
-  if (!eq) atomicAdd(out, 1ull);
-  const float d = fabsf(va - vr);
-  atomicMax(reinterpret_cast<unsigned int*>(out + 1), __float_as_uint(d != d ? 3.0e38f : d));
-  atomicMax(reinterpret_cast<unsigned int*>(out + 2), __float_as_uint(fabsf(vr)));
+  for (int64_t b = blockIdx.z; b < nb; b += gridDim.z)  // grid-stride: any height / batch
+    for (int y = blockIdx.y; y < H; y += gridDim.y) {
+      const float va = reinterpret_cast<const float*>(a + b * abstride + (int64_t)y * apitch)[x];
+      const float vr = ref[(b * H + y) * W + x];
+      const bool eq = (va == vr) || (va != va && vr != vr);
+      if (!eq) atomicAdd(out, 1ull);
+      const float d = fabsf(va - vr);
+      atomicMax(reinterpret_cast<unsigned int*>(out + 1), __float_as_uint(d != d ? 3.0e38f : d));
+      atomicMax(reinterpret_cast<unsigned int*>(out + 2), __float_as_uint(fabsf(vr)));
+    }
 }
 
 static std::mutex g_tune_mu;
@@ -619,8 +654,8 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
     if ((e = run_variant(pc, vt[v], s)) != cudaSuccess) { ++nrej; cudaGetLastError(); continue; }
     if (!(flags & ICL_TUNE_NO_VERIFY) && v != 0) {
       cudaMemsetAsync(cmp, 0, 3 * sizeof(unsigned long long), s);
-      dim3 g((W + 255) / 256, H, batch);
-      compare_kernel<<<g, 256, 0, s>>>(real_dst.base, real_dst.pitch, real_dst.bstride, ref, W, H, cmp);
+      dim3 g((W + 255) / 256, H < 65535 ? H : 65535, batch < 65535 ? batch : 65535);
+      compare_kernel<<<g, 256, 0, s>>>(real_dst.base, real_dst.pitch, real_dst.bstride, ref, W, H, batch, cmp);
       unsigned long long hc[3];
       cudaMemcpyAsync(hc, cmp, sizeof hc, cudaMemcpyDeviceToHost, s);
       cudaStreamSynchronize(s);

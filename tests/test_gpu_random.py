@@ -151,3 +151,55 @@ def test_tall_images_beyond_65535_rows():
     icl.conv2d_u8(src8, out, f, "clamp")  # W = 40 bytes: not 16-byte aligned -> naive_direct
     assert icl.variant_names("conv2d")[icl.last_variant("conv2d")] == "naive_direct"
     check_conv2d(out[iy, ix].cpu().numpy(), u8, f, "clamp", 0.0, points=(xs, ys))
+
+
+def test_batches_beyond_65535_images():
+    """gridDim.z is capped at 65535: a batch of 70000 small images runs as chunks; first, middle
+    and last images against the oracle, every variant of every filter equal to the default."""
+    B, h, w = 70000, 6, 9
+    imgs = np.stack([synth.uniform_image(i % 17, h, w) for i in range(B)])
+    u8 = np.stack([synth.uniform_u8(i % 13, h, w) for i in range(B)])
+    src, src8 = torch.from_numpy(imgs).to(DEV), torch.from_numpy(u8).to(DEV)
+    fx, f2 = synth.gaussian_taps(1), synth.filter2d(3, 1)
+    picks = (0, 65534, 65535, B - 1)
+    calls = {
+        "sepconv": (lambda o: icl.sepconv(src, o, fx, fx, "clamp"),
+                    lambda o, i: check_sepconv(o, imgs[i], fx, fx, "clamp", 0.0)),
+        "harris": (lambda o: icl.harris(src, o, 3, 0.04, "clamp"),
+                   lambda o, i: check_harris(o, None, imgs[i], 3, 0.04, "clamp", 0.0, 0.0)),
+        "nlm": (lambda o: icl.nlm(src, o, 1, 2, 0.1, "clamp"),
+                lambda o, i: check_nlm(o, imgs[i], 1, 2, 0.1, "clamp", 0.0)),
+        "conv2d": (lambda o: icl.conv2d_u8(src8, o, f2, "clamp"),
+                   lambda o, i: check_conv2d(o, u8[i], f2, "clamp", 0.0)),
+    }
+    for f, (run, check) in calls.items():
+        ref = torch.empty(B, h, w, device=DEV)
+        run(ref)
+        refh = ref.cpu().numpy()
+        for i in picks:
+            check(refh[i], i)
+        for vid, name in enumerate(icl.variant_names(f)):
+            icl.force_variant(f, vid)
+            out = torch.full((B, h, w), float("nan"), device=DEV)
+            try:
+                run(out)
+            except icl.IclError as e:
+                if e.status in (3, 4):
+                    continue
+                raise
+            got = out.cpu().numpy()
+            if f == "nlm":
+                np.testing.assert_allclose(got, refh, rtol=0, atol=2e-5, err_msg=name)
+            else:
+                np.testing.assert_array_equal(got, refh, err_msg=f"{f} {name}")
+        icl.force_variant(f, None)
+
+
+def test_tuner_on_tall_images():
+    """The tuner's device-side equivalence check also covers > 65535 rows."""
+    H, W = 66000, 64
+    img = torch.from_numpy(synth.uniform_image(8, H, W)).to(DEV)
+    out = torch.empty_like(img)
+    info = icl.tune("sepconv", img, out, taps_x=synth.gaussian_taps(1), taps_y=synth.gaussian_taps(1),
+                    border="clamp", force=True)
+    assert info["n_rejected"] == 0 and info["n_candidates"] >= 3
