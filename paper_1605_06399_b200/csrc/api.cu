@@ -257,7 +257,36 @@ static cudaError_t run_variant_1(const Prepared& pc, const Variant& v, cudaStrea
 
 // gridDim.z (the batch axis of most launchers) is capped at 65535: larger batches run as chunks
 // of images, each a view offset by whole images (per-pixel results do not depend on the split).
+static cudaError_t run_variant_rows(const Prepared& pc, const Variant& v, cudaStream_t s);
+
+// Row-segment launchers put H / S (S >= 8) on gridDim.y (<= 65535): images taller than 2^19
+// rows run as row chunks -- the destination view starts at a later global row (dst.y0), exactly
+// an icl_band split, so results equal the one-piece call (bit for bit where the per-output
+// order is shared).
 static cudaError_t run_variant(const Prepared& pc, const Variant& v, cudaStream_t s) {
+  constexpr int kMaxRows = 1 << 19;
+  DstView d = pc.f == ICL_FILTER_SEPCONV ? pc.sep.dst
+              : pc.f == ICL_FILTER_HARRIS ? pc.har.dst
+              : pc.f == ICL_FILTER_NLM    ? pc.nlm.dst
+                                          : pc.c2d.dst;
+  if (d.H <= kMaxRows) return run_variant_rows(pc, v, s);
+  for (int r0 = 0; r0 < d.H; r0 += kMaxRows) {
+    Prepared c = pc;
+    DstView* dv = c.f == ICL_FILTER_SEPCONV ? &c.sep.dst
+                  : c.f == ICL_FILTER_HARRIS ? &c.har.dst
+                  : c.f == ICL_FILTER_NLM    ? &c.nlm.dst
+                                             : &c.c2d.dst;
+    dv->base += (int64_t)r0 * dv->pitch;
+    dv->H = std::min(kMaxRows, d.H - r0);
+    dv->y0 = d.y0 + r0;
+    if (c.f == ICL_FILTER_HARRIS && c.har.mask) c.har.mask += (int64_t)r0 * c.har.mpitch;
+    cudaError_t e = run_variant_rows(c, v, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+static cudaError_t run_variant_rows(const Prepared& pc, const Variant& v, cudaStream_t s) {
   constexpr int kMaxZ = 65535;
   const int batch = pc.f == ICL_FILTER_SEPCONV ? pc.sep.batch
                     : pc.f == ICL_FILTER_HARRIS ? pc.har.batch

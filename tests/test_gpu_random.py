@@ -203,3 +203,25 @@ def test_tuner_on_tall_images():
     info = icl.tune("sepconv", img, out, taps_x=synth.gaussian_taps(1), taps_y=synth.gaussian_taps(1),
                     border="clamp", force=True)
     assert info["n_rejected"] == 0 and info["n_candidates"] >= 3
+
+
+def test_images_beyond_a_million_rows():
+    """Row-segment kernels put H/S on gridDim.y: a 1.2M-row image runs as row chunks (icl_band
+    semantics): the oracle at sampled rows, including both sides of a chunk boundary."""
+    H, W = 1_200_000, 8
+    img = synth.uniform_image(9, H, W)
+    src = torch.from_numpy(img).to(DEV)
+    out = torch.empty_like(src)
+    mask = torch.empty(H, W, dtype=torch.uint8, device=DEV)
+    rng = np.random.default_rng(9)
+    ys = np.concatenate([rng.integers(0, H, 2000), np.arange((1 << 19) - 4, (1 << 19) + 4), [0, H - 1]])
+    xs = rng.integers(0, W, ys.size)
+    ix, iy = torch.from_numpy(xs).to(DEV), torch.from_numpy(ys).to(DEV)
+    fx = synth.gaussian_taps(3)
+    icl.sepconv(src, out, fx, fx, "constant")
+    check_sepconv(out[iy, ix].cpu().numpy(), img, fx, fx, "constant", 0.0, points=(xs, ys))
+    icl.harris(src, out, 5, 0.04, "clamp", mask=mask, threshold=0.1)
+    check_harris(out[iy, ix].cpu().numpy(), mask[iy, ix].cpu().numpy(), img, 5, 0.04, "clamp", 0.0, 0.1,
+                 points=(xs, ys))
+    icl.nlm(src, out, 2, 3, 0.1, "clamp")
+    check_nlm(out[iy, ix].cpu().numpy(), img, 2, 3, 0.1, "clamp", 0.0, points=(xs, ys))
