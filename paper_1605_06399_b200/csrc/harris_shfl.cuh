@@ -299,8 +299,19 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
   const int xl = x0 + 120 * warp + 4 * (lane - 1);
   const float* stb = smem + (xl - (x0 - HP));
   const bool emit = lane >= 1 && lane <= 30;
-  float2 hr2[B][4];
-  float hrxy[B][4];
+  // running vertical window sums instead of a ring of B H-rows: when H-row n arrives, the
+  // oldest chain completes output n-B+1 (c[0] + h), the others take h as their next term and
+  // h starts a new chain -- every output is summed oldest row first, the ring's order
+  constexpr int NC = B > 1 ? B - 1 : 1;
+  float2 c2[NC][4];
+  float cxy[NC][4];
+#pragma unroll
+  for (int k = 0; k < NC; ++k)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // (read only by outputs that are never emitted)
+      c2[k][q] = make_float2(0.0f, 0.0f);
+      cxy[k][q] = 0.0f;
+    }
   float* drow = dst_row(p.dst, b, ly0) + xl;
   const int64_t dpitch = p.dst.pitch >> 2;
   char* mrow = p.mask ? p.mask + (int64_t)b * p.mbstride + (int64_t)ly0 * p.mpitch + xl : nullptr;
@@ -312,7 +323,7 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
     if (i + NBLKS - 1 < NBL) load_block(i + NBLKS - 1);
     cp_async_commit();
     const float* sb = stb + (i % NBLKS) * RB * ROWLEN;
-#pragma unroll
+#pragma unroll 1
     for (int u = 0; u < RB; ++u) {
       const int step = i * RB + u;
       if (step < NY) {
@@ -344,33 +355,44 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
         g[6].y = __shfl_down_sync(0xffffffffu, g[2].y, 1);
         g[7].x = __shfl_down_sync(0xffffffffu, g[3].x, 1);
         g[7].y = __shfl_down_sync(0xffffffffu, g[3].y, 1);
-        const int slot = u % B;
+        float2 h2[4];
+        float hxy[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           float2 hxxyy = make_float2(0.0f, 0.0f);
-          float hxy = 0.0f;
+          float hh = 0.0f;
 #pragma unroll
           for (int t = -A; t <= BB; ++t) {
             const float2 gg = g[2 + q + t];
             hxxyy = __ffma2_rn(gg, gg, hxxyy);
-            hxy = __fmaf_rn(gg.x, gg.y, hxy);
+            hh = __fmaf_rn(gg.x, gg.y, hh);
           }
-          hr2[slot][q] = hxxyy;
-          hrxy[slot][q] = hxy;
+          h2[q] = hxxyy;
+          hxy[q] = hh;
+        }
+        float2 s2o[4];
+        float sxyo[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (B > 1) {
+            s2o[q] = __fadd2_rn(c2[0][q], h2[q]);  // completes output row step-B+1
+            sxyo[q] = __fadd_rn(cxy[0][q], hxy[q]);
+#pragma unroll
+            for (int k = 0; k + 1 < NC; ++k) {
+              c2[k][q] = __fadd2_rn(c2[k + 1][q], h2[q]);
+              cxy[k][q] = __fadd_rn(cxy[k + 1][q], hxy[q]);
+            }
+            c2[NC - 1][q] = h2[q];
+            cxy[NC - 1][q] = hxy[q];
+          } else {
+            s2o[q] = h2[q];
+            sxyo[q] = hxy[q];
+          }
         }
         if (step >= B - 1) {
           float R[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float2 s2 = hr2[(u + 1) % B][q];
-            float sxy = hrxy[(u + 1) % B][q];
-#pragma unroll
-            for (int j = 1; j < B; ++j) {
-              s2 = __fadd2_rn(s2, hr2[(u + 1 + j) % B][q]);
-              sxy = __fadd_rn(sxy, hrxy[(u + 1 + j) % B][q]);
-            }
-            R[q] = harris_R(s2.x, sxy, s2.y, p.k);
-          }
+          for (int q = 0; q < 4; ++q) R[q] = harris_R(s2o[q].x, sxyo[q], s2o[q].y, p.k);
           if (emit) {
             st_cs4(drow, make_float4(R[0], R[1], R[2], R[3]));
             if (mrow)
