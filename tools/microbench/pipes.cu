@@ -180,6 +180,31 @@ __global__ void k_shfl_lds(float* out) {
   if (s == 1234.5f) out[0] = s;
 }
 
+// NA independent FFMA2 chains + NB independent scalar FFMA chains per iteration: do FFMA2 (FMA-heavy
+// pipe) and scalar FFMA (heavy or lite) overlap?  Reported as FMA lanes (flop/2) per clk per SM.
+template <int NA, int NB>
+__global__ void k_mix2(float* out, float a, float b) {
+  float2 r2[NA > 0 ? NA : 1];
+  float r1[NB > 0 ? NB : 1];
+  const float2 A = make_float2(a, a), B2 = make_float2(b, b);
+#pragma unroll
+  for (int i = 0; i < NA; ++i) r2[i] = make_float2(threadIdx.x * 1e-3f + i, i * 0.5f);
+#pragma unroll
+  for (int i = 0; i < NB; ++i) r1[i] = threadIdx.x * 1e-3f + i;
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) r2[i] = __ffma2_rn(r2[i], A, B2);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) r1[i] = __fmaf_rn(r1[i], a, b);
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < NA; ++i) s += r2[i].x + r2[i].y;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) s += r1[i];
+  if (s == 1234.5f) out[0] = s;
+}
+
 template <typename F>
 double run(F launch, double ops_per_thread_iter, int blocks, int threads) {
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -219,6 +244,16 @@ int main() {
   printf("LDS.32 (conflict-free)    : %7.2f Tinst/s  %6.1f words/clk/SM\n", r / 1e12, r / per_sm_clk);
   r = run([&] { k_lds128<<<B, T>>>(d); }, 8, B, T);
   printf("LDS.128 (conflict-free)   : %7.2f Tinst/s  %6.1f words/clk/SM\n", r / 1e12, 4 * r / per_sm_clk);
+  r = run([&] { k_mix2<8, 0><<<B, T>>>(d, 0.999f, 0.001f); }, 16, B, T);
+  printf("FFMA2 only (8 chains)     : %6.1f FMA lanes/clk/SM\n", r / per_sm_clk);
+  r = run([&] { k_mix2<4, 4><<<B, T>>>(d, 0.999f, 0.001f); }, 12, B, T);
+  printf("4 FFMA2 + 4 FFMA          : %6.1f FMA lanes/clk/SM\n", r / per_sm_clk);
+  r = run([&] { k_mix2<4, 8><<<B, T>>>(d, 0.999f, 0.001f); }, 16, B, T);
+  printf("4 FFMA2 + 8 FFMA          : %6.1f FMA lanes/clk/SM\n", r / per_sm_clk);
+  r = run([&] { k_mix2<2, 8><<<B, T>>>(d, 0.999f, 0.001f); }, 12, B, T);
+  printf("2 FFMA2 + 8 FFMA          : %6.1f FMA lanes/clk/SM\n", r / per_sm_clk);
+  r = run([&] { k_mix2<0, 8><<<B, T>>>(d, 0.999f, 0.001f); }, 8, B, T);
+  printf("FFMA only (8 chains)      : %6.1f FMA lanes/clk/SM\n", r / per_sm_clk);
   r = run([&] { k_shfl<8><<<B, T>>>(d); }, 8, B, T);
   printf("SHFL.DOWN (independent)   : %7.2f Tinst/s  %6.1f lanes/clk/SM\n", r / 1e12, r / per_sm_clk);
   r = run([&] { k_shfl_lds<<<B, T>>>(d); }, 8, B, T);
