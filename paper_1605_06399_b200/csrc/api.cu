@@ -417,6 +417,7 @@ static const char* policy() {
 static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, icl_variant_info* info);
 
 static icl_status dispatch(Prepared& pc, cudaStream_t s) {
+  if (pc.f < 0 || pc.f >= kNFilters) return fail(ICL_ERR_INVALID_ARG, "unknown filter");
   int n;
   const Variant* vt = table(pc.f, &n);
   int vid = t_force[pc.f];
