@@ -263,6 +263,39 @@ typedef struct {
 /* (device-resident images only; host images -> ICL_ERR_INVALID_ARG) */
 icl_status icl_tune(const icl_problem* problem, unsigned flags, void* stream, icl_variant_info* chosen);
 
+/* Model-guided tuning (§4: "execute the code of several
+ * randomly selected parameter configurations ... build an artificial neural
+ * network performance model ... predict the execution time of all possible
+ * configurations ... some of the configurations with the best predicted
+ * execution times are executed, and the configuration with the best actual
+ * execution time of these is returned").  Like icl_tune, but phase 1 times n1
+ * randomly drawn eligible variants (seeded), phase 2 fits the surrogate
+ * (ann.cu; R23) to their log median times and times the topk
+ * best-predicted untimed variants; the fastest verified variant is cached.
+ * n1 >= number of eligible variants degenerates to icl_tune (exhaustive).
+ * chosen->n_candidates = variants actually timed.  Synchronises.
+ * Errors: as icl_tune; n1 < 1 or topk < 0 -> ICL_ERR_INVALID_ARG. */
+icl_status icl_tune_ann(const icl_problem* problem, int n1, int topk, uint64_t seed, void* stream,
+                        icl_variant_info* chosen);
+
+/* The surrogate and the two-phase search on their own, for any
+ * configuration space (host only, no GPU).  features: row-major
+ * [n_configs][n_features] numeric encoding of each configuration.
+ * evaluate(ctx, i, &value) returns 0 and a value > 0 (e.g. a time) on success,
+ * non-zero for a failed configuration (kept out of training).  evaluated
+ * (nullable, n_configs ints) receives the indices in evaluation order.
+ * Errors: bad arguments -> ICL_ERR_INVALID_ARG; every evaluation failed ->
+ * ICL_ERR_UNSUPPORTED (best_index = -1). */
+typedef int (*icl_eval_fn)(void* ctx, int index, double* value);
+icl_status icl_ann_search(const double* features, int n_configs, int n_features, icl_eval_fn evaluate, void* ctx,
+                          int n1, int topk, uint64_t seed, int* best_index, double* best_value, int* evaluated,
+                          int* n_evaluated);
+/* Fit the surrogate to n >= 10 samples (value > 0, modelled as log value) and
+ * return its final standardised training MSE and (nullable) its predictions
+ * at the training points.  Fewer than 10 samples -> ICL_ERR_INVALID_ARG. */
+icl_status icl_ann_fit(const double* X, const double* value, int n, int n_features, uint64_t seed, double* final_loss,
+                       double* pred_value);
+
 /* Persist / restore the winner cache (JSON; keyed by device name, SM count
  * and library version + problem key -- the "final implementation" of
  * PAPER.md:233-234). */

@@ -30,7 +30,11 @@ EXPORTS = ("icl_sepconv", "icl_sepconv_workspace_bytes", "icl_harris", "icl_nlm"
            "icl_variant_count", "icl_variant_name", "icl_force_variant", "icl_last_variant",
            "icl_launch_count", "icl_transfer_bytes", "icl_last_error", "icl_version", "icl_fill_uniform",
            "icl_halo_rows", "icl_shard_band", "icl_shard_plan", "icl_comm_unique_id", "icl_comm_init",
-           "icl_comm_destroy", "icl_sepconv_sharded", "icl_harris_sharded", "icl_nlm_sharded", "icl_conv2d_u8_sharded")
+           "icl_comm_destroy", "icl_sepconv_sharded", "icl_harris_sharded", "icl_nlm_sharded", "icl_conv2d_u8_sharded",
+           "icl_tune_ann", "icl_ann_search", "icl_ann_fit")
+
+# int evaluate(void* ctx, int index, double* value) -- icl_ann_search's callback
+EVAL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double))
 
 
 class IclError(RuntimeError):
@@ -108,6 +112,11 @@ def load_library(path: str = LIB_PATH):
         "icl_harris_sharded": ([P, img, img, I64, I, F, I, F, img, F, P], I),
         "icl_nlm_sharded": ([P, img, img, I64, I, I, F, I, F, P], I),
         "icl_conv2d_u8_sharded": ([P, img, img, I64, P, I, I, F, P], I),
+        "icl_tune_ann": ([ctypes.POINTER(icl_problem), I, I, ctypes.c_uint64, P, ctypes.POINTER(icl_variant_info)], I),
+        "icl_ann_search": ([ctypes.POINTER(ctypes.c_double), I, I, EVAL_FN, P, I, I, ctypes.c_uint64,
+                            ctypes.POINTER(I), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I), ctypes.POINTER(I)], I),
+        "icl_ann_fit": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), I, I, ctypes.c_uint64,
+                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -319,8 +328,12 @@ class Comm:
 
 
 # ----------------------------------------------------------------------------- tuner / registry
-def tune(filter: str, src, dst, *, force: bool = False, verify: bool = True, stream=None, **params) -> dict:
-    """Auto-tune one problem (icl_tune).  ``params`` as for the filter call."""
+def tune(filter: str, src, dst, *, force: bool = False, verify: bool = True, stream=None, ann=None,
+         **params) -> dict:
+    """Auto-tune one problem (icl_tune).  ``params`` as for the filter call.
+
+    ``ann=(n1, topk, seed)`` selects the model-guided search (icl_tune_ann,
+    PAPER.md:249-256) instead of timing every eligible variant."""
     lib = load_library()
     p = icl_problem()
     p.filter = FILTER[filter]
@@ -349,10 +362,64 @@ def tune(filter: str, src, dst, *, force: bool = False, verify: bool = True, str
         p.patch_radius, p.search_radius = params.get("patch_radius", 2), params.get("search_radius", 5)
         p.h = params.get("h", 0.1)
     info = icl_variant_info()
-    flags = (1 if force else 0) | (0 if verify else 2)
-    _check(lib.icl_tune(ctypes.byref(p), flags, _stream(stream), ctypes.byref(info)))
+    if ann is not None:
+        n1, topk, seed = ann
+        _check(lib.icl_tune_ann(ctypes.byref(p), int(n1), int(topk), int(seed), _stream(stream), ctypes.byref(info)))
+    else:
+        flags = (1 if force else 0) | (0 if verify else 2)
+        _check(lib.icl_tune(ctypes.byref(p), flags, _stream(stream), ctypes.byref(info)))
     return {"variant_id": info.variant_id, "name": info.name.decode(), "median_us": info.median_us,
             "n_candidates": info.n_candidates, "n_rejected": info.n_rejected, "from_cache": bool(info.from_cache)}
+
+
+def _doubles(rows) -> tuple:
+    rows = [list(map(float, r)) for r in rows]
+    nf = len(rows[0]) if rows else 0
+    if any(len(r) != nf for r in rows):
+        raise ValueError("ragged feature rows")
+    return (ctypes.c_double * max(1, len(rows) * nf))(*[v for r in rows for v in r]), len(rows), nf
+
+
+def ann_search(features, evaluate, n1: int, topk: int, seed: int = 0) -> dict:
+    """Two-phase model-guided search over any configuration space (icl_ann_search).
+
+    ``features``: one numeric row per configuration; ``evaluate(i)`` returns a
+    value > 0 (lower is better) or None for a failed configuration."""
+    lib = load_library()
+    X, n, nf = _doubles(features)
+    err = []
+
+    def cb(_ctx, i, out):
+        try:
+            v = evaluate(int(i))
+        except Exception as e:  # noqa: BLE001 -- surfaced after the call
+            err.append(e)
+            return 1
+        if v is None:
+            return 1
+        out[0] = float(v)
+        return 0
+
+    fn = EVAL_FN(cb)
+    best, bv, ne = ctypes.c_int(-1), ctypes.c_double(0.0), ctypes.c_int(0)
+    order = (ctypes.c_int * max(1, n))()
+    st = lib.icl_ann_search(X, n, nf, fn, None, int(n1), int(topk), int(seed), ctypes.byref(best), ctypes.byref(bv),
+                            order, ctypes.byref(ne))
+    if err:
+        raise err[0]
+    _check(st)
+    return {"best": best.value, "value": bv.value, "evaluated": list(order[:ne.value])}
+
+
+def ann_fit(X, values, seed: int = 0) -> dict:
+    """Fit the tuner's surrogate (icl_ann_fit): final standardised MSE and predictions at X."""
+    lib = load_library()
+    Xc, n, nf = _doubles(X)
+    y = (ctypes.c_double * max(1, n))(*map(float, values))
+    loss = ctypes.c_double(0.0)
+    pred = (ctypes.c_double * max(1, n))()
+    _check(lib.icl_ann_fit(Xc, y, n, nf, int(seed), ctypes.byref(loss), pred))
+    return {"final_loss": loss.value, "pred": list(pred[:n])}
 
 
 def tune_cache_save(path: str):

@@ -414,7 +414,8 @@ static const char* policy() {
   return p ? p : "off";
 }
 
-static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, icl_variant_info* info);
+static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, icl_variant_info* info, int ann_n1 = 0,
+                                 int ann_topk = 0, uint64_t ann_seed = 0);
 
 static icl_status dispatch(Prepared& pc, cudaStream_t s) {
   if (pc.f < 0 || pc.f >= kNFilters) return fail(ICL_ERR_INVALID_ARG, "unknown filter");
@@ -608,7 +609,8 @@ static std::mutex g_tune_mu;
 static void* g_flush = nullptr;
 static size_t g_flush_bytes = 0;
 
-static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, icl_variant_info* info) {
+static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, icl_variant_info* info, int ann_n1,
+                                 int ann_topk, uint64_t ann_seed) {
   std::lock_guard<std::mutex> lk(g_tune_mu);
   int n;
   const Variant* vt = table(pc.f, &n);
@@ -677,11 +679,10 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
   cudaEventCreate(&ev1);
   int best = -1, ncand = 0, nrej = 0;
   float best_us = 0.0f;
-  for (int v = 0; v < n; ++v) {
-    icl_status why;
-    if (!eligible(pc, vt[v], &why)) continue;
+  // Time one variant: verify against the naive output, then the median of >= 10 launches.
+  auto evaluate = [&](int v, float* med_out) -> bool {
     ++ncand;
-    if ((e = run_variant(pc, vt[v], s)) != cudaSuccess) { ++nrej; cudaGetLastError(); continue; }
+    if ((e = run_variant(pc, vt[v], s)) != cudaSuccess) { ++nrej; cudaGetLastError(); return false; }
     if (!(flags & ICL_TUNE_NO_VERIFY) && v != 0) {
       cudaMemsetAsync(cmp, 0, 3 * sizeof(unsigned long long), s);
       dim3 g((W + 255) / 256, H < 65535 ? H : 65535, batch < 65535 ? batch : 65535);
@@ -696,7 +697,7 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
       // sepconv / conv2d variants share one fp32 order per output: bit-identical or rejected
       const bool exact = pc.f == ICL_FILTER_SEPCONV || pc.f == ICL_FILTER_CONV2D;
       const bool ok = exact ? hc[0] == 0 : md <= 1e-4f * std::max(mr, 1e-30f);
-      if (!ok) { ++nrej; continue; }
+      if (!ok) { ++nrej; return false; }
     }
     // warm-up then timed reps (median)
     for (int w = 0; w < 2; ++w) run_variant(pc, vt[v], s);
@@ -715,8 +716,44 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
       if (r >= 10 && total > 200000.0f) break;
     }
     std::sort(ts.begin(), ts.end());
-    const float med = ts[ts.size() / 2];
-    if (best < 0 || med < best_us * 0.995f) { best = v; best_us = med; }
+    *med_out = ts[ts.size() / 2];
+    return true;
+  };
+  if (ann_n1 <= 0) {  // exhaustive
+    for (int v = 0; v < n; ++v) {
+      icl_status why;
+      if (!eligible(pc, vt[v], &why)) continue;
+      float med;
+      if (!evaluate(v, &med)) continue;
+      if (best < 0 || med < best_us * 0.995f) { best = v; best_us = med; }
+    }
+  } else {  // model-guided (ann.cu): features = kind one-hot, log2 CTA threads, vector width, log2 segment rows
+    std::vector<int> ids;
+    for (int v = 0; v < n; ++v) {
+      icl_status why;
+      if (eligible(pc, vt[v], &why)) ids.push_back(v);
+    }
+    constexpr int NK = K_TEX + 1, NF = NK + 3;
+    std::vector<double> feats(ids.size() * NF, 0.0);
+    for (size_t i = 0; i < ids.size(); ++i) {
+      const Variant& vv = vt[ids[i]];
+      double* x = &feats[i * NF];
+      x[vv.kind] = 1.0;
+      x[NK] = std::log2(1.0 + vv.nt);
+      x[NK + 1] = vv.vec;
+      x[NK + 2] = std::log2(1.0 + vv.S);
+    }
+    double bv = 0.0;
+    int bi = -1;
+    ann_search((int)ids.size(), NF, feats.data(),
+               [&](int i, double* val) {
+                 float med;
+                 if (!evaluate(ids[i], &med)) return false;
+                 *val = med;
+                 return true;
+               },
+               ann_n1, ann_topk, ann_seed, nullptr, &bi, &bv);
+    if (bi >= 0) { best = ids[bi]; best_us = (float)bv; }
   }
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
@@ -1012,7 +1049,20 @@ icl_status icl_conv2d_u8(const icl_image* src, const icl_image* dst, const float
   return dispatch(pc, static_cast<cudaStream_t>(stream));
 }
 
+static icl_status tune_entry(const icl_problem* p, unsigned flags, void* stream, icl_variant_info* chosen, int n1,
+                             int topk, uint64_t seed);
+
 icl_status icl_tune(const icl_problem* p, unsigned flags, void* stream, icl_variant_info* chosen) {
+  return tune_entry(p, flags, stream, chosen, 0, 0, 0);
+}
+
+icl_status icl_tune_ann(const icl_problem* p, int n1, int topk, uint64_t seed, void* stream, icl_variant_info* chosen) {
+  if (n1 < 1 || topk < 0) return fail(ICL_ERR_INVALID_ARG, "n1 must be >= 1 and topk >= 0");
+  return tune_entry(p, ICL_TUNE_FORCE, stream, chosen, n1, topk, seed);
+}
+
+static icl_status tune_entry(const icl_problem* p, unsigned flags, void* stream, icl_variant_info* chosen, int n1,
+                             int topk, uint64_t seed) {
   if (!p) return fail(ICL_ERR_INVALID_ARG, "null problem");
   if (any_host(&p->src, &p->dst, p->filter == ICL_FILTER_HARRIS ? &p->mask : nullptr))
     return fail(ICL_ERR_INVALID_ARG, "icl_tune needs device-resident images");
@@ -1038,7 +1088,7 @@ icl_status icl_tune(const icl_problem* p, unsigned flags, void* stream, icl_vari
       return fail(ICL_ERR_INVALID_ARG, "unknown filter");
   }
   if (st != ICL_OK) return st;
-  return tune_prepared(pc, flags, static_cast<cudaStream_t>(stream), chosen);
+  return tune_prepared(pc, flags, static_cast<cudaStream_t>(stream), chosen, n1, topk, seed);
 }
 
 icl_status icl_tune_cache_save(const char* path) {
@@ -1052,6 +1102,7 @@ icl_status icl_tune_cache_save(const char* path) {
     int n;
     const Variant* vt = table(kv.first.rfind("sepconv", 0) == 0   ? ICL_FILTER_SEPCONV
                               : kv.first.rfind("harris", 0) == 0 ? ICL_FILTER_HARRIS
+                              : kv.first.rfind("conv2d", 0) == 0 ? ICL_FILTER_CONV2D
                                                                   : ICL_FILTER_NLM,
                               &n);
     f << "\"" << kv.first << "\": [" << kv.second << ", \"" << (kv.second < n ? vt[kv.second].name : "?") << "\"]"

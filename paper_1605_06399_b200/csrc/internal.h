@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
+#include <vector>
+
 #include "../../include/icl.h"
 #include "common.cuh"
 
@@ -84,6 +87,13 @@ cudaError_t launch_nlm_x2(const NlmCall& c, cudaStream_t s);
 // conv2d (u8)
 cudaError_t launch_conv2d_naive(const Conv2dCall& c, cudaStream_t s);
 cudaError_t launch_conv2d_tile(const Conv2dCall& c, int rows_per_thread, bool persistent, cudaStream_t s);
+
+// auto-tuner performance model (ann.cu): phase 1 runs n1 random configurations,
+// phase 2 trains the surrogate on the ok ones and runs the topk best-predicted
+// unmeasured ones; returns the number of ok measurements.
+constexpr int kAnnMinSamples = 10;
+int ann_search(int ncfg, int nf, const double* feats, const std::function<bool(int, double*)>& evaluate, int n1,
+               int topk, uint64_t seed, std::vector<int>* evaluated, int* best, double* best_val);
 
 // synthetic inputs
 cudaError_t launch_fill_uniform(float* base, int64_t W, int64_t H, int64_t pitch, int64_t batch,

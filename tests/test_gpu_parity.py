@@ -416,6 +416,29 @@ def test_tuner_picks_equivalent_variant_and_caches(tmp_path):
     assert n["n_rejected"] == 0
 
 
+def test_model_guided_tuner(tmp_path):
+    """icl_tune_ann (PAPER.md:249-256): n1 random variants, surrogate, top-k;
+    the winner is a verified variant and is cached like icl_tune's."""
+    icl.tune_cache_clear()
+    img = synth.uniform_image(3, 1024, 1024)
+    src, dst = to_dev(img), empty_like_dev(1024, 1024)
+    n_elig = sum(1 for n in icl.variant_names("sepconv") if n != "naive_2pass")  # (no workspace given)
+    info = icl.tune("sepconv", src, dst, taps_x=synth.gaussian_taps(2), taps_y=synth.gaussian_taps(2),
+                    border="constant", ann=(10, 4, 7))
+    assert info["n_rejected"] == 0 and not info["from_cache"]
+    assert info["n_candidates"] == min(14, n_elig)
+    check_sepconv(host(dst), img, synth.gaussian_taps(2), synth.gaussian_taps(2), "constant", 0.0)
+    icl.sepconv(src, dst, synth.gaussian_taps(2), synth.gaussian_taps(2), "constant")
+    assert icl.last_variant("sepconv") == info["variant_id"]
+    h = icl.tune("harris", src, dst, block=5, k=0.04, border="clamp", ann=(10, 1, 1))
+    assert h["n_rejected"] == 0 and h["n_candidates"] == 11  # 10 + 1 of the 13 Harris variants
+    ref = empty_like_dev(1024, 1024)
+    icl.force_variant("harris", "naive_direct")
+    icl.harris(src, ref, 5, 0.04, "clamp")
+    icl.force_variant("harris", None)
+    assert torch.equal(dst, ref)  # Harris variants share one fp32 order
+
+
 def test_errors_are_reported():
     a = torch.zeros(16, 16, device=DEV)
     with pytest.raises(icl.IclError) as e:
