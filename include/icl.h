@@ -210,6 +210,33 @@ icl_status icl_conv2d_u8_sharded(icl_comm* comm, const icl_image* buf, const icl
                                  const float* filter, int radius, icl_border border, float border_value,
                                  void* stream);
 
+/* Two-filter pipeline in one pass (FAST-style filter
+ * chains, §2.2): separable smoothing then Harris,
+ *     blurred  = icl_sepconv(src, taps_x, rx, taps_y, ry, blur_border, ...)
+ *     response = icl_harris(blurred, block, k, border, ...)   (+ mask)
+ * without the intermediate image in memory (9 B/px of HBM traffic instead
+ * of 8 + 9).  Every blurred value is the sepconv fp32 chain and the Harris
+ * stage is the shfl kernel's, so the result equals the two calls bit for bit.
+ * Layout/ownership as icl_harris; src must not alias response/mask.  Device
+ * images only, 16-byte aligned data/pitches (mask 4-byte).  band: as
+ * icl_harris, with the halo grown by max(rx, ry) rows (rows the blur needs).
+ * Schedules: with workspace_bytes >= icl_blur_harris_workspace_bytes(...)
+ * (device memory, 16-byte aligned, owned by the caller) the chain runs as
+ * the two calls through that intermediate -- faster on B200, where Harris is
+ * issue-bound; with no workspace (NULL / too small) it runs
+ * fused.  Both give the same bits.
+ * Errors: rx or ry > 3, block 6..7, batch > 65535 -> ICL_ERR_UNSUPPORTED;
+ * host images, bad arguments -> ICL_ERR_INVALID_ARG (validation of
+ * icl_sepconv + icl_harris); ICL_ERR_ALIASING as icl_harris, or a workspace
+ * overlapping an image. */
+icl_status icl_blur_harris(const icl_image* src, const icl_image* response, const float* taps_x, int rx,
+                           const float* taps_y, int ry, icl_border blur_border, float blur_border_value, int block,
+                           float k, icl_border border, float border_value, const icl_image* mask, float threshold,
+                           const icl_band* band, void* workspace, size_t workspace_bytes, void* stream);
+/* Bytes of intermediate icl_blur_harris's two-pass schedule needs for a
+ * response of width x height x batch (height: the rows the call produces). */
+size_t icl_blur_harris_workspace_bytes(int64_t width, int64_t height, int64_t batch, int block);
+
 /* ------------------------------------------------------------------------
  * Variant space + auto-tuner (§4, Table 1 lines
  * 364-393).

@@ -31,7 +31,7 @@ EXPORTS = ("icl_sepconv", "icl_sepconv_workspace_bytes", "icl_harris", "icl_nlm"
            "icl_launch_count", "icl_transfer_bytes", "icl_last_error", "icl_version", "icl_fill_uniform",
            "icl_halo_rows", "icl_shard_band", "icl_shard_plan", "icl_comm_unique_id", "icl_comm_init",
            "icl_comm_destroy", "icl_sepconv_sharded", "icl_harris_sharded", "icl_nlm_sharded", "icl_conv2d_u8_sharded",
-           "icl_tune_ann", "icl_ann_search", "icl_ann_fit")
+           "icl_tune_ann", "icl_ann_search", "icl_ann_fit", "icl_blur_harris", "icl_blur_harris_workspace_bytes")
 
 # int evaluate(void* ctx, int index, double* value) -- icl_ann_search's callback
 EVAL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double))
@@ -112,6 +112,8 @@ def load_library(path: str = LIB_PATH):
         "icl_harris_sharded": ([P, img, img, I64, I, F, I, F, img, F, P], I),
         "icl_nlm_sharded": ([P, img, img, I64, I, I, F, I, F, P], I),
         "icl_conv2d_u8_sharded": ([P, img, img, I64, P, I, I, F, P], I),
+        "icl_blur_harris": ([img, img, P, I, P, I, I, F, I, F, I, F, img, F, band, P, ctypes.c_size_t, P], I),
+        "icl_blur_harris_workspace_bytes": ([I64, I64, I64, I], ctypes.c_size_t),
         "icl_tune_ann": ([ctypes.POINTER(icl_problem), I, I, ctypes.c_uint64, P, ctypes.POINTER(icl_variant_info)], I),
         "icl_ann_search": ([ctypes.POINTER(ctypes.c_double), I, I, EVAL_FN, P, I, I, ctypes.c_uint64,
                             ctypes.POINTER(I), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I), ctypes.POINTER(I)], I),
@@ -210,6 +212,30 @@ def harris(src, response, block: int = 5, k: float = 0.04, border: str = "clamp"
     _check(lib.icl_harris(ctypes.byref(s), ctypes.byref(r), block, k, BORDER[border], border_value, _ref(m),
                           threshold, _ref(_band(band)), _stream(stream)))
     return response
+
+
+def blur_harris(src, response, taps_x: Sequence[float], taps_y: Sequence[float], blur_border: str = "clamp",
+                blur_border_value: float = 0.0, block: int = 5, k: float = 0.04, border: str = "clamp",
+                border_value: float = 0.0, mask=None, threshold: float = 0.0, band=None, workspace=None,
+                stream=None):
+    """Smoothing + Harris (icl_blur_harris): equals harris(sepconv(src)) bit for bit.
+
+    ``workspace`` (a CUDA tensor of >= blur_harris_workspace_bytes(...) bytes)
+    selects the two-pass schedule; without it the chain runs fused."""
+    lib = load_library()
+    s, r = _image(src), _image(response)
+    m = _image(mask, 1) if mask is not None else None
+    fx, gy = _taps(taps_x), _taps(taps_y)
+    ws, wsb = (workspace.data_ptr(), workspace.numel() * workspace.element_size()) if workspace is not None else (None, 0)
+    _check(lib.icl_blur_harris(ctypes.byref(s), ctypes.byref(r), ctypes.cast(fx, ctypes.c_void_p), len(fx) // 2,
+                               ctypes.cast(gy, ctypes.c_void_p), len(gy) // 2, BORDER[blur_border],
+                               blur_border_value, block, k, BORDER[border], border_value, _ref(m), threshold,
+                               _ref(_band(band)), ws, wsb, _stream(stream)))
+    return response
+
+
+def blur_harris_workspace_bytes(width: int, height: int, batch: int = 1, block: int = 5) -> int:
+    return int(load_library().icl_blur_harris_workspace_bytes(width, height, batch, block))
 
 
 def nlm(src, dst, patch_radius: int = 2, search_radius: int = 5, h: float = 0.1, border: str = "clamp",

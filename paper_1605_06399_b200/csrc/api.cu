@@ -1018,6 +1018,67 @@ icl_status icl_harris(const icl_image* src, const icl_image* response, int block
   return dispatch(pc, static_cast<cudaStream_t>(stream));
 }
 
+icl_status icl_blur_harris(const icl_image* src, const icl_image* response, const float* taps_x, int rx,
+                           const float* taps_y, int ry, icl_border blur_border, float blur_border_value, int block,
+                           float k, icl_border border, float border_value, const icl_image* mask, float threshold,
+                           const icl_band* band, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!src || !response) return fail(ICL_ERR_INVALID_ARG, "null image descriptor");
+  if (!taps_x || !taps_y) return fail(ICL_ERR_INVALID_ARG, "null taps");
+  if (rx < 0 || ry < 0) return fail(ICL_ERR_INVALID_ARG, "negative radius");
+  if (rx > 3 || ry > 3) return fail(ICL_ERR_UNSUPPORTED, "blur radius > 3 (fused chain instantiations: 0..3)");
+  for (int i = 0; i < 2 * rx + 1; ++i)
+    if (!std::isfinite(taps_x[i])) return fail(ICL_ERR_INVALID_ARG, "non-finite tap");
+  for (int i = 0; i < 2 * ry + 1; ++i)
+    if (!std::isfinite(taps_y[i])) return fail(ICL_ERR_INVALID_ARG, "non-finite tap");
+  if (block > 5 && block <= 7) return fail(ICL_ERR_UNSUPPORTED, "fused chain supports Harris blocks 1..5");
+  if (blur_border != ICL_BORDER_CONSTANT && blur_border != ICL_BORDER_CLAMP)
+    return fail(ICL_ERR_INVALID_ARG, "blur border must be ICL_BORDER_CONSTANT or ICL_BORDER_CLAMP");
+  if (std::isnan(blur_border_value)) return fail(ICL_ERR_INVALID_ARG, "blur border_value is NaN");
+  Prepared pc;
+  icl_status st = prep_harris(src, response, block, k, border, border_value, mask, threshold, band, &pc);
+  if (st != ICL_OK) return st;
+  if (any_host(src, response, mask)) return fail(ICL_ERR_INVALID_ARG, "icl_blur_harris takes device images only");
+  // the stencil of the chain: the Harris rows plus the blur radius
+  const int a = block / 2, bb = block - 1 - a, R = std::max(rx, ry);
+  if ((st = make_views(src, response, band, border, border_value, a + 1 + R, bb + 1 + R, &pc.har.src, &pc.har.dst)))
+    return st;
+  if (!pc.a16) return fail(ICL_ERR_UNSUPPORTED, "fused chain needs 16-byte aligned images, pitches and a 4-byte aligned mask");
+  const int64_t Hg = band ? band->global_height : src->height, dy0 = band ? band->dst_y0 : 0;
+  const int64_t sy0 = band ? band->src_y0 : 0;
+  // Two-pass schedule when the caller gives room for the intermediate: the blurred rows Harris
+  // reads (its halo, clipped to the image) through icl_sepconv, then icl_harris on them -- the
+  // same values as the fused kernel, and faster on B200 (Harris is issue-bound)
+  const int64_t m0 = std::max<int64_t>(0, dy0 - (a + 1)), m1 = std::min<int64_t>(Hg, dy0 + response->height + bb + 1);
+  const int64_t mpitch = (src->width + 3) / 4 * 4 * 4, mrows = m1 - m0;
+  const size_t need = (size_t)(mrows * mpitch * src->batch);
+  if (workspace && workspace_bytes >= need) {
+    Range w{reinterpret_cast<uintptr_t>(workspace), reinterpret_cast<uintptr_t>(workspace) + need};
+    if (overlap(w, byte_range(src, 4)) || overlap(w, byte_range(response, 4)) ||
+        (mask && mask->data && overlap(w, byte_range(mask, 1))))
+      return fail(ICL_ERR_ALIASING, "workspace overlaps an image");
+    if (reinterpret_cast<uintptr_t>(workspace) % 16) return fail(ICL_ERR_INVALID_ARG, "workspace not 16-byte aligned");
+    icl_image mid{workspace, src->width, mrows, mpitch, src->batch, mrows * mpitch};
+    icl_band bs{Hg, sy0, m0}, bh{Hg, m0, dy0};
+    if ((st = icl_sepconv(src, &mid, taps_x, rx, taps_y, ry, blur_border, blur_border_value, &bs, nullptr, 0, stream)))
+      return st;
+    return icl_harris(&mid, response, block, k, border, border_value, mask, threshold, &bh, stream);
+  }
+  const int S = pc.pixels <= (1 << 25) ? 16 : 64;
+  if (src->batch > 65535 || (pc.har.dst.H + S - 1) / S > 65535)
+    return fail(ICL_ERR_UNSUPPORTED, "fused chain: batch > 65535 or image taller than 65535 row segments");
+  SrcView raw = pc.har.src;
+  raw.border = blur_border == ICL_BORDER_CLAMP ? kBorderClamp : kBorderConstant;
+  raw.cval = blur_border_value;
+  cudaError_t e = launch_blur_harris(pc.har, raw, taps_x, rx, taps_y, ry, S, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "blur_harris");
+  return ICL_OK;
+}
+
+size_t icl_blur_harris_workspace_bytes(int64_t width, int64_t height, int64_t batch, int block) {
+  if (width < 1 || height < 1 || batch < 1 || block < 1) return 0;
+  return (size_t)((height + block + 1) * ((width + 3) / 4 * 4) * 4 * batch);
+}
+
 icl_status icl_nlm(const icl_image* src, const icl_image* dst, int patch_radius, int search_radius, float h,
                    icl_border border, float border_value, const icl_band* band, void* stream) {
   Prepared pc;

@@ -76,6 +76,9 @@ cudaError_t launch_sep_tile(const SepCall& c, bool persistent, cudaStream_t s);
 cudaError_t launch_harris_naive(const HarrisCall& c, cudaStream_t s);
 cudaError_t launch_harris_stream(const HarrisCall& c, int nt, int vec, int S, cudaStream_t s);
 cudaError_t launch_harris_shfl(const HarrisCall& c, int nw, int S, cudaStream_t s);
+// two-filter chain (blur_harris.cu): separable blur (radius <= 3) then Harris (block <= 5) in one pass
+cudaError_t launch_blur_harris(const HarrisCall& h, const SrcView& raw, const float* fx, int rx, const float* gy,
+                               int ry, int S, cudaStream_t s);
 
 // nlm
 cudaError_t launch_nlm_naive(const NlmCall& c, cudaStream_t s);
