@@ -302,19 +302,20 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
   // running vertical window sums instead of a ring of B H-rows: when H-row n arrives, the
   // oldest chain completes output n-B+1 (c[0] + h), the others take h as their next term and
   // h starts a new chain -- every output is summed oldest row first, the ring's order
+  // Sxy chains of the output pairs (q = 2m, 2m+1) share float2 lanes (FADD2): the same per-lane adds
   constexpr int NC = B > 1 ? B - 1 : 1;
   float2 c2[NC][4];
-  float cxy[NC][4];
+  float2 cxy[NC][2];
 #pragma unroll
-  for (int k = 0; k < NC; ++k)
+  for (int k = 0; k < NC; ++k) {  // (read only by outputs that are never emitted)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {  // (read only by outputs that are never emitted)
-      c2[k][q] = make_float2(0.0f, 0.0f);
-      cxy[k][q] = 0.0f;
-    }
+    for (int q = 0; q < 4; ++q) c2[k][q] = make_float2(0.0f, 0.0f);
+    cxy[k][0] = cxy[k][1] = make_float2(0.0f, 0.0f);
+  }
   float* drow = dst_row(p.dst, b, ly0) + xl;
   const int64_t dpitch = p.dst.pitch >> 2;
-  char* mrow = p.mask ? p.mask + (int64_t)b * p.mbstride + (int64_t)ly0 * p.mpitch + xl : nullptr;
+  const bool has_mask = p.mask != nullptr;
+  char* mrow = has_mask ? p.mask + (int64_t)b * p.mbstride + (int64_t)ly0 * p.mpitch + xl : nullptr;
 
 #pragma unroll 1
   for (int i = 0; i < NBI; ++i) {
@@ -327,24 +328,34 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
     for (int u = 0; u < RB; ++u) {
       const int step = i * RB + u;
       if (step < NY) {
-        float in[3][6];
+        // columns xl-1 .. xl+4 of the three rows; the differences of the two middle column pairs
+        // run as FADD2 on the aligned halves of the LDS.128 (same per-lane subtractions)
+        float4 w[3];
+        float il[3], ir[3];
+        float hd[3][4];
 #pragma unroll
         for (int rr = 0; rr < 3; ++rr) {
-          const float4 w = *reinterpret_cast<const float4*>(sb + (u + rr) * ROWLEN);
-          in[rr][0] = __shfl_up_sync(0xffffffffu, w.w, 1);
-          in[rr][1] = w.x; in[rr][2] = w.y; in[rr][3] = w.z; in[rr][4] = w.w;
-          in[rr][5] = __shfl_down_sync(0xffffffffu, w.x, 1);
+          w[rr] = *reinterpret_cast<const float4*>(sb + (u + rr) * ROWLEN);
+          il[rr] = __shfl_up_sync(0xffffffffu, w[rr].w, 1);    // column xl-1
+          ir[rr] = __shfl_down_sync(0xffffffffu, w[rr].x, 1);  // column xl+4
+          const float2 m = __fadd2_rn(make_float2(w[rr].z, w[rr].w), make_float2(-w[rr].x, -w[rr].y));
+          hd[rr][0] = __fsub_rn(w[rr].y, il[rr]);
+          hd[rr][1] = m.x;
+          hd[rr][2] = m.y;
+          hd[rr][3] = __fsub_rn(ir[rr], w[rr].z);
         }
         float vd[6];
-#pragma unroll
-        for (int c = 0; c < 6; ++c) vd[c] = __fsub_rn(in[2][c], in[0][c]);
+        {
+          const float2 v12 = __fadd2_rn(make_float2(w[2].x, w[2].y), make_float2(-w[0].x, -w[0].y));
+          const float2 v34 = __fadd2_rn(make_float2(w[2].z, w[2].w), make_float2(-w[0].z, -w[0].w));
+          vd[0] = __fsub_rn(il[2], il[0]);
+          vd[1] = v12.x; vd[2] = v12.y; vd[3] = v34.x; vd[4] = v34.y;
+          vd[5] = __fsub_rn(ir[2], ir[0]);
+        }
         float2 g[8];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const float h0 = __fsub_rn(in[0][c + 2], in[0][c]);
-          const float h1 = __fsub_rn(in[1][c + 2], in[1][c]);
-          const float h2 = __fsub_rn(in[2][c + 2], in[2][c]);
-          g[c + 2].x = __fmaf_rn(2.0f, h1, __fadd_rn(h0, h2));
+          g[c + 2].x = __fmaf_rn(2.0f, hd[1][c], __fadd_rn(hd[0][c], hd[2][c]));
           g[c + 2].y = __fmaf_rn(2.0f, vd[c + 1], __fadd_rn(vd[c], vd[c + 2]));
         }
         g[0].x = __shfl_up_sync(0xffffffffu, g[4].x, 1);
@@ -356,7 +367,7 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
         g[7].x = __shfl_down_sync(0xffffffffu, g[3].x, 1);
         g[7].y = __shfl_down_sync(0xffffffffu, g[3].y, 1);
         float2 h2[4];
-        float hxy[4];
+        float2 hxy[2];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           float2 hxxyy = make_float2(0.0f, 0.0f);
@@ -368,39 +379,46 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
             hh = __fmaf_rn(gg.x, gg.y, hh);
           }
           h2[q] = hxxyy;
-          hxy[q] = hh;
+          if (q & 1) hxy[q >> 1].y = hh;
+          else hxy[q >> 1].x = hh;
         }
         float2 s2o[4];
-        float sxyo[4];
+        float2 sxyo[2];
+        if (B > 1) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (B > 1) {
+          for (int q = 0; q < 4; ++q) {
             s2o[q] = __fadd2_rn(c2[0][q], h2[q]);  // completes output row step-B+1
-            sxyo[q] = __fadd_rn(cxy[0][q], hxy[q]);
 #pragma unroll
-            for (int k = 0; k + 1 < NC; ++k) {
-              c2[k][q] = __fadd2_rn(c2[k + 1][q], h2[q]);
-              cxy[k][q] = __fadd_rn(cxy[k + 1][q], hxy[q]);
-            }
+            for (int k = 0; k + 1 < NC; ++k) c2[k][q] = __fadd2_rn(c2[k + 1][q], h2[q]);
             c2[NC - 1][q] = h2[q];
-            cxy[NC - 1][q] = hxy[q];
-          } else {
-            s2o[q] = h2[q];
-            sxyo[q] = hxy[q];
           }
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            sxyo[m] = __fadd2_rn(cxy[0][m], hxy[m]);
+#pragma unroll
+            for (int k = 0; k + 1 < NC; ++k) cxy[k][m] = __fadd2_rn(cxy[k + 1][m], hxy[m]);
+            cxy[NC - 1][m] = hxy[m];
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) s2o[q] = h2[q];
+          sxyo[0] = hxy[0];
+          sxyo[1] = hxy[1];
         }
         if (step >= B - 1) {
           float R[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) R[q] = harris_R(s2o[q].x, sxyo[q], s2o[q].y, p.k);
+          R[0] = harris_R(s2o[0].x, sxyo[0].x, s2o[0].y, p.k);
+          R[1] = harris_R(s2o[1].x, sxyo[0].y, s2o[1].y, p.k);
+          R[2] = harris_R(s2o[2].x, sxyo[1].x, s2o[2].y, p.k);
+          R[3] = harris_R(s2o[3].x, sxyo[1].y, s2o[3].y, p.k);
           if (emit) {
             st_cs4(drow, make_float4(R[0], R[1], R[2], R[3]));
-            if (mrow)
+            if (has_mask)
               *reinterpret_cast<uchar4*>(mrow) =
                   make_uchar4(R[0] > p.threshold, R[1] > p.threshold, R[2] > p.threshold, R[3] > p.threshold);
           }
           drow += dpitch;
-          if (mrow) mrow += p.mpitch;
+          mrow += has_mask ? p.mpitch : 0;
         }
       }
     }
