@@ -105,6 +105,9 @@ __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, f
   const int xl = x0 + 120 * warp + 4 * (lane - 1);
   const int si = xl - (x0 - HP);
   const bool emit = lane >= 1 && lane <= 30 && xl < W;
+  // a warp whose columns (and left halo lane) all lie right of the image produces nothing: it only
+  // helps load the ring (right edge strip: e.g. 16 of 240 columns in the image at W = 4096)
+  const bool warp_live = x0 + 120 * warp - 4 < W;
   // lanes of this warp owning image columns 0 and W-1 (for the dx/dy boundary)
   const int xw = x0 + 120 * warp - 4;  // first column of lane 0
   const int ll = (0 - xw) >> 2, el = (0 - xw) & 3;
@@ -127,6 +130,7 @@ __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, f
     if (i + NBLKS - 1 < NBL) load_block(i + NBLKS - 1);
     cp_async_commit();
     const int base = (i % NBLKS) * RB;
+    if (!warp_live) continue;
 #pragma unroll
     for (int u = 0; u < RB; ++u) {
       const int step = i * RB + u;

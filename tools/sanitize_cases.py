@@ -67,4 +67,16 @@ icl.harris(hs, hd, 5, 0.04, "clamp", mask=hm, threshold=0.1)
 icl.nlm(hs, hd, 2, 5, 0.1, "clamp")
 torch.cuda.synchronize()
 del os.environ["ICL_HOST_CHUNK_ROWS"]
+# fused smoothing + Harris chain (and its two-pass schedule): ragged sizes, all radii, both borders
+for (h, w) in [(61, 52), (130, 516), (300, 200)]:
+    img = torch.from_numpy(synth.uniform_image(6, h, w)).to(dev)
+    out = torch.empty_like(img)
+    mask = torch.empty(h, w, dtype=torch.uint8, device=dev)
+    ws = torch.empty(icl.blur_harris_workspace_bytes(w, h, 1, 5) // 4 + 4, device=dev)
+    for r in (0, 1, 2, 3):
+        fx = synth.gaussian_taps(r)
+        for bb, hb in (("constant", "clamp"), ("clamp", "constant")):
+            icl.blur_harris(img, out, fx, fx, bb, 0.5, 5, 0.04, hb, 0.25, mask=mask, threshold=0.1)
+            icl.blur_harris(img, out, fx, fx, bb, 0.5, 3, 0.04, hb, 0.25, mask=mask, threshold=0.1, workspace=ws)
+    torch.cuda.synchronize()
 print("sanitize cases done")
