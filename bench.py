@@ -594,10 +594,27 @@ def run_sepconv_bands(args):
     def call(src, dst, b, st):
         icl.sepconv(src, dst, fx, fx, "constant", band=b, stream=st)
 
-    native = ws > 1 and not args.torch_comm
+    peer = ws > 1 and args.halo == "peer"
+    native = ws > 1 and not args.torch_comm and not peer
     ncomm = icl.Comm(ws, rank) if native else None  # icl_sepconv_sharded: NCCL halo exchange in libicl.so
+    if peer:  # icl_sepconv_peer: own rows only, the halo read in-kernel from the neighbours (CUDA IPC)
+        own = buf[band.own_slice]
+        meta = [None] * ws
+        dist.all_gather_object(meta, icl.ipc_handle(buf) + (band.r0 - band.s0,))
+        nbr = {}
+        for q in (rank - 1, rank + 1):
+            if 0 <= q < ws:
+                qb = icd.partition(S, ws, q, r, r)
+                h, off, skip = meta[q]
+                nbr[q] = icl.PeerImage(h, off + skip * S * 4, S, qb.rows, S)
+        torch.cuda.synchronize(dev)
+        dist.barrier()  # every rank's own rows are written
 
     def step():
+        if peer:
+            icl.sepconv_peer(own, out, S, band.r0, nbr.get(rank - 1), nbr.get(rank + 1), fx, fx, "constant",
+                             stream=stream)
+            return
         if native:
             ncomm.sepconv(buf, out, S, fx, fx, "constant", stream=stream)
             return
@@ -633,7 +650,8 @@ def run_sepconv_bands(args):
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": "sepconv16k (BASELINE.json configs[3])", "size": [S, S], "radius": r,
                        "border": "constant", "halo_rows": [band.up, band.down],
-                       "exchange": ("icl_sepconv_sharded (NCCL in libicl.so)" if native else
+                       "exchange": ("icl_sepconv_peer (halo rows loaded in-kernel from the peers, CUDA IPC)"
+                                    if peer else "icl_sepconv_sharded (NCCL in libicl.so)" if native else
                                     "torch.distributed batch_isend_irecv" if ws > 1 else "none"),
                        "variant":
                            icl.variant_names("sepconv")[icl.last_variant("sepconv")],
@@ -645,6 +663,10 @@ def run_sepconv_bands(args):
         print(json.dumps(line), flush=True)
     if ncomm is not None:
         ncomm.close()
+    if peer:
+        dist.barrier()  # no rank frees its band while a peer may still read it
+        for p in nbr.values():
+            p.close()
     if ws > 1:
         dist.destroy_process_group()
     return 0
@@ -772,6 +794,9 @@ def main():
     ap.add_argument("--no-tune", action="store_true")
     ap.add_argument("--no-small", action="store_true", help="suite: skip the configs[0..2] latency block")
     ap.add_argument("--torch-comm", action="store_true", help="sepconv16k: exchange halos via torch.distributed")
+    ap.add_argument("--halo", default="nccl", choices=["nccl", "peer"],
+                    help="sepconv16k, N > 1: NCCL send/recv (icl_sepconv_sharded) or in-kernel peer loads "
+                         "(icl_sepconv_peer over CUDA IPC)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -238,6 +238,37 @@ icl_status icl_blur_harris(const icl_image* src, const icl_image* response, cons
 size_t icl_blur_harris_workspace_bytes(int64_t width, int64_t height, int64_t batch, int block);
 
 /* ------------------------------------------------------------------------
+ * Row bands with the halo read in the kernel from the neighbours' memory
+ * (in-kernel NVLink halo reads instead of send/recv).
+ * ---------------------------------------------------------------------- */
+
+/* CUDA IPC export of a device pointer: a 64-byte handle of its allocation
+ * plus the pointer's byte offset inside it (send both to the other ranks). */
+icl_status icl_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset);
+/* Map a handle from another process of this node; *dev_ptr = base + offset.
+ * Errors: ICL_ERR_CUDA with the runtime's message (e.g. same process). */
+icl_status icl_ipc_open(const void* handle64, uint64_t offset, void** dev_ptr);
+icl_status icl_ipc_close(void* dev_ptr, uint64_t offset);
+
+/* Separable convolution of the global rows [own_y0, own_y0 + own->height) of
+ * an image of global_height rows whose row bands live on different GPUs.
+ * own: this rank's rows ONLY (no halo rows); up / down: the neighbouring
+ * ranks' bands (device pointers mapped with icl_ipc_open, or any device
+ * memory this GPU can read) -- `up` ends at global row own_y0, `down` starts
+ * at own_y0 + own->height; either may be NULL at the image edge.  The rows
+ * that need no halo run on the ordinary kernels; the edge rows' kernel loads
+ * its input rows from `own`, `up` or `down` directly (peer loads over NVLink):
+ * no staging, no send/recv.  The boundary applies at the GLOBAL edges, so the
+ * stitched outputs equal the unsharded icl_sepconv bit for bit.  Ordering: the
+ * neighbours' rows must be complete before the call's kernels run and stay
+ * unchanged until they finish (bracket the call with a cross-rank barrier).
+ * Errors: geometry (dst shape != own, neighbour missing or thinner than ry
+ * rows where needed, radius > 15) -> ICL_ERR_INVALID_ARG. */
+icl_status icl_sepconv_peer(const icl_image* own, const icl_image* dst, int64_t global_height, int64_t own_y0,
+                            const icl_image* up, const icl_image* down, const float* taps_x, int rx,
+                            const float* taps_y, int ry, icl_border border, float border_value, void* stream);
+
+/* ------------------------------------------------------------------------
  * Variant space + auto-tuner (§4, Table 1 lines
  * 364-393).
  * ---------------------------------------------------------------------- */

@@ -31,7 +31,8 @@ EXPORTS = ("icl_sepconv", "icl_sepconv_workspace_bytes", "icl_harris", "icl_nlm"
            "icl_launch_count", "icl_transfer_bytes", "icl_last_error", "icl_version", "icl_fill_uniform",
            "icl_halo_rows", "icl_shard_band", "icl_shard_plan", "icl_comm_unique_id", "icl_comm_init",
            "icl_comm_destroy", "icl_sepconv_sharded", "icl_harris_sharded", "icl_nlm_sharded", "icl_conv2d_u8_sharded",
-           "icl_tune_ann", "icl_ann_search", "icl_ann_fit", "icl_blur_harris", "icl_blur_harris_workspace_bytes")
+           "icl_tune_ann", "icl_ann_search", "icl_ann_fit", "icl_blur_harris", "icl_blur_harris_workspace_bytes",
+           "icl_ipc_get_handle", "icl_ipc_open", "icl_ipc_close", "icl_sepconv_peer")
 
 # int evaluate(void* ctx, int index, double* value) -- icl_ann_search's callback
 EVAL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double))
@@ -114,6 +115,10 @@ def load_library(path: str = LIB_PATH):
         "icl_conv2d_u8_sharded": ([P, img, img, I64, P, I, I, F, P], I),
         "icl_blur_harris": ([img, img, P, I, P, I, I, F, I, F, I, F, img, F, band, P, ctypes.c_size_t, P], I),
         "icl_blur_harris_workspace_bytes": ([I64, I64, I64, I], ctypes.c_size_t),
+        "icl_ipc_get_handle": ([P, P, ctypes.POINTER(ctypes.c_uint64)], I),
+        "icl_ipc_open": ([P, ctypes.c_uint64, ctypes.POINTER(P)], I),
+        "icl_ipc_close": ([P, ctypes.c_uint64], I),
+        "icl_sepconv_peer": ([img, img, I64, I64, img, img, P, I, P, I, I, F, P], I),
         "icl_tune_ann": ([ctypes.POINTER(icl_problem), I, I, ctypes.c_uint64, P, ctypes.POINTER(icl_variant_info)], I),
         "icl_ann_search": ([ctypes.POINTER(ctypes.c_double), I, I, EVAL_FN, P, I, I, ctypes.c_uint64,
                             ctypes.POINTER(I), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I), ctypes.POINTER(I)], I),
@@ -446,6 +451,43 @@ def ann_fit(X, values, seed: int = 0) -> dict:
     pred = (ctypes.c_double * max(1, n))()
     _check(lib.icl_ann_fit(Xc, y, n, nf, int(seed), ctypes.byref(loss), pred))
     return {"final_loss": loss.value, "pred": list(pred[:n])}
+
+
+def ipc_handle(t) -> tuple:
+    """(64-byte CUDA IPC handle, byte offset) of a CUDA tensor's data, for another process of this node."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_uint64(0)
+    _check(load_library().icl_ipc_get_handle(t.data_ptr(), h, ctypes.byref(off)))
+    return h.raw, off.value
+
+
+class PeerImage:
+    """A neighbour's band mapped with icl_ipc_open (close() unmaps it)."""
+
+    def __init__(self, handle: bytes, offset: int, width: int, height: int, pitch_elems: int, batch: int = 1,
+                 batch_stride_elems: int = 0):
+        p = ctypes.c_void_p(0)
+        _check(load_library().icl_ipc_open(handle, offset, ctypes.byref(p)))
+        self.ptr, self.offset = p.value, offset
+        self.image = icl_image(self.ptr, width, height, pitch_elems * 4, batch, batch_stride_elems * 4)
+
+    def close(self):
+        if self.ptr:
+            _check(load_library().icl_ipc_close(self.ptr, self.offset))
+            self.ptr = None
+
+
+def sepconv_peer(own, dst, global_height: int, own_y0: int, up: Optional[PeerImage], down: Optional[PeerImage],
+                 taps_x, taps_y, border: str = "constant", border_value: float = 0.0, stream=None):
+    """One rank's rows of a row-band sharded sepconv, halo rows read in-kernel from the peers (icl_sepconv_peer)."""
+    lib = load_library()
+    o, d = _image(own), _image(dst)
+    fx, gy = _taps(taps_x), _taps(taps_y)
+    _check(lib.icl_sepconv_peer(ctypes.byref(o), ctypes.byref(d), global_height, own_y0,
+                                ctypes.byref(up.image) if up else None, ctypes.byref(down.image) if down else None,
+                                ctypes.cast(fx, ctypes.c_void_p), len(fx) // 2, ctypes.cast(gy, ctypes.c_void_p),
+                                len(gy) // 2, BORDER[border], border_value, _stream(stream)))
+    return dst
 
 
 def tune_cache_save(path: str):

@@ -1,0 +1,234 @@
+// peer.cu -- row-band sharding with the halo read IN the filter kernel from the
+// neighbouring ranks' memory ("in-kernel NVLink halo
+// reads instead of send/recv ... the edge CTAs load neighbor rows directly,
+// which fuses the 'collective' into the filter kernel").
+//
+// Ranks of one node map each other's band buffers with CUDA IPC
+// (icl_ipc_get_handle / icl_ipc_open; the 64-byte handles travel over any
+// host channel, e.g. the torch process group).  A rank's buffer then holds
+// ONLY its own rows -- no halo rows, no staging, no send/recv, no pack /
+// unpack: the rows that need no halo run through the ordinary icl_sepconv
+// kernels on the own band, and the edge rows run through sep_edge_peer, whose
+// loads resolve every input row to the own band or to the up / down
+// neighbour's band (peer loads over NVLink on a multi-GPU node).  The global
+// boundary is applied before the resolution, in global coordinates, so the
+// stitched result equals the unsharded call bit for bit (same fp32 chains as
+// every sepconv variant, R16).
+//
+// Ordering contract: the neighbours' rows must be written before this call's
+// kernels run and must not be overwritten until they finish -- the caller
+// brackets the call with a barrier across the ranks (the pattern of a
+// static, pre-sharded input such as BASELINE configs[3]).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "../../include/icl.h"
+#include "common.cuh"
+#include "internal.h"
+
+namespace icl {
+namespace {
+
+struct RowSeg {     // rows [y0, y1) of one band buffer
+  const char* base; // row y0 of image 0
+  int64_t pitch, bstride;
+  int y0, y1;
+};
+
+struct EdgeParams {
+  RowSeg seg[3];  // up, own, down (empty: y0 == y1)
+  int W, Hg;
+  int border;
+  float cval;
+  int rx, ry;
+  float fx[2 * kMaxRadius + 1], gy[2 * kMaxRadius + 1];
+  char* dst;      // output row `out_y0` of image 0
+  int64_t dpitch, dbstride;
+  int out_y0, out_y1;  // global output rows of this launch
+};
+
+constexpr int kEdgeTW = 128;  // output columns per CTA (one per thread)
+constexpr int kEdgeCH = 16;   // output rows per CTA
+
+// in_B(x, gy) row pointer after the global boundary; nullptr -> the constant row
+__device__ __forceinline__ const float* edge_row(const EdgeParams& p, int b, int gy) {
+  if (gy < 0 || gy >= p.Hg) {
+    if (p.border == kBorderConstant) return nullptr;
+    gy = clampi(gy, 0, p.Hg - 1);
+  }
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    const RowSeg& g = p.seg[s];
+    if (gy >= g.y0 && gy < g.y1)
+      return reinterpret_cast<const float*>(g.base + (int64_t)b * g.bstride + (int64_t)(gy - g.y0) * g.pitch);
+  }
+  return nullptr;  // unreachable for a validated call
+}
+
+// One CTA: kEdgeTW columns x kEdgeCH output rows.  Row pass of every input row
+// the chunk needs into shared memory (the fp32 chain over i), then the column
+// pass (the chain over j) -- the per-output operation order of every sepconv
+// variant.  Input rows come from the own band or straight from a peer's band.
+__global__ void __launch_bounds__(kEdgeTW) sep_edge_peer(EdgeParams p) {
+  extern __shared__ float sm[];
+  const int tid = threadIdx.x;
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * kEdgeTW;
+  const int y0 = p.out_y0 + blockIdx.y * kEdgeCH;
+  const int y1 = min(y0 + kEdgeCH, p.out_y1);
+  const int NR = (y1 - y0) + 2 * p.ry;  // input rows
+  const int RL = kEdgeTW + 2 * p.rx;
+  float* raw = sm;                      // one input row (+ rx columns each side)
+  float* t = sm + RL + 2 * kMaxRadius;  // NR row-pass rows
+  const int x = x0 + tid;
+  for (int k = 0; k < NR; ++k) {
+    const float* row = edge_row(p, b, y0 - p.ry + k);
+    __syncthreads();
+    for (int c = tid; c < RL; c += kEdgeTW) {
+      int xx = x0 - p.rx + c;
+      float v;
+      if (!row) v = p.cval;
+      else if (xx < 0 || xx >= p.W) v = p.border == kBorderConstant ? p.cval : row[clampi(xx, 0, p.W - 1)];
+      else v = row[xx];
+      raw[c] = v;
+    }
+    __syncthreads();
+    float a = 0.0f;
+    for (int i = 0; i <= 2 * p.rx; ++i) a = __fmaf_rn(p.fx[i], raw[tid + i], a);
+    t[k * kEdgeTW + tid] = a;
+  }
+  __syncthreads();
+  if (x >= p.W) return;
+  for (int y = y0; y < y1; ++y) {
+    const int k0 = y - y0;
+    float acc = 0.0f;
+    for (int j = 0; j <= 2 * p.ry; ++j) acc = __fmaf_rn(p.gy[j], t[(k0 + j) * kEdgeTW + tid], acc);
+    reinterpret_cast<float*>(p.dst + (int64_t)b * p.dbstride + (int64_t)(y - p.out_y0) * p.dpitch)[x] = acc;
+  }
+}
+
+}  // namespace
+}  // namespace icl
+
+using namespace icl;
+
+extern "C" {
+
+icl_status icl_ipc_get_handle(const void* dev_ptr, void* handle, uint64_t* offset) {
+  if (!dev_ptr || !handle || !offset) return report_error(ICL_ERR_INVALID_ARG, "null argument");
+  // the handle names the whole allocation; the pointer's offset inside it travels beside it
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+    return report_error(ICL_ERR_CUDA, "cuMemGetAddressRange not available");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  auto range = reinterpret_cast<CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr)>(fn);
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return report_error(ICL_ERR_INVALID_ARG, "not a device allocation");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return report_error(ICL_ERR_CUDA, cudaGetErrorString(e));
+  memcpy(handle, &h, sizeof h);
+  *offset = reinterpret_cast<uintptr_t>(dev_ptr) - (uintptr_t)base;
+  return ICL_OK;
+}
+
+icl_status icl_ipc_open(const void* handle, uint64_t offset, void** dev_ptr) {
+  if (!handle || !dev_ptr) return report_error(ICL_ERR_INVALID_ARG, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  void* p = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return report_error(ICL_ERR_CUDA, cudaGetErrorString(e));
+  *dev_ptr = static_cast<char*>(p) + offset;
+  return ICL_OK;
+}
+
+icl_status icl_ipc_close(void* dev_ptr, uint64_t offset) {
+  if (!dev_ptr) return ICL_OK;
+  cudaError_t e = cudaIpcCloseMemHandle(static_cast<char*>(dev_ptr) - offset);
+  return e == cudaSuccess ? ICL_OK : report_error(ICL_ERR_CUDA, cudaGetErrorString(e));
+}
+
+icl_status icl_sepconv_peer(const icl_image* own, const icl_image* dst, int64_t global_height, int64_t own_y0,
+                            const icl_image* up, const icl_image* down, const float* taps_x, int rx,
+                            const float* taps_y, int ry, icl_border border, float border_value, void* stream) {
+  if (!own || !dst || !taps_x || !taps_y) return report_error(ICL_ERR_INVALID_ARG, "null argument");
+  if (rx < 0 || ry < 0 || rx > kMaxRadius || ry > kMaxRadius)
+    return report_error(ICL_ERR_INVALID_ARG, "radius outside [0, 15]");
+  const int64_t H = global_height, y0 = own_y0, y1 = own_y0 + own->height;
+  if (H < 1 || H >= (1ll << 31) || y0 < 0 || y1 > H || dst->height != own->height || dst->width != own->width ||
+      dst->batch != own->batch || own->width < 1 || own->height < 1 || own->batch < 1 || own->batch > 65535)
+    return report_error(ICL_ERR_INVALID_ARG, "bad band geometry");
+  // the neighbours must provide the rows the edges need (ry rows, or up to the image edge)
+  const int64_t need_up = std::min<int64_t>(ry, y0), need_dn = std::min<int64_t>(ry, H - y1);
+  auto check_nb = [&](const icl_image* nb, int64_t need, const char* which) -> icl_status {
+    if (need == 0) return ICL_OK;
+    if (!nb || !nb->data || nb->height < need || nb->width != own->width || nb->batch != own->batch)
+      return report_error(ICL_ERR_INVALID_ARG, which);
+    return ICL_OK;
+  };
+  icl_status st;
+  if ((st = check_nb(up, need_up, "up neighbour band missing or thinner than the halo"))) return st;
+  if ((st = check_nb(down, need_dn, "down neighbour band missing or thinner than the halo"))) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // rows needing no halo: the ordinary kernels on the own band
+  const int64_t i0 = y0 + (y0 > 0 ? ry : 0), i1 = y1 - (y1 < H ? ry : 0);
+  if (i1 > i0) {
+    icl_image dv = *dst;
+    dv.data = static_cast<char*>(dst->data) + (i0 - y0) * dst->pitch_bytes;
+    dv.height = i1 - i0;
+    const icl_band bi{H, y0, i0};
+    if ((st = icl_sepconv(own, &dv, taps_x, rx, taps_y, ry, border, border_value, &bi, nullptr, 0, s))) return st;
+  }
+  // edge rows: input rows from the own band and the neighbours' bands (peer loads)
+  EdgeParams p;
+  memset(&p, 0, sizeof p);
+  auto seg = [](const icl_image* im, int64_t gy0) {
+    RowSeg g;
+    g.base = static_cast<const char*>(im->data);
+    g.pitch = im->pitch_bytes;
+    g.bstride = im->batch > 1 ? im->batch_stride_bytes : 0;
+    g.y0 = (int)gy0;
+    g.y1 = (int)(gy0 + im->height);
+    return g;
+  };
+  p.seg[1] = seg(own, y0);
+  if (need_up) {  // the up neighbour's LAST rows end at y0
+    p.seg[0] = seg(up, y0 - up->height);
+  }
+  if (need_dn) p.seg[2] = seg(down, y1);
+  p.W = (int)own->width;
+  p.Hg = (int)H;
+  p.border = border == ICL_BORDER_CLAMP ? kBorderClamp : kBorderConstant;
+  p.cval = border_value;
+  p.rx = rx;
+  p.ry = ry;
+  for (int i = 0; i <= 2 * rx; ++i) p.fx[i] = taps_x[i];
+  for (int j = 0; j <= 2 * ry; ++j) p.gy[j] = taps_y[j];
+  p.dpitch = dst->pitch_bytes;
+  p.dbstride = dst->batch > 1 ? dst->batch_stride_bytes : 0;
+  const size_t smem = (size_t)(kEdgeTW + 4 * kMaxRadius + (kEdgeCH + 2 * ry) * kEdgeTW) * sizeof(float);
+  auto edge = [&](int64_t a0, int64_t a1) -> icl_status {
+    if (a1 <= a0) return ICL_OK;
+    p.dst = static_cast<char*>(dst->data) + (a0 - y0) * dst->pitch_bytes;
+    p.out_y0 = (int)a0;
+    p.out_y1 = (int)a1;
+    dim3 grd((unsigned)((own->width + kEdgeTW - 1) / kEdgeTW), (unsigned)((a1 - a0 + kEdgeCH - 1) / kEdgeCH),
+             (unsigned)own->batch);
+    cudaFuncSetAttribute(sep_edge_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sep_edge_peer<<<grd, kEdgeTW, smem, s>>>(p);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? ICL_OK : report_error(ICL_ERR_CUDA, cudaGetErrorString(e));
+  };
+  if (i1 <= i0) return edge(y0, y1);  // thin band: every row is an edge row
+  if ((st = edge(y0, i0))) return st;
+  return edge(i1, y1);
+}
+
+}  // extern "C"

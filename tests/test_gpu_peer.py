@@ -1,0 +1,101 @@
+"""Row-band sepconv with the halo rows read in the kernel from the other ranks'
+memory (icl_sepconv_peer over CUDA IPC).
+
+Two or three processes share the one GPU of the test box (CUDA IPC works
+between processes of one device exactly as between the GPUs of a node; on an
+NVLink node the same loads go over NVLink).  Each rank holds ONLY its own
+rows; the handles travel over a gloo group.  The stitched bands must equal
+the unsharded icl_sepconv bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, n, port, H, W, B, rx, ry, border, cval):
+    import paper_1605_06399_b200 as icl
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=n)
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    full = np.stack([synth.uniform_image(50 + i, H, W) for i in range(B)])
+    rows = -(-H // n)
+    r0, r1 = rank * rows, min(H, (rank + 1) * rows)
+    pitch = W + 3 + (rank % 2) * 8  # ranks use different pitches
+    buf = torch.full((B, r1 - r0, pitch), float("nan"), device=dev)
+    own = buf[..., :W]
+    own.copy_(torch.from_numpy(full[:, r0:r1]))
+    out = torch.full((B, r1 - r0, W), float("nan"), device=dev)
+    torch.cuda.synchronize()
+    h, off = icl.ipc_handle(buf)
+    meta = [None] * n
+    dist.all_gather_object(meta, (h, off, r1 - r0, pitch))
+    up = down = None
+    if rank > 0:
+        hh, oo, hgt, pp = meta[rank - 1]
+        up = icl.PeerImage(hh, oo, W, hgt, pp, B, hgt * pp)
+    if rank < n - 1:
+        hh, oo, hgt, pp = meta[rank + 1]
+        down = icl.PeerImage(hh, oo, W, hgt, pp, B, hgt * pp)
+    dist.barrier()  # every band written
+    fx, gy = synth.gaussian_taps(rx), synth.signed_taps(3, ry)
+    icl.sepconv_peer(own, out, H, r0, up, down, fx, gy, border, cval)
+    torch.cuda.synchronize()
+    dist.barrier()  # every peer read done before anyone frees its band
+    parts = [None] * n
+    dist.all_gather_object(parts, out.cpu().numpy())
+    if rank == 0:
+        src = torch.from_numpy(full).to(dev)
+        ref = torch.empty_like(src)
+        icl.sepconv(src, ref, fx, gy, border, cval)
+        got = np.concatenate(parts, axis=1)
+        np.testing.assert_array_equal(got, ref.cpu().numpy())
+    for p in (up, down):
+        if p:
+            p.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,H,W,B,rx,ry,border,cval", [
+    (2, 200, 389, 1, 2, 2, "constant", 0.0),
+    (3, 300, 389, 2, 15, 15, "clamp", 0.0),
+    (3, 97, 130, 1, 1, 3, "constant", 0.5),
+    (2, 33, 1029, 1, 7, 15, "clamp", 0.0),
+])
+def test_sepconv_peer_bands_equal_unsharded(n, H, W, B, rx, ry, border, cval):
+    mp.spawn(_worker, args=(n, _free_port(), H, W, B, rx, ry, border, cval), nprocs=n, join=True)
+
+
+def test_sepconv_peer_single_rank_and_errors():
+    import paper_1605_06399_b200 as icl
+    dev = torch.device("cuda:0")
+    img = torch.from_numpy(synth.uniform_image(60, 64, 100)).to(dev)
+    out, ref = torch.empty_like(img), torch.empty_like(img)
+    f = synth.gaussian_taps(2)
+    icl.sepconv_peer(img, out, 64, 0, None, None, f, f, "constant")  # one rank: no neighbours needed
+    icl.sepconv(img, ref, f, f, "constant")
+    assert torch.equal(out, ref)
+    with pytest.raises(icl.IclError):  # rows above exist but no up neighbour given
+        icl.sepconv_peer(img[32:], out[32:], 64, 32, None, None, f, f, "constant")
+    h, off = icl.ipc_handle(img[10:])
+    assert len(h) == 64 and off >= 10 * 100 * 4
