@@ -19,7 +19,7 @@
 #include "harris_stream.cuh"
 
 #ifndef ICL_HSHFL_MINB
-#define ICL_HSHFL_MINB 1
+#define ICL_HSHFL_MINB (16 / NW)
 #endif
 
 namespace icl {
@@ -256,7 +256,11 @@ __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, f
 // input rows of a step are base + (u + rr) with compile-time offsets; the
 // loader walks a row pointer by the pitch; every emitting lane stores a full
 // float4.  Bit-identical to the general path.
-template <int B, int NW>
+// EDGE: the strip touches the left / right image edge (its rows are still inside the image): the
+// loader zero-fills columns outside [0, W), fix_block applies the input boundary there (mirror rows
+// included), dx/dy outside [0, W) take the per-stage boundary, and stores are guarded -- the
+// general path's column logic without its row logic.
+template <int B, int NW, bool EDGE>
 __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int S, float* smem) {
   constexpr int A = B / 2;
   constexpr int BB = B - 1 - A;
@@ -279,7 +283,11 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
   const int NBL = (NL + RB - 1) / RB;
   const int64_t spitch = p.src.pitch >> 2;
   const bool loader = tid < NSLOT;
-  const float* gsrc = src_row(p.src, b, g0 - A - 1) + (x0 - HP + 4 * tid);
+  const int W = p.src.W;
+  const int xs = x0 - HP + 4 * tid;  // first column of this loader slot
+  // EDGE: bytes of the slot inside [0, W) (zero-filled beyond), from an in-row address
+  const int nb = !EDGE ? 16 : (xs < 0 ? 0 : min(max(W - xs, 0), 4) * 4);
+  const float* gsrc = src_row(p.src, b, g0 - A - 1) + (EDGE && nb == 0 ? 0 : xs);
   float* sdst = smem + 4 * tid;
 
   auto load_block = [&](int m) {
@@ -289,10 +297,30 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
 #pragma unroll
     for (int u = 0; u < RB; ++u) {
       if (m * RB + u < NL) {
-        cp_async16(sdst + (r0 + u) * ROWLEN, g, 16);
-        if (u < 2 && r0 == 0) cp_async16(sdst + (NSR + u) * ROWLEN, g, 16);  // mirror
+        cp_async16(sdst + (r0 + u) * ROWLEN, g, nb);
+        if (u < 2 && r0 == 0) cp_async16(sdst + (NSR + u) * ROWLEN, g, nb);  // mirror
       }
       g += spitch;
+    }
+  };
+  // EDGE: input boundary of the halo columns outside [0, W) of load block m (and of its mirror rows)
+  const bool clampb = p.src.border == kBorderClamp;
+  auto fix_block = [&](int m) {
+    for (int u = 0; u < RB; ++u) {
+      const int kl = m * RB + u;
+      if (kl >= NL) break;
+      const int rr = kl % NSR;
+      for (int mirror = 0; mirror < (rr < 2 ? 2 : 1); ++mirror) {
+        float* st = smem + (mirror ? NSR + rr : rr) * ROWLEN;
+        const int il = HP - x0, ir = (W - 1) - x0 + HP;
+        const float vl = (il >= 0 && il < ROWLEN) ? st[il] : 0.0f;
+        const float vr = (ir >= 0 && ir < ROWLEN) ? st[ir] : 0.0f;
+        for (int c = tid; c < ROWLEN; c += NT) {
+          const int xe = x0 - HP + c;
+          if (xe < 0) st[c] = clampb ? vl : p.src.cval;
+          else if (xe >= W) st[c] = clampb ? vr : p.src.cval;
+        }
+      }
     }
   };
   for (int m = 0; m < NBLKS - 1; ++m) {
@@ -302,7 +330,12 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
 
   const int xl = x0 + 120 * warp + 4 * (lane - 1);
   const float* stb = smem + (xl - (x0 - HP));
-  const bool emit = lane >= 1 && lane <= 30;
+  const bool emit = lane >= 1 && lane <= 30 && (!EDGE || xl < W);
+  const bool warp_live = !EDGE || x0 + 120 * warp - 4 < W;  // (see harris_shfl_fast)
+  // lanes of this warp owning image columns 0 and W-1 (for the dx/dy boundary)
+  const int xw = x0 + 120 * warp - 4;
+  const int ll = (0 - xw) >> 2, el = (0 - xw) & 3;
+  const int lr = (W - 1 - xw) >> 2, er = (W - 1 - xw) & 3;
   // running vertical window sums instead of a ring of B H-rows: when H-row n arrives, the
   // oldest chain completes output n-B+1 (c[0] + h), the others take h as their next term and
   // h starts a new chain -- every output is summed oldest row first, the ring's order
@@ -325,8 +358,14 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
   for (int i = 0; i < NBI; ++i) {
     cp_async_wait<NBLKS - 3>();
     __syncthreads();
+    if (EDGE) {  // rows of load blocks i (first time only) and i+1 become visible now
+      if (i == 0) fix_block(0);
+      if (i + 1 < NBL) fix_block(i + 1);
+      __syncthreads();
+    }
     if (i + NBLKS - 1 < NBL) load_block(i + NBLKS - 1);
     cp_async_commit();
+    if (!warp_live) continue;
     const float* sb = stb + (i % NBLKS) * RB * ROWLEN;
 #pragma unroll 1
     for (int u = 0; u < RB; ++u) {
@@ -361,6 +400,22 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
         for (int c = 0; c < 4; ++c) {
           g[c + 2].x = __fmaf_rn(2.0f, hd[1][c], __fadd_rn(hd[0][c], hd[2][c]));
           g[c + 2].y = __fmaf_rn(2.0f, vd[c + 1], __fadd_rn(vd[c], vd[c + 2]));
+        }
+        if (EDGE) {  // per-stage boundary of dx/dy: outside [0, W) -> dx(clamp(q)) or 0
+          const float2 e0 = el == 0 ? g[2] : el == 1 ? g[3] : el == 2 ? g[4] : g[5];
+          const float2 e1 = er == 0 ? g[2] : er == 1 ? g[3] : er == 2 ? g[4] : g[5];
+          float2 gl, gr;
+          gl.x = __shfl_sync(0xffffffffu, e0.x, ll & 31);
+          gl.y = __shfl_sync(0xffffffffu, e0.y, ll & 31);
+          gr.x = __shfl_sync(0xffffffffu, e1.x, lr & 31);
+          gr.y = __shfl_sync(0xffffffffu, e1.y, lr & 31);
+          if (!clampb) gl = gr = make_float2(0.0f, 0.0f);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int xe = xl + c;
+            if (xe < 0) g[c + 2] = gl;
+            else if (xe >= W) g[c + 2] = gr;
+          }
         }
         g[0].x = __shfl_up_sync(0xffffffffu, g[4].x, 1);
         g[0].y = __shfl_up_sync(0xffffffffu, g[4].y, 1);
@@ -416,10 +471,19 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
           R[2] = harris_R(s2o[2].x, sxyo[1].x, s2o[2].y, p.k);
           R[3] = harris_R(s2o[3].x, sxyo[1].y, s2o[3].y, p.k);
           if (emit) {
-            st_cs4(drow, make_float4(R[0], R[1], R[2], R[3]));
-            if (has_mask)
-              *reinterpret_cast<uchar4*>(mrow) =
-                  make_uchar4(R[0] > p.threshold, R[1] > p.threshold, R[2] > p.threshold, R[3] > p.threshold);
+            if (!EDGE || xl + 3 < W) {
+              st_cs4(drow, make_float4(R[0], R[1], R[2], R[3]));
+              if (has_mask)
+                *reinterpret_cast<uchar4*>(mrow) =
+                    make_uchar4(R[0] > p.threshold, R[1] > p.threshold, R[2] > p.threshold, R[3] > p.threshold);
+            } else {
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (xl + q < W) {
+                  drow[q] = R[q];
+                  if (has_mask) mrow[q] = R[q] > p.threshold ? 1 : 0;
+                }
+            }
           }
           drow += dpitch;
           mrow += has_mask ? p.mpitch : 0;
@@ -440,7 +504,10 @@ __global__ void __launch_bounds__(32 * NW, ICL_HSHFL_MINB) harris_shfl(HarrisPar
   // every input row (g0-A-1 .. last output row + BB + 1) and column inside the image
   const bool interior = x0 - HP >= 0 && x0 + TW + HP <= p.src.W && g0 - A - 1 >= 0 &&
                         p.dst.y0 + ly1 + BB + 1 <= p.src.Hg;
-  if (interior) harris_shfl_interior<B, NW>(p, S, smem);
+  // rows inside the image: the interior path (with the column boundary logic on the edge strips)
+  const bool rows_in = g0 - A - 1 >= 0 && p.dst.y0 + ly1 + BB + 1 <= p.src.Hg;
+  if (interior) harris_shfl_interior<B, NW, false>(p, S, smem);
+  else if (rows_in) harris_shfl_interior<B, NW, true>(p, S, smem);
   else harris_shfl_fast<B, NW>(p, S, smem);
 }
 
