@@ -32,7 +32,8 @@ EXPORTS = ("icl_sepconv", "icl_sepconv_workspace_bytes", "icl_harris", "icl_nlm"
            "icl_halo_rows", "icl_shard_band", "icl_shard_plan", "icl_comm_unique_id", "icl_comm_init",
            "icl_comm_destroy", "icl_sepconv_sharded", "icl_harris_sharded", "icl_nlm_sharded", "icl_conv2d_u8_sharded",
            "icl_tune_ann", "icl_ann_search", "icl_ann_fit", "icl_blur_harris", "icl_blur_harris_workspace_bytes",
-           "icl_ipc_get_handle", "icl_ipc_open", "icl_ipc_close", "icl_sepconv_peer")
+           "icl_ipc_get_handle", "icl_ipc_open", "icl_ipc_close", "icl_sepconv_peer",
+           "icl_halo_pull")
 
 # int evaluate(void* ctx, int index, double* value) -- icl_ann_search's callback
 EVAL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double))
@@ -119,6 +120,7 @@ def load_library(path: str = LIB_PATH):
         "icl_ipc_open": ([P, ctypes.c_uint64, ctypes.POINTER(P)], I),
         "icl_ipc_close": ([P, ctypes.c_uint64], I),
         "icl_sepconv_peer": ([img, img, I64, I64, img, img, P, I, P, I, I, F, P], I),
+        "icl_halo_pull": ([img, I64, I64, I64, I64, img, img, I, P], I),
         "icl_tune_ann": ([ctypes.POINTER(icl_problem), I, I, ctypes.c_uint64, P, ctypes.POINTER(icl_variant_info)], I),
         "icl_ann_search": ([ctypes.POINTER(ctypes.c_double), I, I, EVAL_FN, P, I, I, ctypes.c_uint64,
                             ctypes.POINTER(I), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I), ctypes.POINTER(I)], I),
@@ -488,6 +490,16 @@ def sepconv_peer(own, dst, global_height: int, own_y0: int, up: Optional[PeerIma
                                 ctypes.cast(fx, ctypes.c_void_p), len(fx) // 2, ctypes.cast(gy, ctypes.c_void_p),
                                 len(gy) // 2, BORDER[border], border_value, _stream(stream)))
     return dst
+
+
+def halo_pull(buf, global_height: int, buf_y0: int, own_y0: int, own_y1: int, up: Optional[PeerImage],
+              down: Optional[PeerImage], stream=None):
+    """Fill buf's halo rows from the neighbours' owned rows (peer loads; icl_halo_pull)."""
+    elem = buf.element_size()
+    _check(load_library().icl_halo_pull(ctypes.byref(_image(buf, elem)), global_height, buf_y0, own_y0, own_y1,
+                                        ctypes.byref(up.image) if up else None,
+                                        ctypes.byref(down.image) if down else None, elem, _stream(stream)))
+    return buf
 
 
 def tune_cache_save(path: str):

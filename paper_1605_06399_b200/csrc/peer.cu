@@ -110,6 +110,27 @@ __global__ void __launch_bounds__(kEdgeTW) sep_edge_peer(EdgeParams p) {
   }
 }
 
+// Copy rows of a neighbour's band (peer memory) into this rank's halo rows:
+// one thread per 16-byte (or 4-byte) chunk, rows x chunks x images.
+struct PullParams {
+  const char* src;  // first source row, image 0
+  int64_t spitch, sbstride;
+  char* dst;        // first destination row, image 0
+  int64_t dpitch, dbstride;
+  int rows, chunks;  // chunks per row
+  int vec16;
+};
+
+__global__ void __launch_bounds__(256) halo_pull(PullParams p) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y, b = blockIdx.z;
+  if (c >= p.chunks || r >= p.rows) return;
+  const char* s = p.src + (int64_t)b * p.sbstride + (int64_t)r * p.spitch;
+  char* d = p.dst + (int64_t)b * p.dbstride + (int64_t)r * p.dpitch;
+  if (p.vec16) reinterpret_cast<float4*>(d)[c] = __ldcv(reinterpret_cast<const float4*>(s) + c);
+  else reinterpret_cast<float*>(d)[c] = __ldcv(reinterpret_cast<const float*>(s) + c);
+}
+
 }  // namespace
 }  // namespace icl
 
@@ -229,6 +250,44 @@ icl_status icl_sepconv_peer(const icl_image* own, const icl_image* dst, int64_t 
   if (i1 <= i0) return edge(y0, y1);  // thin band: every row is an edge row
   if ((st = edge(y0, i0))) return st;
   return edge(i1, y1);
+}
+
+icl_status icl_halo_pull(const icl_image* buf, int64_t global_height, int64_t buf_y0, int64_t own_y0,
+                         int64_t own_y1, const icl_image* up, const icl_image* down, int elem_bytes, void* stream) {
+  if (!buf || !buf->data || (elem_bytes != 1 && elem_bytes != 4)) return report_error(ICL_ERR_INVALID_ARG, "bad buffer");
+  const int64_t H = global_height, s0 = buf_y0, s1 = buf_y0 + buf->height;
+  if (H < 1 || s0 < 0 || s1 > H || own_y0 < s0 || own_y1 > s1 || own_y0 > own_y1 || buf->batch < 1 ||
+      buf->batch > 65535)
+    return report_error(ICL_ERR_INVALID_ARG, "bad band geometry");
+  const int64_t rowb = buf->width * elem_bytes;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto pull = [&](const icl_image* nb, int64_t nb_y0, int64_t g0, int64_t g1) -> icl_status {
+    if (g1 <= g0) return ICL_OK;
+    if (!nb || !nb->data || nb->width != buf->width || nb->batch != buf->batch || g0 < nb_y0 ||
+        g1 > nb_y0 + nb->height)
+      return report_error(ICL_ERR_INVALID_ARG, "neighbour band does not hold the halo rows");
+    PullParams p;
+    p.src = static_cast<const char*>(nb->data) + (g0 - nb_y0) * nb->pitch_bytes;
+    p.spitch = nb->pitch_bytes;
+    p.sbstride = nb->batch > 1 ? nb->batch_stride_bytes : 0;
+    p.dst = static_cast<char*>(buf->data) + (g0 - s0) * buf->pitch_bytes;
+    p.dpitch = buf->pitch_bytes;
+    p.dbstride = buf->batch > 1 ? buf->batch_stride_bytes : 0;
+    p.rows = (int)(g1 - g0);
+    const uintptr_t al = reinterpret_cast<uintptr_t>(p.src) | reinterpret_cast<uintptr_t>(p.dst) |
+                         (uintptr_t)p.spitch | (uintptr_t)p.dpitch | (uintptr_t)p.sbstride | (uintptr_t)p.dbstride;
+    p.vec16 = (al % 16 == 0) && rowb % 16 == 0;
+    if (!p.vec16 && (al % 4 != 0 || rowb % 4 != 0)) return report_error(ICL_ERR_UNSUPPORTED, "rows not 4-byte aligned");
+    p.chunks = (int)(rowb / (p.vec16 ? 16 : 4));
+    dim3 grd((unsigned)((p.chunks + 255) / 256), (unsigned)p.rows, (unsigned)buf->batch);
+    halo_pull<<<grd, 256, 0, s>>>(p);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? ICL_OK : report_error(ICL_ERR_CUDA, cudaGetErrorString(e));
+  };
+  icl_status st = pull(up, own_y0 - (up ? up->height : 0), s0, own_y0);
+  if (st != ICL_OK) return st;
+  return pull(down, own_y1, own_y1, s1);
 }
 
 }  // extern "C"

@@ -86,6 +86,59 @@ def test_sepconv_peer_bands_equal_unsharded(n, H, W, B, rx, ry, border, cval):
     mp.spawn(_worker, args=(n, _free_port(), H, W, B, rx, ry, border, cval), nprocs=n, join=True)
 
 
+def _pull_worker(rank, n, port, H, W, filt):
+    """Halo rows pulled from the neighbours' owned rows (icl_halo_pull), then the ordinary band call."""
+    import paper_1605_06399_b200 as icl
+    from paper_1605_06399_b200 import dist as icd
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=n)
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    full = synth.rect_scene(70, H, W)
+    up_rows, down_rows = icl.harris_halo(5) if filt == "harris" else icl.nlm_halo(2, 5)
+    band = icd.partition(H, n, rank, up_rows, down_rows)
+    buf = torch.full((band.buf_rows, W), float("nan"), device=dev)
+    buf[band.own_slice] = torch.from_numpy(full[band.r0:band.r1]).to(dev)
+    torch.cuda.synchronize()
+    meta = [None] * n
+    dist.all_gather_object(meta, icl.ipc_handle(buf) + (band.r0 - band.s0, band.rows))
+    nb = {}
+    for q in (rank - 1, rank + 1):
+        if 0 <= q < n:
+            h, off, skip, rows = meta[q]
+            nb[q] = icl.PeerImage(h, off + skip * W * 4, W, rows, W)
+    dist.barrier()
+    icl.halo_pull(buf, H, band.s0, band.r0, band.r1, nb.get(rank - 1), nb.get(rank + 1))
+    out = torch.empty(band.rows, W, device=dev)
+    if filt == "harris":
+        icl.harris(buf, out, 5, 0.04, "clamp", band=band.icl_band())
+    else:
+        icl.nlm(buf, out, 2, 5, 0.1, "clamp", band=band.icl_band())
+    torch.cuda.synchronize()
+    dist.barrier()
+    parts = [None] * n
+    dist.all_gather_object(parts, out.cpu().numpy())
+    if rank == 0:
+        src = torch.from_numpy(full).to(dev)
+        ref = torch.empty_like(src)
+        if filt == "harris":
+            icl.harris(src, ref, 5, 0.04, "clamp")
+            np.testing.assert_array_equal(np.concatenate(parts), ref.cpu().numpy())
+        else:  # box-sum tiles restart at band edges: equal to rounding
+            icl.nlm(src, ref, 2, 5, 0.1, "clamp")
+            np.testing.assert_allclose(np.concatenate(parts), ref.cpu().numpy(), rtol=0, atol=2e-6)
+    for p in nb.values():
+        p.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,filt", [(2, "harris"), (3, "harris"), (3, "nlm")])
+def test_halo_pull_bands_equal_unsharded(n, filt):
+    mp.spawn(_pull_worker, args=(n, _free_port(), 150, 203, filt), nprocs=n, join=True)
+
+
 def test_sepconv_peer_single_rank_and_errors():
     import paper_1605_06399_b200 as icl
     dev = torch.device("cuda:0")
