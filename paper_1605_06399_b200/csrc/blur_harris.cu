@@ -24,6 +24,17 @@
 
 namespace icl {
 
+// Ring of blurred rows: RB rows per block as harris_shfl (a multiple of B, so the general
+// path's window slots are static), but only 3 blocks -- the producer writes block i+2 while
+// the consumer reads block i and the first rows of block i+1, and rows are produced by the
+// CTA itself (no load latency to hide), so a deeper ring would only cost occupancy.
+template <int B>
+struct ChainGeom {
+  static constexpr int RB = HarFastGeom<B>::RB;
+  static constexpr int NBLKS = 3;
+  static constexpr int NSR = RB * NBLKS;
+};
+
 struct BlurHarrisParams {
   HarrisParams h;  // h.src: the source image with the HARRIS boundary (applied to the blurred image)
   SrcView raw;     // the same image with the SEPCONV boundary
@@ -32,8 +43,7 @@ struct BlurHarrisParams {
 };
 
 template <int R, int B, int NW>
-__global__ void __launch_bounds__(32 * NW) blur_harris_kernel(BlurHarrisParams bp, int S) {
-  extern __shared__ __align__(16) float smem[];
+__device__ __forceinline__ void blur_harris_general(const BlurHarrisParams& bp, int S, float* smem) {
   const HarrisParams& p = bp.h;
   constexpr int A = B / 2;
   constexpr int BB = B - 1 - A;
@@ -42,7 +52,7 @@ __global__ void __launch_bounds__(32 * NW) blur_harris_kernel(BlurHarrisParams b
   constexpr int TW = 120 * NW;
   constexpr int ROWLEN = TW + 2 * HP;
   constexpr int NSLOT = ROWLEN / 4;
-  constexpr int RB = HarFastGeom<B>::RB, NBLKS = HarFastGeom<B>::NBLKS, NSR = HarFastGeom<B>::NSR;
+  constexpr int RB = ChainGeom<B>::RB, NBLKS = ChainGeom<B>::NBLKS, NSR = ChainGeom<B>::NSR;
   constexpr int K = 2 * R + 1;
   static_assert(NSLOT <= NT, "one producer slot per thread");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -322,12 +332,247 @@ __global__ void __launch_bounds__(32 * NW) blur_harris_kernel(BlurHarrisParams b
   }
 }
 
+// Interior CTAs (every raw row and column the chain touches inside the image): the
+// harris_shfl_interior consumer (mirror ring rows, compile-time offsets, running
+// vertical sums) fed by the blur producer.  The producer keeps its row-pass rows t
+// in a per-slot shared-memory ring (K rows x 4 columns per thread) instead of
+// registers, so the consumer keeps its register budget.  Same values as the
+// general path (bit-identical).
+template <int R, int B, int NW>
+__device__ __forceinline__ void blur_harris_interior(const BlurHarrisParams& bp, int S, float* smem) {
+  const HarrisParams& p = bp.h;
+  constexpr int A = B / 2;
+  constexpr int BB = B - 1 - A;
+  constexpr int HP = 8;
+  constexpr int TW = 120 * NW;
+  constexpr int ROWLEN = TW + 2 * HP;
+  constexpr int NSLOT = ROWLEN / 4;
+  constexpr int RB = ChainGeom<B>::RB, NBLKS = ChainGeom<B>::NBLKS, NSR = ChainGeom<B>::NSR;
+  constexpr int K = 2 * R + 1;
+  constexpr int RAWLEN = ROWLEN + 8;
+  constexpr int NRAW = 2 * RB + 2 * R + 1;
+  static_assert(RB >= 2, "mirror rows cover the two rows a step reads past its block");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * TW;
+  const int ly0 = blockIdx.y * S;
+  const int ly1 = min(ly0 + S, p.dst.H);
+  const int g0 = p.dst.y0 + ly0;
+  const int NY = (ly1 - ly0) + B - 1;
+  const int NL = NY + 2;
+  const int NBI = (NY + RB - 1) / RB;
+  const int NBL = (NL + RB - 1) / RB;
+  float* raw = smem + (NSR + 2) * ROWLEN;
+  float* tring = raw + NRAW * RAWLEN;  // [K][NSLOT][4]
+  const int xr0 = x0 - HP - 4;
+  const int64_t spitch = bp.raw.pitch >> 2;
+  const float* rbase = src_row(bp.raw, b, 0) + xr0;  // raw row 0, ring column 0
+
+  // raw rows: cp.async, one ring block ahead of the producer
+  int rl = g0 - A - 1 - R;  // next raw row to load
+  auto load_for_block = [&](int m) {
+    const int hi = g0 - A - 1 + min(m * RB + RB - 1, NL - 1) + R;
+    for (; rl <= hi; ++rl) {
+      float* st = raw + (rl % NRAW) * RAWLEN;
+      const float* g = rbase + (int64_t)rl * spitch;
+      for (int c = tid; c < RAWLEN / 4; c += 32 * NW) cp_async16(st + 4 * c, g + 4 * c, 16);
+    }
+    cp_async_commit();
+  };
+  int tn = g0 - A - 1 - R;  // next raw row whose row pass goes into the t ring
+  auto produce_block = [&](int m) {
+    if (tid >= NSLOT) return;
+#pragma unroll 1
+    for (int u = 0; u < RB; ++u) {
+      const int kl = m * RB + u;
+      if (kl >= NL) break;
+      const int gi = g0 - A - 1 + kl;
+      for (; tn <= gi + R; ++tn) {  // row pass of the raw rows the window gains
+        const float4* rr = reinterpret_cast<const float4*>(raw + (tn % NRAW) * RAWLEN + 4 * tid);
+        const float4 w0 = rr[0], w1 = rr[1], w2 = rr[2];
+        const float v12[12] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w, w2.x, w2.y, w2.z, w2.w};
+        float o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float a = 0.0f;
+#pragma unroll
+          for (int i = 0; i < K; ++i) a = __fmaf_rn(bp.fx[i], v12[4 - R + q + i], a);
+          o[q] = a;
+        }
+        *reinterpret_cast<float4*>(tring + ((tn % K) * NSLOT + tid) * 4) = make_float4(o[0], o[1], o[2], o[3]);
+      }
+      float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const float4 tv = *reinterpret_cast<const float4*>(tring + (((gi - R + j) % K) * NSLOT + tid) * 4);
+        acc.x = __fmaf_rn(bp.gy[j], tv.x, acc.x);
+        acc.y = __fmaf_rn(bp.gy[j], tv.y, acc.y);
+        acc.z = __fmaf_rn(bp.gy[j], tv.z, acc.z);
+        acc.w = __fmaf_rn(bp.gy[j], tv.w, acc.w);
+      }
+      const int rr = kl % NSR;
+      *reinterpret_cast<float4*>(smem + rr * ROWLEN + 4 * tid) = acc;
+      if (rr < 2) *reinterpret_cast<float4*>(smem + (NSR + rr) * ROWLEN + 4 * tid) = acc;  // mirror
+    }
+  };
+  load_for_block(0);
+  for (int m = 0; m < NBLKS - 1; ++m) {
+    if (m + 1 < NBL) load_for_block(m + 1);
+    else cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (m < NBL) produce_block(m);
+    __syncthreads();
+  }
+  if (NBLKS - 1 < NBL) load_for_block(NBLKS - 1);
+  else cp_async_commit();
+
+  const int xl = x0 + 120 * warp + 4 * (lane - 1);
+  const float* stb = smem + (xl - (x0 - HP));
+  const bool emit = lane >= 1 && lane <= 30;
+  constexpr int NC = B > 1 ? B - 1 : 1;
+  float2 c2[NC][4];
+  float2 cxy[NC][2];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c2[k][q] = make_float2(0.0f, 0.0f);
+    cxy[k][0] = cxy[k][1] = make_float2(0.0f, 0.0f);
+  }
+  float* drow = dst_row(p.dst, b, ly0) + xl;
+  const int64_t dpitch = p.dst.pitch >> 2;
+  const bool has_mask = p.mask != nullptr;
+  char* mrow = has_mask ? p.mask + (int64_t)b * p.mbstride + (int64_t)ly0 * p.mpitch + xl : nullptr;
+
+#pragma unroll 1
+  for (int i = 0; i < NBI; ++i) {
+    cp_async_wait<0>();
+    __syncthreads();
+    if (i + NBLKS - 1 < NBL) produce_block(i + NBLKS - 1);
+    if (i + NBLKS < NBL) load_for_block(i + NBLKS);
+    const float* sb = stb + (i % NBLKS) * RB * ROWLEN;
+#pragma unroll 1
+    for (int u = 0; u < RB; ++u) {
+      const int step = i * RB + u;
+      if (step < NY) {
+        float4 w[3];
+        float il[3], ir[3];
+        float hd[3][4];
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr) {
+          w[rr] = *reinterpret_cast<const float4*>(sb + (u + rr) * ROWLEN);
+          il[rr] = __shfl_up_sync(0xffffffffu, w[rr].w, 1);
+          ir[rr] = __shfl_down_sync(0xffffffffu, w[rr].x, 1);
+          const float2 m = __fadd2_rn(make_float2(w[rr].z, w[rr].w), make_float2(-w[rr].x, -w[rr].y));
+          hd[rr][0] = __fsub_rn(w[rr].y, il[rr]);
+          hd[rr][1] = m.x;
+          hd[rr][2] = m.y;
+          hd[rr][3] = __fsub_rn(ir[rr], w[rr].z);
+        }
+        float vd[6];
+        {
+          const float2 v12 = __fadd2_rn(make_float2(w[2].x, w[2].y), make_float2(-w[0].x, -w[0].y));
+          const float2 v34 = __fadd2_rn(make_float2(w[2].z, w[2].w), make_float2(-w[0].z, -w[0].w));
+          vd[0] = __fsub_rn(il[2], il[0]);
+          vd[1] = v12.x; vd[2] = v12.y; vd[3] = v34.x; vd[4] = v34.y;
+          vd[5] = __fsub_rn(ir[2], ir[0]);
+        }
+        float2 g[8];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          g[c + 2].x = __fmaf_rn(2.0f, hd[1][c], __fadd_rn(hd[0][c], hd[2][c]));
+          g[c + 2].y = __fmaf_rn(2.0f, vd[c + 1], __fadd_rn(vd[c], vd[c + 2]));
+        }
+        g[0].x = __shfl_up_sync(0xffffffffu, g[4].x, 1);
+        g[0].y = __shfl_up_sync(0xffffffffu, g[4].y, 1);
+        g[1].x = __shfl_up_sync(0xffffffffu, g[5].x, 1);
+        g[1].y = __shfl_up_sync(0xffffffffu, g[5].y, 1);
+        g[6].x = __shfl_down_sync(0xffffffffu, g[2].x, 1);
+        g[6].y = __shfl_down_sync(0xffffffffu, g[2].y, 1);
+        g[7].x = __shfl_down_sync(0xffffffffu, g[3].x, 1);
+        g[7].y = __shfl_down_sync(0xffffffffu, g[3].y, 1);
+        float2 h2[4];
+        float2 hxy[2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float2 hxxyy = make_float2(0.0f, 0.0f);
+          float hh = 0.0f;
+#pragma unroll
+          for (int t2 = -A; t2 <= BB; ++t2) {
+            const float2 gg = g[2 + q + t2];
+            hxxyy = __ffma2_rn(gg, gg, hxxyy);
+            hh = __fmaf_rn(gg.x, gg.y, hh);
+          }
+          h2[q] = hxxyy;
+          if (q & 1) hxy[q >> 1].y = hh;
+          else hxy[q >> 1].x = hh;
+        }
+        float2 s2o[4];
+        float2 sxyo[2];
+        if (B > 1) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            s2o[q] = __fadd2_rn(c2[0][q], h2[q]);
+#pragma unroll
+            for (int k = 0; k + 1 < NC; ++k) c2[k][q] = __fadd2_rn(c2[k + 1][q], h2[q]);
+            c2[NC - 1][q] = h2[q];
+          }
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            sxyo[m] = __fadd2_rn(cxy[0][m], hxy[m]);
+#pragma unroll
+            for (int k = 0; k + 1 < NC; ++k) cxy[k][m] = __fadd2_rn(cxy[k + 1][m], hxy[m]);
+            cxy[NC - 1][m] = hxy[m];
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) s2o[q] = h2[q];
+          sxyo[0] = hxy[0];
+          sxyo[1] = hxy[1];
+        }
+        if (step >= B - 1) {
+          float R4[4];
+          R4[0] = harris_R(s2o[0].x, sxyo[0].x, s2o[0].y, p.k);
+          R4[1] = harris_R(s2o[1].x, sxyo[0].y, s2o[1].y, p.k);
+          R4[2] = harris_R(s2o[2].x, sxyo[1].x, s2o[2].y, p.k);
+          R4[3] = harris_R(s2o[3].x, sxyo[1].y, s2o[3].y, p.k);
+          if (emit) {
+            st_cs4(drow, make_float4(R4[0], R4[1], R4[2], R4[3]));
+            if (has_mask)
+              *reinterpret_cast<uchar4*>(mrow) = make_uchar4(R4[0] > p.threshold, R4[1] > p.threshold,
+                                                             R4[2] > p.threshold, R4[3] > p.threshold);
+          }
+          drow += dpitch;
+          mrow += has_mask ? p.mpitch : 0;
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
+template <int R, int B, int NW>
+__global__ void __launch_bounds__(32 * NW, 16 / NW) blur_harris_kernel(BlurHarrisParams bp, int S) {
+  extern __shared__ __align__(16) float smem[];
+  constexpr int TW = 120 * NW, HP = 8, A = B / 2, BB = B - 1 - A;
+  const int x0 = blockIdx.x * TW, ly0 = blockIdx.y * S;
+  const int ly1 = min(ly0 + S, bp.h.dst.H);
+  const int g0 = bp.h.dst.y0 + ly0;
+  // every raw row and column the CTA touches (Harris halo + blur radius) inside the image
+  const bool interior = x0 - HP - 4 >= 0 && x0 + TW + HP + 4 <= bp.h.src.W && g0 - A - 1 - R >= 0 &&
+                        bp.h.dst.y0 + ly1 + BB + 1 + R <= bp.h.src.Hg &&
+                        ((bp.raw.pitch | (int64_t)bp.raw.base) & 15) == 0;
+  if (interior) blur_harris_interior<R, B, NW>(bp, S, smem);
+  else blur_harris_general<R, B, NW>(bp, S, smem);
+}
+
 template <int R, int B>
 static cudaError_t launch_bh(const BlurHarrisParams& bp, int batch, int S, cudaStream_t s) {
   constexpr int NW = 2;
   constexpr int TW = 120 * NW;
-  const size_t smem = ((size_t)HarFastGeom<B>::NSR * (TW + 16) +
-                       (size_t)(2 * HarFastGeom<B>::RB + 2 * R + 1) * (TW + 24)) * sizeof(float);
+  const size_t smem = ((size_t)(ChainGeom<B>::NSR + 2) * (TW + 16) +   // blurred ring + mirror rows
+                       (size_t)(2 * ChainGeom<B>::RB + 2 * R + 1) * (TW + 24) +  // raw rows
+                       (size_t)(2 * R + 1) * (TW + 16)) * sizeof(float);  // row-pass ring (interior)
   auto kern = blur_harris_kernel<R, B, NW>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
