@@ -379,40 +379,60 @@ __device__ __forceinline__ void blur_harris_interior(const BlurHarrisParams& bp,
     }
     cp_async_commit();
   };
-  int tn = g0 - A - 1 - R;  // next raw row whose row pass goes into the t ring
+  // Ring indices are carried incrementally (no constant-divisor modulo in the row loop): the
+  // raw row gi + R of produced row kl sits in raw slot rs, its row pass goes to t slot ts, and
+  // the window's oldest t row (gi - R) is t slot to.
+  const float* rawt = raw + 4 * tid;
+  float* trt = tring + 4 * tid;
+  auto row_pass = [&](const float* rrow, float* tdst) {
+    const float4* rr = reinterpret_cast<const float4*>(rrow);
+    const float4 w0 = rr[0], w1 = rr[1], w2 = rr[2];
+    const float v12[12] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w, w2.x, w2.y, w2.z, w2.w};
+    float o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int i = 0; i < K; ++i) acc = __fmaf_rn(bp.fx[i], v12[4 - R + q + i], acc);
+      o[q] = acc;
+    }
+    *reinterpret_cast<float4*>(tdst) = make_float4(o[0], o[1], o[2], o[3]);
+  };
+  const int r_first = g0 - A - 1 - R;  // first raw row of the CTA (>= 0 here)
+  int rs = (r_first + 2 * R) % NRAW;   // raw slot of row (gi + R) for kl = 0
+  int ts = (2 * R) % K;                // t slot of that row
+  int to = 0;                          // t slot of row gi - R
+  int kr = 0;                          // blurred ring row of kl
   auto produce_block = [&](int m) {
     if (tid >= NSLOT) return;
+    if (m == 0) {  // the window's first 2R rows
+      int s = r_first % NRAW;
 #pragma unroll 1
-    for (int u = 0; u < RB; ++u) {
-      const int kl = m * RB + u;
-      if (kl >= NL) break;
-      const int gi = g0 - A - 1 + kl;
-      for (; tn <= gi + R; ++tn) {  // row pass of the raw rows the window gains
-        const float4* rr = reinterpret_cast<const float4*>(raw + (tn % NRAW) * RAWLEN + 4 * tid);
-        const float4 w0 = rr[0], w1 = rr[1], w2 = rr[2];
-        const float v12[12] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w, w2.x, w2.y, w2.z, w2.w};
-        float o[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float a = 0.0f;
-#pragma unroll
-          for (int i = 0; i < K; ++i) a = __fmaf_rn(bp.fx[i], v12[4 - R + q + i], a);
-          o[q] = a;
-        }
-        *reinterpret_cast<float4*>(tring + ((tn % K) * NSLOT + tid) * 4) = make_float4(o[0], o[1], o[2], o[3]);
+      for (int j = 0; j < 2 * R; ++j) {
+        row_pass(rawt + s * RAWLEN, trt + j * NSLOT * 4);
+        s = s + 1 == NRAW ? 0 : s + 1;
       }
+    }
+    const int nu = min(RB, NL - m * RB);
+#pragma unroll 1
+    for (int u = 0; u < nu; ++u) {
+      row_pass(rawt + rs * RAWLEN, trt + ts * NSLOT * 4);
       float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 #pragma unroll
       for (int j = 0; j < K; ++j) {
-        const float4 tv = *reinterpret_cast<const float4*>(tring + (((gi - R + j) % K) * NSLOT + tid) * 4);
+        const int sj = to + j < K ? to + j : to + j - K;
+        const float4 tv = *reinterpret_cast<const float4*>(trt + sj * NSLOT * 4);
         acc.x = __fmaf_rn(bp.gy[j], tv.x, acc.x);
         acc.y = __fmaf_rn(bp.gy[j], tv.y, acc.y);
         acc.z = __fmaf_rn(bp.gy[j], tv.z, acc.z);
         acc.w = __fmaf_rn(bp.gy[j], tv.w, acc.w);
       }
-      const int rr = kl % NSR;
-      *reinterpret_cast<float4*>(smem + rr * ROWLEN + 4 * tid) = acc;
-      if (rr < 2) *reinterpret_cast<float4*>(smem + (NSR + rr) * ROWLEN + 4 * tid) = acc;  // mirror
+      *reinterpret_cast<float4*>(smem + kr * ROWLEN + 4 * tid) = acc;
+      if (kr < 2) *reinterpret_cast<float4*>(smem + (NSR + kr) * ROWLEN + 4 * tid) = acc;  // mirror
+      rs = rs + 1 == NRAW ? 0 : rs + 1;
+      ts = ts + 1 == K ? 0 : ts + 1;
+      to = to + 1 == K ? 0 : to + 1;
+      kr = kr + 1 == NSR ? 0 : kr + 1;
     }
   };
   load_for_block(0);
