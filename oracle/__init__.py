@@ -52,7 +52,10 @@ def _load():
         lib.oracle_harris.argtypes = [p, i64, i64, i64, i32, f32, i32, f32, p, p, i64, p, p, i32]
         lib.oracle_nlm.argtypes = [p, i64, i64, i64, i32, i32, f32, i32, f32, p, p, i64, p, p, i32]
         lib.oracle_conv2d_u8.argtypes = [p, i64, i64, i64, p, i32, i32, f32, p, p, i64, p, i32]
-        for fn in (lib.oracle_sepconv, lib.oracle_harris, lib.oracle_nlm, lib.oracle_conv2d_u8):
+        lib.oracle_sepconv3d.argtypes = [p, i64, i64, i64, i64, i64, p, i32, p, i32, p, i32, i32, f32, p, p, p,
+                                         i64, p, i32]
+        for fn in (lib.oracle_sepconv, lib.oracle_harris, lib.oracle_nlm, lib.oracle_conv2d_u8,
+                   lib.oracle_sepconv3d):
             fn.restype = i32
         lib.oracle_nthreads_default.restype = i32
         _lib = lib
@@ -99,6 +102,33 @@ def sepconv(img, taps_x, taps_y, border="constant", border_value=0.0, points=Non
                                 _ptr(ys), n, out.ctypes.data, threads)
     if rc:
         raise ValueError("oracle_sepconv: invalid arguments")
+    return out
+
+
+def sepconv3d(vol, taps_x, taps_y, taps_z, border="constant", border_value=0.0, points=None, threads=0):
+    """3-D separable convolution of a (D, H, W) fp32 volume ("2D/3D indexing"):
+    out(x,y,z) = sum_k h_k sum_j g_j sum_i f_i in_B(x+i, y+j, z+k), the boundary per axis.
+    points: (xs, ys, zs) arrays for sampled outputs."""
+    if vol.dtype != np.float32 or vol.ndim != 3 or vol.strides[2] != 4 or vol.strides[1] % 4 or vol.strides[0] % 4:
+        raise TypeError("oracle volumes are (D, H, W) float32 arrays with contiguous rows")
+    fx = np.ascontiguousarray(taps_x, dtype=np.float32)
+    gy = np.ascontiguousarray(taps_y, dtype=np.float32)
+    hz = np.ascontiguousarray(taps_z, dtype=np.float32)
+    assert fx.size % 2 == 1 and gy.size % 2 == 1 and hz.size % 2 == 1
+    d, h, w = vol.shape
+    if points is None:
+        xs = ys = zs = None
+        n, shape = d * h * w, (d, h, w)
+    else:
+        xs, ys, zs = (np.ascontiguousarray(a, dtype=np.int64) for a in points)
+        n, shape = xs.size, (xs.size,)
+    out = np.empty(shape, dtype=np.float64)
+    rc = _load().oracle_sepconv3d(vol.ctypes.data, w, h, d, vol.strides[1] // 4, vol.strides[0] // 4,
+                                  fx.ctypes.data, fx.size // 2, gy.ctypes.data, gy.size // 2, hz.ctypes.data,
+                                  hz.size // 2, _BORDERS[border], float(border_value), _ptr(xs), _ptr(ys),
+                                  _ptr(zs), n, out.ctypes.data, threads)
+    if rc:
+        raise ValueError("oracle_sepconv3d: invalid arguments")
     return out
 
 

@@ -33,6 +33,10 @@
  *     PAPER.md:577-579; Table 3):
  *       out(x,y) = sum_{j=-r..r} sum_{i=-r..r} f[j+r][i+r] * in_B(x+i, y+j)
  *     (correlation, reading R1; real-valued output, reading R22).
+ *   3-D separable convolution of a volume (ImageCL Images "support 2D/3D
+ *     indexing"; R26): the
+ *     sepconv definition with a third axis and the boundary applied per axis,
+ *       out(x,y,z) = sum_k h_k sum_j g_j sum_i f_i in_B(x+i, y+j, z+k).
  *
  * Threading: the point list is split into contiguous chunks, one pthread per
  * chunk; each output is computed independently in a fixed order, so results
@@ -336,6 +340,93 @@ int oracle_conv2d_u8(const uint8_t* in, int64_t W, int64_t H, int64_t pitch, con
     int64_t npts = xs ? n : W * H;
     run_points(F_CONV2D, &a, W, npts, xs, ys, out, NULL, nthreads);
     free(f);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* 3-D separable convolution (plain triple sum over the boundary-extended     */
+/* volume, pixel by pixel).                                                    */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    const float* u;
+    int64_t W, H, D, pitch, spitch; /* elements */
+    int border;
+    double c;
+    const double *f, *g, *h;
+    int rx, ry, rz;
+    const int64_t *xs, *ys, *zs;
+    int64_t begin, end;
+    double* out;
+} sep3_job;
+
+static double read_B3(const sep3_job* a, int64_t x, int64_t y, int64_t z) {
+    if (x < 0 || x >= a->W || y < 0 || y >= a->H || z < 0 || z >= a->D) {
+        if (a->border == OR_BORDER_CONSTANT) return a->c;
+        x = clampi(x, 0, a->W - 1);
+        y = clampi(y, 0, a->H - 1);
+        z = clampi(z, 0, a->D - 1);
+    }
+    return (double)a->u[z * a->spitch + y * a->pitch + x];
+}
+
+static void* sep3_run(void* p) {
+    sep3_job* a = (sep3_job*)p;
+    for (int64_t n = a->begin; n < a->end; ++n) {
+        int64_t x, y, z;
+        if (a->xs) { x = a->xs[n]; y = a->ys[n]; z = a->zs[n]; }
+        else { x = n % a->W; y = (n / a->W) % a->H; z = n / (a->W * a->H); }
+        double out = 0.0;
+        for (int k = -a->rz; k <= a->rz; ++k) {
+            double s = 0.0;
+            for (int j = -a->ry; j <= a->ry; ++j) {
+                double t = 0.0;
+                for (int i = -a->rx; i <= a->rx; ++i) t += a->f[i + a->rx] * read_B3(a, x + i, y + j, z + k);
+                s += a->g[j + a->ry] * t;
+            }
+            out += a->h[k + a->rz] * s;
+        }
+        a->out[n] = out;
+    }
+    return NULL;
+}
+
+int oracle_sepconv3d(const float* in, int64_t W, int64_t H, int64_t D, int64_t pitch, int64_t spitch,
+                     const float* fx, int rx, const float* gy, int ry, const float* hz, int rz, int border,
+                     float c, const int64_t* xs, const int64_t* ys, const int64_t* zs, int64_t n, double* out,
+                     int nthreads) {
+    if (!in || W < 1 || H < 1 || D < 1 || pitch < W || spitch < pitch * H || rx < 0 || ry < 0 || rz < 0 ||
+        !fx || !gy || !hz || !out)
+        return -1;
+    if (border != OR_BORDER_CONSTANT && border != OR_BORDER_CLAMP) return -1;
+    double* f = (double*)malloc(sizeof(double) * (size_t)(2 * rx + 1));
+    double* g = (double*)malloc(sizeof(double) * (size_t)(2 * ry + 1));
+    double* h = (double*)malloc(sizeof(double) * (size_t)(2 * rz + 1));
+    for (int i = 0; i < 2 * rx + 1; ++i) f[i] = (double)fx[i];
+    for (int j = 0; j < 2 * ry + 1; ++j) g[j] = (double)gy[j];
+    for (int k = 0; k < 2 * rz + 1; ++k) h[k] = (double)hz[k];
+    const int64_t npts = xs ? n : W * H * D;
+    if (nthreads <= 0) nthreads = (int)sysconf(_SC_NPROCESSORS_ONLN);
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    if ((int64_t)nthreads > npts) nthreads = npts > 0 ? (int)npts : 1;
+    pthread_t th[256];
+    int spawned[256];
+    sep3_job jobs[256];
+    const int64_t chunk = (npts + nthreads - 1) / nthreads;
+    for (int t = 0; t < nthreads; ++t) {
+        sep3_job j = {in, W, H, D, pitch, spitch, border, (double)c, f, g, h, rx, ry, rz, xs, ys, zs,
+                      t * chunk < npts ? t * chunk : npts, (t + 1) * chunk < npts ? (t + 1) * chunk : npts, out};
+        jobs[t] = j;
+        spawned[t] = 0;
+        if (jobs[t].begin >= jobs[t].end) continue;
+        if (t != nthreads - 1 && pthread_create(&th[t], NULL, sep3_run, &jobs[t]) == 0) spawned[t] = 1;
+        else sep3_run(&jobs[t]);
+    }
+    for (int t = 0; t < nthreads; ++t)
+        if (spawned[t]) pthread_join(th[t], NULL);
+    free(f);
+    free(g);
+    free(h);
     return 0;
 }
 

@@ -324,3 +324,60 @@ def test_uniform_u8_is_the_top_byte_of_the_u01_stream():
     b = synth.uniform_u8(13, 7, 9)
     np.testing.assert_array_equal(b, np.floor(u.astype(np.float64) * 256).astype(np.uint8))
     np.testing.assert_array_equal(synth.uniform_u8(13, 7, 9, row0=3, rows=2), b[3:5])
+
+
+# ----------------------------------------------------------------------------- 3-D separable convolution
+def _vol(seed, d, h, w):
+    return np.stack([synth.uniform_image(seed + z, h, w) for z in range(d)]) - np.float32(0.5)
+
+
+@pytest.mark.parametrize("border,c", BORDERS)
+@pytest.mark.parametrize("shape,rx,ry,rz", [((5, 7, 9), 2, 1, 1), ((9, 4, 6), 1, 2, 3), ((1, 6, 11), 1, 1, 2),
+                                            ((7, 1, 1), 0, 0, 3), ((4, 5, 3), 3, 3, 2)])
+def test_sepconv3d_equals_3d_correlation(border, c, shape, rx, ry, rz):
+    """Separable 3-D = scipy.ndimage.correlate with the outer-product kernel h (x) g (x) f."""
+    vol = _vol(21, *shape)
+    f, g, h = synth.signed_taps(7, rx), synth.signed_taps(8, ry), synth.signed_taps(9, rz)
+    out = oracle.sepconv3d(vol, f, g, h, border, c)
+    ker = np.einsum("k,j,i->kji", h.astype(np.float64), g.astype(np.float64), f.astype(np.float64))
+    ref = ndi.correlate(vol.astype(np.float64), ker, **_mode(border, c))
+    np.testing.assert_allclose(out, ref, rtol=0, atol=1e-13)
+
+
+def test_sepconv3d_delta_orientation():
+    """A delta at (x0,y0,z0) lands at out(x0-i, y0-j, z0-k) = f_i g_j h_k: correlation on every axis."""
+    vol = np.zeros((7, 8, 9), np.float32)
+    vol[3, 4, 5] = 1.0
+    f, g, h = synth.signed_taps(1, 1), synth.signed_taps(2, 2), synth.signed_taps(3, 1)
+    out = oracle.sepconv3d(vol, f, g, h, "constant", 0.0)
+    for k in range(-1, 2):
+        for j in range(-2, 3):
+            for i in range(-1, 2):
+                assert out[3 - k, 4 - j, 5 - i] == float(f[i + 1]) * float(g[j + 2]) * float(h[k + 1])
+    assert np.count_nonzero(out) == 3 * 5 * 3
+
+
+@pytest.mark.parametrize("border,c", BORDERS)
+def test_sepconv3d_reduces_to_2d_and_constant(border, c):
+    """rz = 0 with h = [1] is the 2-D oracle slice by slice; a constant volume gives c·Σf·Σg·Σh."""
+    vol = _vol(31, 3, 6, 7)
+    f, g = synth.gaussian_taps(2), synth.signed_taps(4, 1)
+    out = oracle.sepconv3d(vol, f, g, [1.0], border, c)
+    for z in range(3):
+        np.testing.assert_array_equal(out[z], oracle.sepconv(np.ascontiguousarray(vol[z]), f, g, border, c))
+    cv = np.full((4, 5, 6), 0.375, np.float32)
+    h = synth.signed_taps(6, 2)
+    out = oracle.sepconv3d(cv, f, g, h, "clamp")
+    exp = 0.375 * f.astype(np.float64).sum() * g.astype(np.float64).sum() * h.astype(np.float64).sum()
+    np.testing.assert_allclose(out, exp, rtol=1e-13, atol=1e-15)
+
+
+def test_sepconv3d_points_and_strides():
+    vol = _vol(41, 5, 6, 7)
+    padded = np.zeros((5, 8, 12), np.float32)
+    padded[:, :6, :7] = vol
+    f, g, h = synth.gaussian_taps(1), synth.gaussian_taps(2), synth.gaussian_taps(1)
+    full = oracle.sepconv3d(vol, f, g, h, "clamp")
+    np.testing.assert_array_equal(oracle.sepconv3d(padded[:, :6, :7], f, g, h, "clamp"), full)
+    xs, ys, zs = np.array([0, 6, 3]), np.array([0, 5, 2]), np.array([4, 0, 2])
+    np.testing.assert_array_equal(oracle.sepconv3d(vol, f, g, h, "clamp", points=(xs, ys, zs)), full[zs, ys, xs])
