@@ -57,7 +57,13 @@ typedef enum {
 
 typedef enum { ICL_BORDER_CONSTANT = 0, ICL_BORDER_CLAMP = 1 } icl_border;
 
-typedef enum { ICL_FILTER_SEPCONV = 0, ICL_FILTER_HARRIS = 1, ICL_FILTER_NLM = 2, ICL_FILTER_CONV2D = 3 } icl_filter;
+typedef enum {
+    ICL_FILTER_SEPCONV = 0,
+    ICL_FILTER_HARRIS = 1,
+    ICL_FILTER_NLM = 2,
+    ICL_FILTER_CONV2D = 3,
+    ICL_FILTER_SEPCONV3D = 4 /* icl_sepconv3d (variant registry / force / last only) */
+} icl_filter;
 
 /* A (batch of) 2-D image(s).  `data` is a device pointer or a HOST pointer
  * (fp32 pixels for images, uint8 for masks).  When any operand of
@@ -209,6 +215,18 @@ icl_status icl_nlm_sharded(icl_comm* comm, const icl_image* buf, const icl_image
 icl_status icl_conv2d_u8_sharded(icl_comm* comm, const icl_image* buf, const icl_image* dst, int64_t global_height,
                                  const float* filter, int radius, icl_border border, float border_value,
                                  void* stream);
+
+/* Separable convolution of a 3-D volume (ImageCL Images support "2D/3D
+ * indexing"):
+ *     out(x,y,z) = sum_k h_k sum_j g_j sum_i f_i in_B(x+i, y+j, z+k)
+ * (correlation on every axis, the boundary per axis, R26).  A
+ * volume is an icl_image whose batch axis is z: batch = depth,
+ * batch_stride_bytes = the slice stride.  Taps: HOST pointers, 2r+1 each,
+ * radii 0..7 (> 7 -> ICL_ERR_UNSUPPORTED).  Device volumes only; src and dst
+ * must not overlap (ICL_ERR_ALIASING); shapes must match.  All variants
+ * evaluate the same fp32 chains (bit-identical).  Enqueues on stream. */
+icl_status icl_sepconv3d(const icl_image* src, const icl_image* dst, const float* taps_x, int rx, const float* taps_y,
+                         int ry, const float* taps_z, int rz, icl_border border, float border_value, void* stream);
 
 /* Two-filter pipeline in one pass (FAST-style filter
  * chains, §2.2): separable smoothing then Harris,

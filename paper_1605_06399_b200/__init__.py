@@ -22,7 +22,7 @@ ICL_OK = 0
 STATUS = {0: "ICL_OK", 1: "ICL_ERR_INVALID_ARG", 2: "ICL_ERR_ALIASING", 3: "ICL_ERR_UNSUPPORTED",
           4: "ICL_ERR_WORKSPACE", 5: "ICL_ERR_CUDA", 6: "ICL_ERR_NCCL", 7: "ICL_ERR_NOT_TUNED"}
 BORDER = {"constant": 0, "clamp": 1}
-FILTER = {"sepconv": 0, "harris": 1, "nlm": 2, "conv2d": 3}
+FILTER = {"sepconv": 0, "harris": 1, "nlm": 2, "conv2d": 3, "sepconv3d": 4}
 
 # Symbols include/icl.h declares (checked by tests/test_abi.py).
 EXPORTS = ("icl_sepconv", "icl_sepconv_workspace_bytes", "icl_harris", "icl_nlm", "icl_conv2d_u8", "icl_tune",
@@ -33,7 +33,7 @@ EXPORTS = ("icl_sepconv", "icl_sepconv_workspace_bytes", "icl_harris", "icl_nlm"
            "icl_comm_destroy", "icl_sepconv_sharded", "icl_harris_sharded", "icl_nlm_sharded", "icl_conv2d_u8_sharded",
            "icl_tune_ann", "icl_ann_search", "icl_ann_fit", "icl_blur_harris", "icl_blur_harris_workspace_bytes",
            "icl_ipc_get_handle", "icl_ipc_open", "icl_ipc_close", "icl_sepconv_peer",
-           "icl_halo_pull")
+           "icl_halo_pull", "icl_sepconv3d")
 
 # int evaluate(void* ctx, int index, double* value) -- icl_ann_search's callback
 EVAL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double))
@@ -121,6 +121,7 @@ def load_library(path: str = LIB_PATH):
         "icl_ipc_close": ([P, ctypes.c_uint64], I),
         "icl_sepconv_peer": ([img, img, I64, I64, img, img, P, I, P, I, I, F, P], I),
         "icl_halo_pull": ([img, I64, I64, I64, I64, img, img, I, P], I),
+        "icl_sepconv3d": ([img, img, P, I, P, I, P, I, I, F, P], I),
         "icl_tune_ann": ([ctypes.POINTER(icl_problem), I, I, ctypes.c_uint64, P, ctypes.POINTER(icl_variant_info)], I),
         "icl_ann_search": ([ctypes.POINTER(ctypes.c_double), I, I, EVAL_FN, P, I, I, ctypes.c_uint64,
                             ctypes.POINTER(I), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I), ctypes.POINTER(I)], I),
@@ -203,6 +204,20 @@ def sepconv(src, dst, taps_x: Sequence[float], taps_y: Sequence[float], border: 
     _check(lib.icl_sepconv(ctypes.byref(s), ctypes.byref(d), ctypes.cast(fx, ctypes.c_void_p), len(fx) // 2,
                            ctypes.cast(gy, ctypes.c_void_p), len(gy) // 2, BORDER[border], border_value,
                            _ref(_band(band)), ws, wsb, _stream(stream)))
+    return dst
+
+
+def sepconv3d(src, dst, taps_x: Sequence[float], taps_y: Sequence[float], taps_z: Sequence[float],
+              border: str = "constant", border_value: float = 0.0, stream=None):
+    """Separable convolution of (D, H, W) volumes (icl_sepconv3d; PAPER.md:303-304 2D/3D Images)."""
+    if src.dim() != 3 or dst.dim() != 3:
+        raise ValueError("volumes are (D, H, W) tensors")
+    lib = load_library()
+    s, d = _image(src), _image(dst)
+    fx, gy, hz = _taps(taps_x), _taps(taps_y), _taps(taps_z)
+    _check(lib.icl_sepconv3d(ctypes.byref(s), ctypes.byref(d), ctypes.cast(fx, ctypes.c_void_p), len(fx) // 2,
+                             ctypes.cast(gy, ctypes.c_void_p), len(gy) // 2, ctypes.cast(hz, ctypes.c_void_p),
+                             len(hz) // 2, BORDER[border], border_value, _stream(stream)))
     return dst
 
 

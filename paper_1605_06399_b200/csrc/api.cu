@@ -194,20 +194,27 @@ static const Variant kConvVariants[] = {
     {"tex_c4r4", K_TEX, 128, 4, 4},
 };
 
+// 3-D volumes (icl_sepconv3d; sep3d.cu): dispatched by icl_sepconv3d itself
+static const Variant kSep3Variants[] = {
+    {"naive_direct", K_NAIVE, 0, 0, 0},
+    {"tile64x16", K_TILE2, 256, 1, 64},
+};
+
 static const Variant* table(icl_filter f, int* n) {
   switch (f) {
     case ICL_FILTER_SEPCONV: *n = (int)(sizeof kSepVariants / sizeof *kSepVariants); return kSepVariants;
     case ICL_FILTER_HARRIS: *n = (int)(sizeof kHarVariants / sizeof *kHarVariants); return kHarVariants;
     case ICL_FILTER_NLM: *n = (int)(sizeof kNlmVariants / sizeof *kNlmVariants); return kNlmVariants;
     case ICL_FILTER_CONV2D: *n = (int)(sizeof kConvVariants / sizeof *kConvVariants); return kConvVariants;
+    case ICL_FILTER_SEPCONV3D: *n = (int)(sizeof kSep3Variants / sizeof *kSep3Variants); return kSep3Variants;
   }
   *n = 0;
   return nullptr;
 }
 
-constexpr int kNFilters = 4;
-static thread_local int t_force[kNFilters] = {-1, -1, -1, -1};
-static thread_local int t_last[kNFilters] = {-1, -1, -1, -1};
+constexpr int kNFilters = 5;
+static thread_local int t_force[kNFilters] = {-1, -1, -1, -1, -1};
+static thread_local int t_last[kNFilters] = {-1, -1, -1, -1, -1};
 
 // Prepared call of any filter (what a variant launcher needs).
 struct Prepared {
@@ -1071,6 +1078,53 @@ icl_status icl_blur_harris(const icl_image* src, const icl_image* response, cons
   raw.cval = blur_border_value;
   cudaError_t e = launch_blur_harris(pc.har, raw, taps_x, rx, taps_y, ry, S, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "blur_harris");
+  return ICL_OK;
+}
+
+icl_status icl_sepconv3d(const icl_image* src, const icl_image* dst, const float* taps_x, int rx, const float* taps_y,
+                         int ry, const float* taps_z, int rz, icl_border border, float border_value, void* stream) {
+  icl_status st;
+  if ((st = check_image(src, 4, "src")) || (st = check_image(dst, 4, "dst"))) return st;
+  if (!taps_x || !taps_y || !taps_z) return fail(ICL_ERR_INVALID_ARG, "null taps");
+  if (rx < 0 || ry < 0 || rz < 0) return fail(ICL_ERR_INVALID_ARG, "negative radius");
+  if (rx > 7 || ry > 7 || rz > 7) return fail(ICL_ERR_UNSUPPORTED, "3-D radius > 7");
+  for (int i = 0; i < 2 * rx + 1; ++i)
+    if (!std::isfinite(taps_x[i])) return fail(ICL_ERR_INVALID_ARG, "non-finite tap");
+  for (int i = 0; i < 2 * ry + 1; ++i)
+    if (!std::isfinite(taps_y[i])) return fail(ICL_ERR_INVALID_ARG, "non-finite tap");
+  for (int i = 0; i < 2 * rz + 1; ++i)
+    if (!std::isfinite(taps_z[i])) return fail(ICL_ERR_INVALID_ARG, "non-finite tap");
+  if (border != ICL_BORDER_CONSTANT && border != ICL_BORDER_CLAMP)
+    return fail(ICL_ERR_INVALID_ARG, "border must be ICL_BORDER_CONSTANT or ICL_BORDER_CLAMP");
+  if (std::isnan(border_value)) return fail(ICL_ERR_INVALID_ARG, "border_value is NaN");
+  if (src->width != dst->width || src->height != dst->height || src->batch != dst->batch)
+    return fail(ICL_ERR_INVALID_ARG, "src and dst volumes differ in shape");
+  if (src->height > 524280) return fail(ICL_ERR_UNSUPPORTED, "volume slices taller than 524280 rows");
+  if (overlap(byte_range(src, 4), byte_range(dst, 4))) return fail(ICL_ERR_ALIASING, "src and dst overlap");
+  if (any_host(src, dst, nullptr)) return fail(ICL_ERR_INVALID_ARG, "icl_sepconv3d takes device volumes only");
+  Sep3Params p;
+  p.src = static_cast<const char*>(src->data);
+  p.spitch = src->pitch_bytes;
+  p.sslice = src->batch > 1 ? src->batch_stride_bytes : 0;
+  p.dst = static_cast<char*>(dst->data);
+  p.dpitch = dst->pitch_bytes;
+  p.dslice = dst->batch > 1 ? dst->batch_stride_bytes : 0;
+  p.W = (int)src->width;
+  p.H = (int)src->height;
+  p.D = (int)src->batch;
+  p.border = border == ICL_BORDER_CLAMP ? kBorderClamp : kBorderConstant;
+  p.cval = border_value;
+  p.rx = rx;
+  p.ry = ry;
+  p.rz = rz;
+  for (int i = 0; i < 15; ++i) p.fx[i] = p.gy[i] = p.hz[i] = 0.0f;
+  for (int i = 0; i < 2 * rx + 1; ++i) p.fx[i] = taps_x[i];
+  for (int i = 0; i < 2 * ry + 1; ++i) p.gy[i] = taps_y[i];
+  for (int i = 0; i < 2 * rz + 1; ++i) p.hz[i] = taps_z[i];
+  const int vid = t_force[ICL_FILTER_SEPCONV3D] >= 0 ? t_force[ICL_FILTER_SEPCONV3D] : 1;
+  cudaError_t e = launch_sep3d(p, vid, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "sepconv3d");
+  t_last[ICL_FILTER_SEPCONV3D] = vid;
   return ICL_OK;
 }
 

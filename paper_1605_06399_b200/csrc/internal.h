@@ -98,6 +98,22 @@ constexpr int kAnnMinSamples = 10;
 int ann_search(int ncfg, int nf, const double* feats, const std::function<bool(int, double*)>& evaluate, int n1,
                int topk, uint64_t seed, std::vector<int>* evaluated, int* best, double* best_val);
 
+// 3-D separable convolution (sep3d.cu); variant 0 naive, 1 tile<R>.  A volume's z axis is the
+// icl_image batch axis (slice stride = batch stride).
+struct Sep3Params {
+  const char* src;
+  int64_t spitch, sslice;  // bytes
+  char* dst;
+  int64_t dpitch, dslice;
+  int W, H, D;
+  int border;
+  float cval;
+  int rx, ry, rz;
+  float fx[2 * 7 + 1], gy[2 * 7 + 1], hz[2 * 7 + 1];  // padded to R in tile<R>
+};
+bool sep3d_tile_supported(int R);
+cudaError_t launch_sep3d(const Sep3Params& p, int variant, cudaStream_t s);
+
 // synthetic inputs
 cudaError_t launch_fill_uniform(float* base, int64_t W, int64_t H, int64_t pitch, int64_t batch,
                                 int64_t bstride, uint64_t seed, int64_t row0, cudaStream_t s);

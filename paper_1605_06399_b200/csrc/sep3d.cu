@@ -1,0 +1,190 @@
+// sep3d.cu -- separable convolution of 3-D volumes (ImageCL Images support
+// "2D/3D indexing"; R26).
+//
+//     out(x,y,z) = sum_k h_k sum_j g_j sum_i f_i in_B(x+i, y+j, z+k)
+//
+// A volume is an icl_image whose batch axis is z (batch = depth, the batch
+// stride = the slice stride); the boundary applies per axis.  Every variant
+// evaluates the same fp32 chains (from 0.0f, taps in index order):
+//     t = fma-chain_i f_i in_B,  s = fma-chain_j g_j t,  out = fma-chain_k h_k s
+// so the variants are bit-identical (R16's rule carried to 3-D).
+//
+// Variants: "naive_direct" (one thread per voxel, direct loads) and
+// "tile64x16" (tile<R>): a CTA owns a 64 x 16 (x, y) tile and streams a
+// chunk of slices along z.  Per input slice: the (16+2R) x (64+2R) input tile
+// into shared memory, the row pass into a second smem tile, the column pass
+// into registers (4 consecutive rows per thread, sliding), and a register
+// ring of the last 2R+1 column-pass results per output; once it is full each
+// new slice emits one output slice.
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace icl {
+
+__device__ __forceinline__ float read_B3(const Sep3Params& p, int x, int y, int z) {
+  if (x < 0 || x >= p.W || y < 0 || y >= p.H || z < 0 || z >= p.D) {
+    if (p.border == kBorderConstant) return p.cval;
+    x = clampi(x, 0, p.W - 1);
+    y = clampi(y, 0, p.H - 1);
+    z = clampi(z, 0, p.D - 1);
+  }
+  return __ldg(reinterpret_cast<const float*>(p.src + (int64_t)z * p.sslice + (int64_t)y * p.spitch) + x);
+}
+
+__global__ void __launch_bounds__(256) sep3d_naive(Sep3Params p) {
+  const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (x >= p.W || y >= p.H) return;
+  for (int z = blockIdx.z; z < p.D; z += gridDim.z) {
+    float out = 0.0f;
+    for (int k = -p.rz; k <= p.rz; ++k) {
+      float s = 0.0f;
+      for (int j = -p.ry; j <= p.ry; ++j) {
+        float t = 0.0f;
+        for (int i = -p.rx; i <= p.rx; ++i) t = __fmaf_rn(p.fx[i + p.rx], read_B3(p, x + i, y + j, z + k), t);
+        s = __fmaf_rn(p.gy[j + p.ry], t, s);
+      }
+      out = __fmaf_rn(p.hz[k + p.rz], s, out);
+    }
+    reinterpret_cast<float*>(p.dst + (int64_t)z * p.dslice + (int64_t)y * p.dpitch)[x] = out;
+  }
+}
+
+constexpr int k3TW = 64, k3TH = 16, k3NT = 256;
+
+template <int R>
+__global__ void __launch_bounds__(k3NT) sep3d_tile(Sep3Params p, int zchunk) {
+  constexpr int K = 2 * R + 1;
+  constexpr int IW = k3TW + 2 * R, IH = k3TH + 2 * R;
+  __shared__ float sin_[IH][IW];
+  __shared__ float st[IH][k3TW];
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * k3TW, y0 = blockIdx.y * k3TH;
+  const int z0 = blockIdx.z * zchunk, z1 = min(z0 + zchunk, p.D);
+  const int tx = tid & (k3TW - 1), ty = (tid / k3TW) * 4;  // outputs (x0+tx, y0+ty .. +3)
+  const int x = x0 + tx;
+  float ring[K][4];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ring[k][q] = 0.0f;
+  const bool interior_xy = x0 - R >= 0 && x0 + k3TW + R <= p.W && y0 - R >= 0 && y0 + k3TH + R <= p.H;
+
+  // input slices are fetched into registers one slice ahead (the global loads of slice zz+1
+  // are in flight while slice zz is convolved), then stored to shared memory
+  constexpr int NPRE = (IH * IW + k3NT - 1) / k3NT;
+  float pre[NPRE];
+  auto fetch = [&](int zz) {
+    const bool zout = zz < 0 || zz >= p.D;
+    const int zs = clampi(zz, 0, p.D - 1);
+    const char* sl = p.src + (int64_t)zs * p.sslice;
+#pragma unroll
+    for (int e = 0; e < NPRE; ++e) {
+      const int idx = tid + e * k3NT;
+      if (idx < IH * IW) {
+        const int r = idx / IW, c = idx - r * IW;
+        if (zout && p.border == kBorderConstant) pre[e] = p.cval;  // constant slice
+        else if (interior_xy)
+          pre[e] = __ldg(reinterpret_cast<const float*>(sl + (int64_t)(y0 - R + r) * p.spitch) + (x0 - R + c));
+        else pre[e] = read_B3(p, x0 - R + c, y0 - R + r, zs);
+      }
+    }
+  };
+  fetch(z0 - R);
+#pragma unroll 1
+  for (int zz = z0 - R; zz < z1 + R; ++zz) {
+#pragma unroll
+    for (int e = 0; e < NPRE; ++e) {
+      const int idx = tid + e * k3NT;
+      if (idx < IH * IW) (&sin_[0][0])[idx] = pre[e];
+    }
+    __syncthreads();
+    if (zz + 1 < z1 + R) fetch(zz + 1);
+    // row pass: t(x, y') for the tile's columns and its 16 + 2R rows
+    for (int e = tid; e < IH * k3TW; e += k3NT) {
+      const int r = e / k3TW, c = e - r * k3TW;
+      float t = 0.0f;
+#pragma unroll
+      for (int i = 0; i < K; ++i) t = __fmaf_rn(p.fx[i], sin_[r][c + i], t);
+      st[r][c] = t;
+    }
+    __syncthreads();
+    // column pass for 4 consecutive rows; slide the z ring
+    float s[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float a = 0.0f;
+#pragma unroll
+      for (int j = 0; j < K; ++j) a = __fmaf_rn(p.gy[j], st[ty + q + j][tx], a);
+      s[q] = a;
+    }
+#pragma unroll
+    for (int k = 0; k + 1 < K; ++k)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ring[k][q] = ring[k + 1][q];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ring[K - 1][q] = s[q];
+    const int z = zz - R;  // output slice completed by input slice zz
+    if (z >= z0 && x < p.W) {
+      float* drow = reinterpret_cast<float*>(p.dst + (int64_t)z * p.dslice);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int y = y0 + ty + q;
+        if (y < p.H) {
+          float o = 0.0f;
+#pragma unroll
+          for (int k = 0; k < K; ++k) o = __fmaf_rn(p.hz[k], ring[k][q], o);
+          reinterpret_cast<float*>(reinterpret_cast<char*>(drow) + (int64_t)y * p.dpitch)[x] = o;
+        }
+      }
+    }
+    __syncthreads();  // smem tiles are rewritten by the next slice
+  }
+}
+
+bool sep3d_tile_supported(int R) { return R >= 0 && R <= 7; }
+
+cudaError_t launch_sep3d(const Sep3Params& p0, int variant, cudaStream_t s) {
+  Sep3Params p = p0;
+  if (variant == 0) {
+    dim3 grd((p.W + 31) / 32, (p.H + 7) / 8, (unsigned)min(p.D, 65535));
+    sep3d_naive<<<grd, 256, 0, s>>>(p);
+    count_launch();
+    return cudaGetLastError();
+  }
+  const int R = max(p.rx, max(p.ry, p.rz));
+  // zero-pad the taps to R (fma(0, v, a) == a: the same values)
+  float f[15] = {0}, g[15] = {0}, h[15] = {0};
+  for (int i = -p.rx; i <= p.rx; ++i) f[R + i] = p0.fx[p.rx + i];
+  for (int j = -p.ry; j <= p.ry; ++j) g[R + j] = p0.gy[p.ry + j];
+  for (int k = -p.rz; k <= p.rz; ++k) h[R + k] = p0.hz[p.rz + k];
+  for (int i = 0; i < 15; ++i) { p.fx[i] = f[i]; p.gy[i] = g[i]; p.hz[i] = h[i]; }
+  // z chunk: enough CTAs for ~4 per SM (2 resident at 256 threads x ~120 registers), but at
+  // least 8R slices so the 2R recomputed halo slices stay <= 25% of a chunk
+  static int nsm = 0;
+  if (!nsm) {
+    int d = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, d);
+    if (nsm < 1) nsm = 148;
+  }
+  const int64_t tiles = (int64_t)((p.W + k3TW - 1) / k3TW) * ((p.H + k3TH - 1) / k3TH);
+  int zchunk = (int)std::min<int64_t>(64, std::max<int64_t>(1, (int64_t)p.D * tiles / (4 * nsm)));
+  zchunk = std::max(zchunk, std::max(8, 8 * R));
+  const int zb = (p.D + zchunk - 1) / zchunk;
+  if (zb > 65535) return cudaErrorInvalidValue;
+  dim3 grd((p.W + k3TW - 1) / k3TW, (p.H + k3TH - 1) / k3TH, zb);
+  switch (R) {
+#define ICL_S3(RR) \
+  case RR: sep3d_tile<RR><<<grd, k3NT, 0, s>>>(p, zchunk); break;
+    ICL_S3(0) ICL_S3(1) ICL_S3(2) ICL_S3(3) ICL_S3(4) ICL_S3(5) ICL_S3(6) ICL_S3(7)
+#undef ICL_S3
+    default: return cudaErrorInvalidValue;
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace icl
