@@ -1,6 +1,8 @@
 """Small ragged cases exercising every variant of every filter once (for
 compute-sanitizer memcheck / racecheck / synccheck runs; see tools/sanitize.sh)."""
 import sys
+
+import numpy as np
 import torch
 sys.path.insert(0, '.')
 import paper_1605_06399_b200 as icl  # noqa: E402
@@ -79,4 +81,16 @@ for (h, w) in [(61, 52), (130, 516), (300, 200)]:
             icl.blur_harris(img, out, fx, fx, bb, 0.5, 5, 0.04, hb, 0.25, mask=mask, threshold=0.1)
             icl.blur_harris(img, out, fx, fx, bb, 0.5, 3, 0.04, hb, 0.25, mask=mask, threshold=0.1, workspace=ws)
     torch.cuda.synchronize()
+# 3-D volumes: both variants, ragged shapes, radii up to 7, both borders
+for shape in [(5, 13, 70), (17, 20, 3)]:
+    v = torch.from_numpy(np.stack([synth.uniform_image(7 + z, shape[1], shape[2]) for z in range(shape[0])])).to(dev)
+    o = torch.empty_like(v)
+    for name in icl.variant_names("sepconv3d"):
+        icl.force_variant("sepconv3d", name)
+        for r in (0, 1, 3, 7):
+            fx = synth.gaussian_taps(r)
+            for border in ("constant", "clamp"):
+                icl.sepconv3d(v, o, fx, fx, fx, border, 0.5)
+        torch.cuda.synchronize()
+    icl.force_variant("sepconv3d", None)
 print("sanitize cases done")
