@@ -12,10 +12,10 @@
 // Variants: "naive_direct" (one thread per voxel, direct loads) and
 // "tile64x16" (tile<R>): a CTA owns a 64 x 16 (x, y) tile and streams a
 // chunk of slices along z.  Per input slice: the (16+2R) x (64+2R) input tile
-// into shared memory, the row pass into a second smem tile, the column pass
-// into registers (4 consecutive rows per thread, sliding), and a register
-// ring of the last 2R+1 column-pass results per output; once it is full each
-// new slice emits one output slice.
+// arrives in a 4-stage cp.async ring in shared memory, the row pass goes into
+// a second smem tile, the column pass into registers (4 consecutive rows per
+// thread), and a register ring keeps the last 2R+1 column-pass results per
+// output; once it is full each new slice emits one output slice.
 #include <algorithm>
 
 #include "common.cuh"
@@ -54,11 +54,17 @@ __global__ void __launch_bounds__(256) sep3d_naive(Sep3Params p) {
 
 constexpr int k3TW = 64, k3TH = 16, k3NT = 256;
 
+// Input slices stream through an NS-stage ring of shared-memory tiles filled by
+// 4-byte cp.async (per-element source address: clamped for the clamp boundary,
+// zero-fill for a constant-0 boundary), so NS-1 slices of loads are in flight
+// while a slice is convolved; two barriers per slice.  Constant boundaries with
+// c != 0 take the synchronous loader (async = false).
 template <int R>
-__global__ void __launch_bounds__(k3NT) sep3d_tile(Sep3Params p, int zchunk) {
+__global__ void __launch_bounds__(k3NT, 2) sep3d_tile(Sep3Params p, int zchunk, int async) {
   constexpr int K = 2 * R + 1;
   constexpr int IW = k3TW + 2 * R, IH = k3TH + 2 * R;
-  __shared__ float sin_[IH][IW];
+  constexpr int NS = 4;
+  __shared__ float sin_[NS][IH][IW];
   __shared__ float st[IH][k3TW];
   const int tid = threadIdx.x;
   const int x0 = blockIdx.x * k3TW, y0 = blockIdx.y * k3TH;
@@ -70,62 +76,84 @@ __global__ void __launch_bounds__(k3NT) sep3d_tile(Sep3Params p, int zchunk) {
   for (int k = 0; k < K; ++k)
 #pragma unroll
     for (int q = 0; q < 4; ++q) ring[k][q] = 0.0f;
-  const bool interior_xy = x0 - R >= 0 && x0 + k3TW + R <= p.W && y0 - R >= 0 && y0 + k3TH + R <= p.H;
+  const bool clampb = p.border == kBorderClamp;
 
-  // input slices are fetched into registers one slice ahead (the global loads of slice zz+1
-  // are in flight while slice zz is convolved), then stored to shared memory
+  // The loader's element list is slice-invariant: precompute each element's slice-relative
+  // source byte offset (clamped columns / rows for the clamp boundary) and whether it lies
+  // outside the image (zero-fill for a constant-0 boundary).
   constexpr int NPRE = (IH * IW + k3NT - 1) / k3NT;
-  float pre[NPRE];
-  auto fetch = [&](int zz) {
+  int soff[NPRE];
+  unsigned outm = 0;  // bit e: element e outside the image in x or y
+#pragma unroll
+  for (int e = 0; e < NPRE; ++e) {
+    const int idx = tid + e * k3NT;
+    const int r = idx / IW, c = idx - r * IW;
+    const int xx = x0 - R + c, yy = y0 - R + r;
+    if (xx < 0 || xx >= p.W || yy < 0 || yy >= p.H) outm |= 1u << e;
+    soff[e] = (int)(clampi(yy, 0, p.H - 1) * p.spitch + 4 * clampi(xx, 0, p.W - 1));
+  }
+  // issue the loads of input slice zz into stage s
+  auto issue = [&](int zz, int s) {
     const bool zout = zz < 0 || zz >= p.D;
     const int zs = clampi(zz, 0, p.D - 1);
     const char* sl = p.src + (int64_t)zs * p.sslice;
+    float* dst = &sin_[s][0][0];
 #pragma unroll
     for (int e = 0; e < NPRE; ++e) {
       const int idx = tid + e * k3NT;
       if (idx < IH * IW) {
-        const int r = idx / IW, c = idx - r * IW;
-        if (zout && p.border == kBorderConstant) pre[e] = p.cval;  // constant slice
-        else if (interior_xy)
-          pre[e] = __ldg(reinterpret_cast<const float*>(sl + (int64_t)(y0 - R + r) * p.spitch) + (x0 - R + c));
-        else pre[e] = read_B3(p, x0 - R + c, y0 - R + r, zs);
+        if (async) {
+          const bool zero = !clampb && (zout || ((outm >> e) & 1u));  // constant 0: zero-fill
+          cp_async4(dst + idx, sl + (zero ? 0 : soff[e]), zero ? 0 : 4);
+        } else {
+          const int r = idx / IW, c = idx - r * IW;
+          dst[idx] = (zout && !clampb) ? p.cval : read_B3(p, x0 - R + c, y0 - R + r, zs);
+        }
       }
     }
   };
-  fetch(z0 - R);
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) {
+    if (z0 - R + s < z1 + R) issue(z0 - R + s, s);
+    cp_async_commit();
+  }
 #pragma unroll 1
   for (int zz = z0 - R; zz < z1 + R; ++zz) {
-#pragma unroll
-    for (int e = 0; e < NPRE; ++e) {
-      const int idx = tid + e * k3NT;
-      if (idx < IH * IW) (&sin_[0][0])[idx] = pre[e];
-    }
-    __syncthreads();
-    if (zz + 1 < z1 + R) fetch(zz + 1);
+    const int s = (zz - (z0 - R)) % NS;
+    cp_async_wait<NS - 2>();
+    __syncthreads();  // slice zz landed; the previous slice's st reads are done
+    if (zz + NS - 1 < z1 + R) issue(zz + NS - 1, (s + NS - 1) % NS);
+    cp_async_commit();
     // row pass: t(x, y') for the tile's columns and its 16 + 2R rows
-    for (int e = tid; e < IH * k3TW; e += k3NT) {
-      const int r = e / k3TW, c = e - r * k3TW;
-      float t = 0.0f;
+    for (int e = tid; e < IH * (k3TW / 4); e += k3NT) {  // item = 4 consecutive columns of one row
+      const int r = e / (k3TW / 4), c = 4 * (e - r * (k3TW / 4));
+      float v[4 + 2 * R];
 #pragma unroll
-      for (int i = 0; i < K; ++i) t = __fmaf_rn(p.fx[i], sin_[r][c + i], t);
-      st[r][c] = t;
+      for (int m = 0; m < 4 + 2 * R; ++m) v[m] = sin_[s][r][c + m];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float tq = 0.0f;
+#pragma unroll
+        for (int i = 0; i < K; ++i) tq = __fmaf_rn(p.fx[i], v[q + i], tq);
+        st[r][c + q] = tq;
+      }
     }
     __syncthreads();
     // column pass for 4 consecutive rows; slide the z ring
-    float s[4];
+    float sc[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       float a = 0.0f;
 #pragma unroll
       for (int j = 0; j < K; ++j) a = __fmaf_rn(p.gy[j], st[ty + q + j][tx], a);
-      s[q] = a;
+      sc[q] = a;
     }
 #pragma unroll
     for (int k = 0; k + 1 < K; ++k)
 #pragma unroll
       for (int q = 0; q < 4; ++q) ring[k][q] = ring[k + 1][q];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) ring[K - 1][q] = s[q];
+    for (int q = 0; q < 4; ++q) ring[K - 1][q] = sc[q];
     const int z = zz - R;  // output slice completed by input slice zz
     if (z >= z0 && x < p.W) {
       float* drow = reinterpret_cast<float*>(p.dst + (int64_t)z * p.dslice);
@@ -140,8 +168,8 @@ __global__ void __launch_bounds__(k3NT) sep3d_tile(Sep3Params p, int zchunk) {
         }
       }
     }
-    __syncthreads();  // smem tiles are rewritten by the next slice
   }
+  cp_async_wait<0>();
 }
 
 bool sep3d_tile_supported(int R) { return R >= 0 && R <= 7; }
@@ -175,10 +203,11 @@ cudaError_t launch_sep3d(const Sep3Params& p0, int variant, cudaStream_t s) {
   zchunk = std::max(zchunk, std::max(8, 8 * R));
   const int zb = (p.D + zchunk - 1) / zchunk;
   if (zb > 65535) return cudaErrorInvalidValue;
+  const int async = (p.border == kBorderClamp || p.cval == 0.0f) ? 1 : 0;
   dim3 grd((p.W + k3TW - 1) / k3TW, (p.H + k3TH - 1) / k3TH, zb);
   switch (R) {
 #define ICL_S3(RR) \
-  case RR: sep3d_tile<RR><<<grd, k3NT, 0, s>>>(p, zchunk); break;
+  case RR: sep3d_tile<RR><<<grd, k3NT, 0, s>>>(p, zchunk, async); break;
     ICL_S3(0) ICL_S3(1) ICL_S3(2) ICL_S3(3) ICL_S3(4) ICL_S3(5) ICL_S3(6) ICL_S3(7)
 #undef ICL_S3
     default: return cudaErrorInvalidValue;
