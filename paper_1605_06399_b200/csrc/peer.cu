@@ -241,7 +241,8 @@ icl_status icl_sepconv_peer(const icl_image* own, const icl_image* dst, int64_t 
     p.out_y1 = (int)a1;
     dim3 grd((unsigned)((own->width + kEdgeTW - 1) / kEdgeTW), (unsigned)((a1 - a0 + kEdgeCH - 1) / kEdgeCH),
              (unsigned)own->batch);
-    cudaFuncSetAttribute(sep_edge_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e0 = cudaFuncSetAttribute(sep_edge_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e0 != cudaSuccess) return report_error(ICL_ERR_CUDA, cudaGetErrorString(e0));
     sep_edge_peer<<<grd, kEdgeTW, smem, s>>>(p);
     count_launch();
     cudaError_t e = cudaGetLastError();

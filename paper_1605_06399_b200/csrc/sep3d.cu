@@ -191,13 +191,9 @@ cudaError_t launch_sep3d(const Sep3Params& p0, int variant, cudaStream_t s) {
   for (int i = 0; i < 15; ++i) { p.fx[i] = f[i]; p.gy[i] = g[i]; p.hz[i] = h[i]; }
   // z chunk: enough CTAs for ~4 per SM (2 resident at 256 threads x ~120 registers), but at
   // least 8R slices so the 2R recomputed halo slices stay <= 25% of a chunk
-  static int nsm = 0;
-  if (!nsm) {
-    int d = 0;
-    cudaGetDevice(&d);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, d);
-    if (nsm < 1) nsm = 148;
-  }
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm < 1) nsm = 148;
   const int64_t tiles = (int64_t)((p.W + k3TW - 1) / k3TW) * ((p.H + k3TH - 1) / k3TH);
   int zchunk = (int)std::min<int64_t>(64, std::max<int64_t>(1, (int64_t)p.D * tiles / (4 * nsm)));
   zchunk = std::max(zchunk, std::max(8, 8 * R));
