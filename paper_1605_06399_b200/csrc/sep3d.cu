@@ -62,9 +62,11 @@ constexpr int k3TW = 64, k3TH = 16, k3NT = 256;
 template <int R>
 __global__ void __launch_bounds__(k3NT, 2) sep3d_tile(Sep3Params p, int zchunk, int async) {
   constexpr int K = 2 * R + 1;
+  constexpr int HA = 4 * ((R + 3) / 4);           // 16-byte aligned halo >= R
   constexpr int IW = k3TW + 2 * R, IH = k3TH + 2 * R;
+  constexpr int IWS = k3TW + 2 * HA;              // smem row: columns x0-HA .. x0+64+HA
   constexpr int NS = 4;
-  __shared__ float sin_[NS][IH][IW];
+  __shared__ __align__(16) float sin_[NS][IH][IWS];
   __shared__ float st[IH][k3TW];
   const int tid = threadIdx.x;
   const int x0 = blockIdx.x * k3TW, y0 = blockIdx.y * k3TH;
@@ -77,37 +79,64 @@ __global__ void __launch_bounds__(k3NT, 2) sep3d_tile(Sep3Params p, int zchunk, 
 #pragma unroll
     for (int q = 0; q < 4; ++q) ring[k][q] = 0.0f;
   const bool clampb = p.border == kBorderClamp;
+  // interior tile with 16-byte aligned rows: whole-row 16-byte copies of the aligned superset
+  const bool vec16 = async && x0 - HA >= 0 && x0 + k3TW + HA <= p.W && y0 - R >= 0 && y0 + k3TH + R <= p.H &&
+                     ((p.spitch | p.sslice | (int64_t)p.src) & 15) == 0;
 
   // The loader's element list is slice-invariant: precompute each element's slice-relative
   // source byte offset (clamped columns / rows for the clamp boundary) and whether it lies
   // outside the image (zero-fill for a constant-0 boundary).
-  constexpr int NPRE = (IH * IW + k3NT - 1) / k3NT;
-  int soff[NPRE];
+  constexpr int NV = IH * (IWS / 4);                  // 16-byte chunks per slice (vec16)
+  constexpr int NPRE = (IH * IW + k3NT - 1) / k3NT;   // elements per thread (4-byte path)
+  constexpr int NPRE16 = (NV + k3NT - 1) / k3NT;
+  int soff[NPRE > NPRE16 ? NPRE : NPRE16];
   unsigned outm = 0;  // bit e: element e outside the image in x or y
+  if (vec16) {
 #pragma unroll
-  for (int e = 0; e < NPRE; ++e) {
-    const int idx = tid + e * k3NT;
-    const int r = idx / IW, c = idx - r * IW;
-    const int xx = x0 - R + c, yy = y0 - R + r;
-    if (xx < 0 || xx >= p.W || yy < 0 || yy >= p.H) outm |= 1u << e;
-    soff[e] = (int)(clampi(yy, 0, p.H - 1) * p.spitch + 4 * clampi(xx, 0, p.W - 1));
+    for (int e = 0; e < NPRE16; ++e) {
+      const int idx = tid + e * k3NT;
+      const int r = idx / (IWS / 4), c4 = idx - r * (IWS / 4);
+      soff[e] = (int)((y0 - R + r) * p.spitch + 4 * (x0 - HA + 4 * c4));
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < NPRE; ++e) {
+      const int idx = tid + e * k3NT;
+      const int r = idx / IW, c = idx - r * IW;
+      const int xx = x0 - R + c, yy = y0 - R + r;
+      if (xx < 0 || xx >= p.W || yy < 0 || yy >= p.H) outm |= 1u << e;
+      soff[e] = (int)(clampi(yy, 0, p.H - 1) * p.spitch + 4 * clampi(xx, 0, p.W - 1));
+    }
   }
-  // issue the loads of input slice zz into stage s
+  // issue the loads of input slice zz into stage s (element (r, c) of the R-halo tile lives at
+  // smem column HA - R + c)
   auto issue = [&](int zz, int s) {
     const bool zout = zz < 0 || zz >= p.D;
     const int zs = clampi(zz, 0, p.D - 1);
     const char* sl = p.src + (int64_t)zs * p.sslice;
     float* dst = &sin_[s][0][0];
+    if (vec16) {
+#pragma unroll
+      for (int e = 0; e < NPRE16; ++e) {
+        const int idx = tid + e * k3NT;
+        if (idx < NV) {
+          const bool zero = !clampb && zout;
+          cp_async16(dst + 4 * idx, sl + (zero ? 0 : soff[e]), zero ? 0 : 16);
+        }
+      }
+      return;
+    }
 #pragma unroll
     for (int e = 0; e < NPRE; ++e) {
       const int idx = tid + e * k3NT;
       if (idx < IH * IW) {
+        const int r = idx / IW, c = idx - r * IW;
+        float* d = dst + r * IWS + (HA - R) + c;
         if (async) {
           const bool zero = !clampb && (zout || ((outm >> e) & 1u));  // constant 0: zero-fill
-          cp_async4(dst + idx, sl + (zero ? 0 : soff[e]), zero ? 0 : 4);
+          cp_async4(d, sl + (zero ? 0 : soff[e]), zero ? 0 : 4);
         } else {
-          const int r = idx / IW, c = idx - r * IW;
-          dst[idx] = (zout && !clampb) ? p.cval : read_B3(p, x0 - R + c, y0 - R + r, zs);
+          *d = (zout && !clampb) ? p.cval : read_B3(p, x0 - R + c, y0 - R + r, zs);
         }
       }
     }
@@ -129,7 +158,7 @@ __global__ void __launch_bounds__(k3NT, 2) sep3d_tile(Sep3Params p, int zchunk, 
       const int r = e / (k3TW / 4), c = 4 * (e - r * (k3TW / 4));
       float v[4 + 2 * R];
 #pragma unroll
-      for (int m = 0; m < 4 + 2 * R; ++m) v[m] = sin_[s][r][c + m];
+      for (int m = 0; m < 4 + 2 * R; ++m) v[m] = sin_[s][r][(HA - R) + c + m];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         float tq = 0.0f;
