@@ -91,3 +91,41 @@ def test_cpu_tensors_need_a_cuda_device():
         icl.sepconv(t, t.clone(), [1.0], [1.0])
     with pytest.raises(ValueError, match="CUDA"):
         icl.fill_uniform(t, 1)
+
+
+def test_new_entry_points_validate_on_the_host():
+    """icl_sepconv3d / icl_blur_harris / icl_sepconv_peer / icl_halo_pull / icl_tune_ann reject
+    bad arguments before touching a device."""
+    lib = icl.load_library()
+    P = ctypes.c_void_p
+    taps = (ctypes.c_float * 17)(*([0.1] * 17))
+    tp = ctypes.cast(taps, P)
+    src = icl.icl_image(4096, 16, 16, 64, 4, 16 * 64)
+    dst = icl.icl_image(1 << 20, 16, 16, 64, 4, 16 * 64)
+    # 3-D: radius 8 -> unsupported; shape mismatch / overlap / null
+    assert lib.icl_sepconv3d(ctypes.byref(src), ctypes.byref(dst), tp, 8, tp, 1, tp, 1, 0, 0.0, None) == 3
+    bad = icl.icl_image(1 << 20, 16, 16, 64, 5, 16 * 64)
+    assert lib.icl_sepconv3d(ctypes.byref(src), ctypes.byref(bad), tp, 1, tp, 1, tp, 1, 0, 0.0, None) == 1
+    ov = icl.icl_image(4096 + 64, 16, 16, 64, 4, 16 * 64)
+    assert lib.icl_sepconv3d(ctypes.byref(src), ctypes.byref(ov), tp, 1, tp, 1, tp, 1, 0, 0.0, None) == 2
+    nul = icl.icl_image(0, 16, 16, 64, 4, 16 * 64)
+    assert lib.icl_sepconv3d(ctypes.byref(nul), ctypes.byref(dst), tp, 1, tp, 1, tp, 1, 0, 0.0, None) == 1
+    # chain: blur radius 4 and Harris block 6 are unsupported
+    one = icl.icl_image(4096, 16, 16, 64, 1, 0)
+    two = icl.icl_image(1 << 20, 16, 16, 64, 1, 0)
+    st = lib.icl_blur_harris(ctypes.byref(one), ctypes.byref(two), tp, 4, tp, 1, 0, 0.0, 5, 0.04, 1, 0.0, None, 0.0,
+                             None, None, 0, None)
+    assert st == 3
+    st = lib.icl_blur_harris(ctypes.byref(one), ctypes.byref(two), tp, 1, tp, 1, 0, 0.0, 6, 0.04, 1, 0.0, None, 0.0,
+                             None, None, 0, None)
+    assert st == 3
+    # peer: a band with rows above but no up neighbour; halo pull with a bad element size
+    band = icl.icl_image(4096, 16, 8, 64, 1, 0)
+    out = icl.icl_image(1 << 20, 16, 8, 64, 1, 0)
+    st = lib.icl_sepconv_peer(ctypes.byref(band), ctypes.byref(out), 16, 8, None, None, tp, 1, tp, 1, 0, 0.0, None)
+    assert st == 1 and b"neighbour" in lib.icl_last_error()
+    assert lib.icl_halo_pull(ctypes.byref(band), 16, 0, 0, 8, None, None, 2, None) == 1
+    # model-guided tuning: n1 < 1
+    prob = icl.icl_problem()
+    assert lib.icl_tune_ann(ctypes.byref(prob), 0, 1, 0, None, None) == 1
+    assert icl.variant_names("sepconv3d") == ["naive_direct", "tile64x16"]
