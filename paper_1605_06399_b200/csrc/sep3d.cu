@@ -52,35 +52,43 @@ __global__ void __launch_bounds__(256) sep3d_naive(Sep3Params p) {
   }
 }
 
-constexpr int k3TW = 64, k3TH = 16, k3NT = 256;
+constexpr int k3TW = 64, k3NT = 256;
 
 // Input slices stream through an NS-stage ring of shared-memory tiles filled by
 // 4-byte cp.async (per-element source address: clamped for the clamp boundary,
 // zero-fill for a constant-0 boundary), so NS-1 slices of loads are in flight
 // while a slice is convolved; two barriers per slice.  Constant boundaries with
 // c != 0 take the synchronous loader (async = false).
+// Tile height per radius: 32 rows (8 per thread) with a 3-stage slice ring for R <= 3 (halves
+// the y halo and the barriers per voxel), 16 rows with 4 stages above (static smem < 48 KB).
+template <int R>
+struct Sep3Geom {
+  static constexpr int TH = R <= 3 ? 32 : 16;
+  static constexpr int NS = R <= 3 ? 3 : 4;
+};
+
 template <int R>
 __global__ void __launch_bounds__(k3NT, 2) sep3d_tile(Sep3Params p, int zchunk, int async) {
   constexpr int K = 2 * R + 1;
+  constexpr int TH = Sep3Geom<R>::TH, RPT = TH / 4, NS = Sep3Geom<R>::NS;  // rows per thread
   constexpr int HA = 4 * ((R + 3) / 4);           // 16-byte aligned halo >= R
-  constexpr int IW = k3TW + 2 * R, IH = k3TH + 2 * R;
+  constexpr int IW = k3TW + 2 * R, IH = TH + 2 * R;
   constexpr int IWS = k3TW + 2 * HA;              // smem row: columns x0-HA .. x0+64+HA
-  constexpr int NS = 4;
   __shared__ __align__(16) float sin_[NS][IH][IWS];
   __shared__ float st[IH][k3TW];
   const int tid = threadIdx.x;
-  const int x0 = blockIdx.x * k3TW, y0 = blockIdx.y * k3TH;
+  const int x0 = blockIdx.x * k3TW, y0 = blockIdx.y * TH;
   const int z0 = blockIdx.z * zchunk, z1 = min(z0 + zchunk, p.D);
-  const int tx = tid & (k3TW - 1), ty = (tid / k3TW) * 4;  // outputs (x0+tx, y0+ty .. +3)
+  const int tx = tid & (k3TW - 1), ty = (tid / k3TW) * RPT;  // outputs (x0+tx, y0+ty .. +RPT-1)
   const int x = x0 + tx;
-  float ring[K][4];
+  float ring[K][RPT];
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) ring[k][q] = 0.0f;
+    for (int q = 0; q < RPT; ++q) ring[k][q] = 0.0f;
   const bool clampb = p.border == kBorderClamp;
   // interior tile with 16-byte aligned rows: whole-row 16-byte copies of the aligned superset
-  const bool vec16 = async && x0 - HA >= 0 && x0 + k3TW + HA <= p.W && y0 - R >= 0 && y0 + k3TH + R <= p.H &&
+  const bool vec16 = async && x0 - HA >= 0 && x0 + k3TW + HA <= p.W && y0 - R >= 0 && y0 + TH + R <= p.H &&
                      ((p.spitch | p.sslice | (int64_t)p.src) & 15) == 0;
 
   // The loader's element list is slice-invariant: precompute each element's slice-relative
@@ -153,7 +161,7 @@ __global__ void __launch_bounds__(k3NT, 2) sep3d_tile(Sep3Params p, int zchunk, 
     __syncthreads();  // slice zz landed; the previous slice's st reads are done
     if (zz + NS - 1 < z1 + R) issue(zz + NS - 1, (s + NS - 1) % NS);
     cp_async_commit();
-    // row pass: t(x, y') for the tile's columns and its 16 + 2R rows
+    // row pass: t(x, y') for the tile's columns and its TH + 2R rows
     for (int e = tid; e < IH * (k3TW / 4); e += k3NT) {  // item = 4 consecutive columns of one row
       const int r = e / (k3TW / 4), c = 4 * (e - r * (k3TW / 4));
       float v[4 + 2 * R];
@@ -168,10 +176,10 @@ __global__ void __launch_bounds__(k3NT, 2) sep3d_tile(Sep3Params p, int zchunk, 
       }
     }
     __syncthreads();
-    // column pass for 4 consecutive rows; slide the z ring
-    float sc[4];
+    // column pass for RPT consecutive rows; slide the z ring
+    float sc[RPT];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < RPT; ++q) {
       float a = 0.0f;
 #pragma unroll
       for (int j = 0; j < K; ++j) a = __fmaf_rn(p.gy[j], st[ty + q + j][tx], a);
@@ -180,14 +188,14 @@ __global__ void __launch_bounds__(k3NT, 2) sep3d_tile(Sep3Params p, int zchunk, 
 #pragma unroll
     for (int k = 0; k + 1 < K; ++k)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) ring[k][q] = ring[k + 1][q];
+      for (int q = 0; q < RPT; ++q) ring[k][q] = ring[k + 1][q];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) ring[K - 1][q] = sc[q];
+    for (int q = 0; q < RPT; ++q) ring[K - 1][q] = sc[q];
     const int z = zz - R;  // output slice completed by input slice zz
     if (z >= z0 && x < p.W) {
       float* drow = reinterpret_cast<float*>(p.dst + (int64_t)z * p.dslice);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < RPT; ++q) {
         const int y = y0 + ty + q;
         if (y < p.H) {
           float o = 0.0f;
@@ -223,13 +231,14 @@ cudaError_t launch_sep3d(const Sep3Params& p0, int variant, cudaStream_t s) {
   int dev = 0, nsm = 0;
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm < 1) nsm = 148;
-  const int64_t tiles = (int64_t)((p.W + k3TW - 1) / k3TW) * ((p.H + k3TH - 1) / k3TH);
+  const int th = R <= 3 ? 32 : 16;  // Sep3Geom<R>::TH
+  const int64_t tiles = (int64_t)((p.W + k3TW - 1) / k3TW) * ((p.H + th - 1) / th);
   int zchunk = (int)std::min<int64_t>(64, std::max<int64_t>(1, (int64_t)p.D * tiles / (4 * nsm)));
   zchunk = std::max(zchunk, std::max(8, 8 * R));
   const int zb = (p.D + zchunk - 1) / zchunk;
   if (zb > 65535) return cudaErrorInvalidValue;
   const int async = (p.border == kBorderClamp || p.cval == 0.0f) ? 1 : 0;
-  dim3 grd((p.W + k3TW - 1) / k3TW, (p.H + k3TH - 1) / k3TH, zb);
+  dim3 grd((p.W + k3TW - 1) / k3TW, (p.H + th - 1) / th, zb);
   switch (R) {
 #define ICL_S3(RR) \
   case RR: sep3d_tile<RR><<<grd, k3NT, 0, s>>>(p, zchunk, async); break;
