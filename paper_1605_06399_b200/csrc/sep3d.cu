@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(k3NT, 2) sep3d_tile(Sep3Params p, int zchunk, 
   constexpr int IW = k3TW + 2 * R, IH = TH + 2 * R;
   constexpr int IWS = k3TW + 2 * HA;              // smem row: columns x0-HA .. x0+64+HA
   __shared__ __align__(16) float sin_[NS][IH][IWS];
-  __shared__ float st[IH][k3TW];
+  __shared__ __align__(16) float st[IH][k3TW];
   const int tid = threadIdx.x;
   const int x0 = blockIdx.x * k3TW, y0 = blockIdx.y * TH;
   const int z0 = blockIdx.z * zchunk, z1 = min(z0 + zchunk, p.D);
@@ -164,16 +164,22 @@ __global__ void __launch_bounds__(k3NT, 2) sep3d_tile(Sep3Params p, int zchunk, 
     // row pass: t(x, y') for the tile's columns and its TH + 2R rows
     for (int e = tid; e < IH * (k3TW / 4); e += k3NT) {  // item = 4 consecutive columns of one row
       const int r = e / (k3TW / 4), c = 4 * (e - r * (k3TW / 4));
-      float v[4 + 2 * R];
+      // smem columns c .. c+4+2HA-1 as aligned LDS.128 (lanes 16 bytes apart: conflict-free)
+      float v[4 + 2 * HA];
 #pragma unroll
-      for (int m = 0; m < 4 + 2 * R; ++m) v[m] = sin_[s][r][(HA - R) + c + m];
+      for (int m4 = 0; m4 < (4 + 2 * HA) / 4; ++m4) {
+        const float4 w4 = *reinterpret_cast<const float4*>(&sin_[s][r][c + 4 * m4]);
+        v[4 * m4] = w4.x; v[4 * m4 + 1] = w4.y; v[4 * m4 + 2] = w4.z; v[4 * m4 + 3] = w4.w;
+      }
+      float tq[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        float tq = 0.0f;
+        float acc = 0.0f;
 #pragma unroll
-        for (int i = 0; i < K; ++i) tq = __fmaf_rn(p.fx[i], v[q + i], tq);
-        st[r][c + q] = tq;
+        for (int i = 0; i < K; ++i) acc = __fmaf_rn(p.fx[i], v[(HA - R) + q + i], acc);
+        tq[q] = acc;
       }
+      *reinterpret_cast<float4*>(&st[r][c]) = make_float4(tq[0], tq[1], tq[2], tq[3]);
     }
     __syncthreads();
     // column pass for RPT consecutive rows; slide the z ring
