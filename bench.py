@@ -2,7 +2,7 @@
 """bench.py -- megapixels/s of the ImageCL hot path on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl icl|reference]
-                    [--workload suite|sepconv16k|conv2d8k] [--batch B] [--size S] [--radius R]
+                    [--workload suite|sepconv16k|conv2d8k|sep3d] [--batch B] [--size S] [--radius R]
 
 Default workload ("suite", BASELINE.json configs[4] per GPU): every rank
 processes its own batch of B (default 8) synthetic 4096x4096 fp32 images
@@ -779,13 +779,126 @@ def run_conv2d(args):
     return 0
 
 
+def run_sep3d(args):
+    """SURVEY.md §8(f) row 4 (3-D Images; R26): separable convolution
+    of a 128 x 512 x 512 fp32 volume per rank (weak scaling), radius r on every axis, clamp.
+    Two input/output volume pairs alternate (4 x 134 MB > L2).  e2e: pinned host volume in,
+    the call, result out (explicit copies around icl_sepconv3d, which takes device volumes)."""
+    import numpy as np
+    import torch
+
+    import paper_1605_06399_b200 as icl
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = init_dist(ws, "nccl")
+    icl.load_library()
+    D, S, r = args.depth, args.size, args.radius
+    f = synth.gaussian_taps(r)
+    vols = [torch.empty(D, S, S, device=dev) for _ in range(2)]
+    for k, v in enumerate(vols):
+        icl.fill_uniform(v, 5000 + 100 * rank + 10 * k)  # slice z = synth.uniform_image(seed + z, S, S)
+    outs = [torch.empty_like(v) for v in vols]
+    stream = torch.cuda.current_stream(dev)
+
+    def step(k):
+        icl.sepconv3d(vols[k & 1], outs[k & 1], f, f, f, "clamp", stream=stream)
+
+    for k in range(max(3, args.warmup)):
+        step(k)
+    torch.cuda.synchronize(dev)
+    variant = icl.variant_names("sepconv3d")[icl.last_variant("sepconv3d")]
+    if ws > 1:
+        dist.barrier()
+    n0 = icl.launch_count()
+    with ClockSampler(local) as clk:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for k in range(args.steps):
+            step(k)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+    launches = icl.launch_count() - n0
+    if ws > 1:
+        dist.barrier()
+    step_ms = max_over_ranks(a.elapsed_time(b) / args.steps, ws, dev)
+    nvox = D * S * S
+    value = ws * nvox / (step_ms * 1e-3) / 1e6
+    hbm, hbm_kind = measured_peaks()
+    gbs = 8 * nvox / (step_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "traffic": None,
+            "peak_kind": hbm_kind, "bytes_per_voxel": 8, "flop_per_voxel": 6 * (2 * r + 1)}
+    e2e = None
+    if not args.no_e2e:
+        hin = vols[0].cpu().pin_memory()
+        hout = torch.empty(D, S, S).pin_memory()
+        din, dout = torch.empty_like(vols[0]), torch.empty_like(vols[0])
+        ke = max(1, min(args.steps, 5))
+
+        def e2e_step():
+            din.copy_(hin, non_blocking=True)
+            icl.sepconv3d(din, dout, f, f, f, "clamp", stream=stream)
+            hout.copy_(dout, non_blocking=True)
+
+        e2e_step()
+        stream.synchronize()
+        if ws > 1:
+            dist.barrier()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        for _ in range(ke):
+            e2e_step()
+        eb.record(stream)
+        stream.synchronize()
+        e_ms = max_over_ranks(ea.elapsed_time(eb) / ke, ws, dev)
+        ok = bool(torch.equal(hout[:, ::61, ::67], outs[0].cpu()[:, ::61, ::67]))
+        e2e = {"value": ws * nvox / (e_ms * 1e-3) / 1e6, "unit": "Mvoxel/s", "h2d_bytes_per_step": 4 * nvox,
+               "d2h_bytes_per_step": 4 * nvox, "ms_per_step": e_ms, "steps": ke,
+               "path": "pinned host volume -> icl_sepconv3d -> pinned host volume (copies on the call's stream)",
+               "matches_device_outputs": ok}
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        import oracle
+        rng = np.random.default_rng(0)
+        # the oracle's input is regenerated on the host from the same seeds (never read back from the GPU)
+        host = np.stack([synth.uniform_image(5000 + 100 * rank + z, S, S) for z in range(D)])
+        npts = 500_000
+        while True:  # grow the random sample until it takes >= 2 s (bounded by the volume)
+            xs, ys, zs = rng.integers(0, S, npts), rng.integers(0, S, npts), rng.integers(0, D, npts)
+            t0 = time.perf_counter()
+            oracle.sepconv3d(host, f, f, f, "clamp", points=(xs, ys, zs))
+            dt = time.perf_counter() - t0
+            if dt >= 2.0 or npts >= nvox:
+                break
+            npts = min(nvox, npts * 4)
+        cpu = {"value": npts / dt / 1e6, "unit": "Mvoxel/s", "cores": oracle.default_threads(), "kind": "oracle",
+               "cpu_model": cpu_model(),
+               "sample": f"{npts} random voxels of one {D}x{S}x{S} volume (f64 oracle, {dt:.1f} s)"}
+    if rank == 0:
+        line = {
+            "metric": f"sepconv3d megavoxels/s ({D}x{S}x{S} fp32, radius {r} on every axis, clamp)",
+            "value": value, "unit": "Mvoxel/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "sep3d (PAPER.md:303-304 3-D Images; SURVEY.md §8(f) row 4)",
+                       "size": [D, S, S], "radius": r, "border": "clamp", "variant": variant,
+                       "l2": "two input/output volume pairs alternate (4 x 134 MB > L2)"},
+            "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="icl", choices=["icl", "reference"])
-    ap.add_argument("--workload", default="suite", choices=["suite", "sepconv16k", "conv2d8k"])
+    ap.add_argument("--workload", default="suite", choices=["suite", "sepconv16k", "conv2d8k", "sep3d"])
+    ap.add_argument("--depth", type=int, default=128, help="sep3d: volume depth (slices)")
     ap.add_argument("--radius", type=int, default=2)
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--size", type=int, default=4096)
@@ -810,6 +923,10 @@ def main():
         if args.size == 4096:
             args.size = 16384
         return run_sepconv_bands(args)
+    if args.workload == "sep3d":
+        if args.size == 4096:
+            args.size = 512
+        return run_sep3d(args)
     return run_suite(args)
 
 
