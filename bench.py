@@ -2,7 +2,7 @@
 """bench.py -- megapixels/s of the ImageCL hot path on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl icl|reference]
-                    [--workload suite|sepconv16k|conv2d8k|sep3d] [--batch B] [--size S] [--radius R]
+                    [--workload suite|sepconv16k|conv2d8k|sep3d|chain] [--batch B] [--size S] [--radius R]
 
 Default workload ("suite", BASELINE.json configs[4] per GPU): every rank
 processes its own batch of B (default 8) synthetic 4096x4096 fp32 images
@@ -891,13 +891,103 @@ def run_sep3d(args):
     return 0
 
 
+def run_chain(args):
+    """SURVEY.md §8(f) row 4 (FAST-style filter chains; R24): Gaussian
+    smoothing (radius r) then Harris B = 5 + mask on the suite's 8 x 4096^2 batch per rank, through
+    icl_blur_harris -- the two-pass schedule (caller workspace) is timed as the value, the fused
+    one-pass kernel beside it.  Inputs 512 MB > L2 (no flush)."""
+    import numpy as np
+    import torch
+
+    import paper_1605_06399_b200 as icl
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = init_dist(ws, "nccl")
+    icl.load_library()
+    B, S, r = args.batch, args.size, args.radius
+    f = synth.gaussian_taps(r)
+    src = torch.empty(B, S, S, device=dev)
+    icl.fill_uniform(src, 7000 + 100 * rank)
+    R = torch.empty_like(src)
+    mask = torch.empty(B, S, S, dtype=torch.uint8, device=dev)
+    wsb = torch.empty(icl.blur_harris_workspace_bytes(S, S, B, 5) // 4 + 4, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn, steps):
+        for _ in range(max(3, args.warmup)):
+            fn()
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        return max_over_ranks(a.elapsed_time(b) / steps, ws, dev)
+
+    def two_pass():
+        icl.blur_harris(src, R, f, f, "constant", 0.0, 5, 0.04, "clamp", mask=mask, threshold=1.0, workspace=wsb,
+                        stream=stream)
+
+    def fused():
+        icl.blur_harris(src, R, f, f, "constant", 0.0, 5, 0.04, "clamp", mask=mask, threshold=1.0, stream=stream)
+
+    n0 = icl.launch_count()
+    with ClockSampler(local) as clk:
+        step_ms = timed(two_pass, args.steps)
+    launches = (icl.launch_count() - n0) // (args.steps + max(3, args.warmup)) * args.steps
+    fused_ms = timed(fused, args.steps)
+    R2 = R.clone()
+    two_pass()
+    torch.cuda.synchronize(dev)
+    same = bool(torch.equal(R, R2))
+    px = B * S * S
+    value = ws * px / (step_ms * 1e-3) / 1e6
+    hbm, hbm_kind = measured_peaks()
+    # algorithmic bytes of the chain: read 4 + response 4 + mask 1 (the intermediate is not algorithmic)
+    gbs = 9 * px / (step_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "traffic": None,
+            "peak_kind": hbm_kind, "bytes_per_px": 9,
+            "note": "two-pass schedule moves 8 + 9 B/px (intermediate through HBM); fused moves 9"}
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        import oracle
+        n = 2048
+        img = synth.uniform_image(7000, n, n)
+        t0 = time.perf_counter()
+        oracle.harris(oracle.sepconv(img, f, f, "constant").astype(np.float32), 5, 0.04, "clamp")
+        dt = time.perf_counter() - t0
+        cpu = {"value": n * n / dt / 1e6, "unit": "Mpx/s", "cores": oracle.default_threads(), "kind": "oracle",
+               "cpu_model": cpu_model(),
+               "sample": f"one {n}x{n} image through oracle sepconv then Harris ({dt:.2f} s)"}
+    if rank == 0:
+        line = {
+            "metric": f"blur r{r} + Harris B5 megapixels/s (icl_blur_harris, {B} x {S}x{S} fp32)",
+            "value": value, "unit": "Mpx/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "chain (FAST-style pipeline, PAPER.md:128-142; SURVEY.md §8(f) row 4)",
+                       "images_per_gpu": B, "size": [S, S], "radius": r, "schedule": "two-pass (workspace)",
+                       "l2": "input 512 MB > L2; no flush"},
+            "fused_ms_per_step": fused_ms, "fused_equals_two_pass": same,
+            "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": None, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="icl", choices=["icl", "reference"])
-    ap.add_argument("--workload", default="suite", choices=["suite", "sepconv16k", "conv2d8k", "sep3d"])
+    ap.add_argument("--workload", default="suite", choices=["suite", "sepconv16k", "conv2d8k", "sep3d", "chain"])
     ap.add_argument("--depth", type=int, default=128, help="sep3d: volume depth (slices)")
     ap.add_argument("--radius", type=int, default=2)
     ap.add_argument("--batch", type=int, default=8)
@@ -923,6 +1013,8 @@ def main():
         if args.size == 4096:
             args.size = 16384
         return run_sepconv_bands(args)
+    if args.workload == "chain":
+        return run_chain(args)
     if args.workload == "sep3d":
         if args.size == 4096:
             args.size = 512
