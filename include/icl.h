@@ -222,7 +222,8 @@ icl_status icl_conv2d_u8_sharded(icl_comm* comm, const icl_image* buf, const icl
  * (correlation on every axis, the boundary per axis, R26).  A
  * volume is an icl_image whose batch axis is z: batch = depth,
  * batch_stride_bytes = the slice stride.  Taps: HOST pointers, 2r+1 each,
- * radii 0..7 (> 7 -> ICL_ERR_UNSUPPORTED).  Device volumes only; src and dst
+ * radii 0..7 (> 7 -> ICL_ERR_UNSUPPORTED; so are slices of 2 GiB or more).
+ * Device volumes only; src and dst
  * must not overlap (ICL_ERR_ALIASING); shapes must match.  All variants
  * evaluate the same fp32 chains (bit-identical).  Enqueues on stream. */
 icl_status icl_sepconv3d(const icl_image* src, const icl_image* dst, const float* taps_x, int rx, const float* taps_y,

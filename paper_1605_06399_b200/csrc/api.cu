@@ -1102,6 +1102,8 @@ icl_status icl_sepconv3d(const icl_image* src, const icl_image* dst, const float
   if (src->width != dst->width || src->height != dst->height || src->batch != dst->batch)
     return fail(ICL_ERR_INVALID_ARG, "src and dst volumes differ in shape");
   if (src->height > 524280) return fail(ICL_ERR_UNSUPPORTED, "volume slices taller than 524280 rows");
+  if (src->height * src->pitch_bytes >= (1ll << 31))  // the tile loader's slice-relative offsets are int32
+    return fail(ICL_ERR_UNSUPPORTED, "volume slices of 2 GiB or more");
   if (overlap(byte_range(src, 4), byte_range(dst, 4))) return fail(ICL_ERR_ALIASING, "src and dst overlap");
   if (any_host(src, dst, nullptr)) return fail(ICL_ERR_INVALID_ARG, "icl_sepconv3d takes device volumes only");
   Sep3Params p;
