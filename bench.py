@@ -164,10 +164,15 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- distributed
+# ICL_BENCH_ONE_GPU=1: every rank on cuda:0 with a gloo group -- a functional check of the
+# multi-rank code paths on a one-GPU box (timings are then meaningless; never a bench number)
+ONE_GPU = os.environ.get("ICL_BENCH_ONE_GPU") == "1"
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if ONE_GPU else int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
 
 
@@ -175,7 +180,7 @@ def init_dist(ws, backend):
     import torch.distributed as dist
     if ws > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group(backend)
+        dist.init_process_group("gloo" if ONE_GPU else backend)
     return dist
 
 
@@ -184,7 +189,7 @@ def max_over_ranks(x: float, ws: int, device) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=device)
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if ONE_GPU else device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
