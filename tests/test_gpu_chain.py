@@ -158,6 +158,21 @@ def test_chain_two_pass_schedule(block):
     assert e.value.status == 2
 
 
+def test_chain_padding_never_written():
+    """Row padding of the response and mask (NaN / 77 canaries) survives both schedules."""
+    h, w = 37, 101
+    src = dev(synth.uniform_image(80, h, w), pitch=w + 11)
+    f = synth.gaussian_taps(3)
+    for ws in (None, torch.empty(icl.blur_harris_workspace_bytes(w, h, 1, 5) // 4 + 4, device=DEV)):
+        Rb = torch.full((h, w + 7), float("nan"), device=DEV)
+        Mb = torch.full((h, w + 7), 77, dtype=torch.uint8, device=DEV)
+        icl.blur_harris(src, Rb[:, :w], f, f, "clamp", 0.0, 5, 0.04, "clamp", mask=Mb[:, :w], threshold=0.01,
+                        workspace=ws)
+        torch.cuda.synchronize()
+        assert torch.isnan(Rb[:, w:]).all() and (Mb[:, w:] == 77).all()
+        assert not torch.isnan(Rb[:, :w]).any()
+
+
 def test_chain_large_sampled():
     """4096^2 in the bench's launch configuration (S = 64 row segments), vs the two calls."""
     img = torch.empty(2, 4096, 4096, device=DEV)

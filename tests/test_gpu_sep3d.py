@@ -61,6 +61,24 @@ def test_sepconv3d_vs_oracle_and_variants(shape, radii, border, c):
         assert torch.equal(o, outs[0])
 
 
+def test_sepconv3d_padding_and_slice_stride():
+    """Pitched rows and a padded slice stride on both sides; canaries in the padding survive."""
+    d, h, w = 9, 21, 45
+    v = vol(60, d, h, w)
+    sb = torch.full((d, h + 3, w + 9), float("nan"), device=DEV)
+    sb[:, :h, :w] = torch.from_numpy(v).to(DEV)
+    db = torch.full((d, h + 2, w + 5), float("nan"), device=DEV)
+    f, g, hz = synth.gaussian_taps(2), synth.gaussian_taps(1), synth.gaussian_taps(3)
+    for name in icl.variant_names("sepconv3d"):
+        icl.force_variant("sepconv3d", name)
+        db.fill_(float("nan"))
+        icl.sepconv3d(sb[:, :h, :w], db[:, :h, :w], f, g, hz, "clamp")
+        torch.cuda.synchronize()
+        assert torch.isnan(db[:, :, w:]).all() and torch.isnan(db[:, h:, :]).all()
+        check(db[:, :h, :w].cpu().numpy(), v, f, g, hz, "clamp", 0.0)
+    icl.force_variant("sepconv3d", None)
+
+
 def test_sepconv3d_large_sampled():
     """64 x 512 x 512 (256 MB in + out), r = 3 on every axis, sampled voxels incl. the boundary faces."""
     d, hh, w = 64, 512, 512
