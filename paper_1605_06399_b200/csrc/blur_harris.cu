@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) blur_harris_kernel(BlurHarri
 
 template <int R, int B>
 static cudaError_t launch_bh(const BlurHarrisParams& bp, int batch, int S, cudaStream_t s) {
-  constexpr int NW = 2;
+  constexpr int NW = 4;
   constexpr int TW = 120 * NW;
   const size_t smem = ((size_t)(ChainGeom<B>::NSR + 2) * (TW + 16) +   // blurred ring + mirror rows
                        (size_t)(2 * ChainGeom<B>::RB + 2 * R + 1) * (TW + 24) +  // raw rows
