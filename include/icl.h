@@ -269,6 +269,20 @@ icl_status icl_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* off
 icl_status icl_ipc_open(const void* handle64, uint64_t offset, void** dev_ptr);
 icl_status icl_ipc_close(void* dev_ptr, uint64_t offset);
 
+/* Pull this rank's halo rows straight from the neighbours' bands (peer loads
+ * in a copy kernel over NVLink; no NCCL, no staging): buf holds global rows
+ * [buf_y0, buf_y0 + buf->height) with the owned rows [own_y0, own_y1) inside;
+ * rows [buf_y0, own_y0) come from the last rows of `up` (the up neighbour's
+ * owned rows, ending at own_y0), rows [own_y1, end) from the first rows of
+ * `down` (starting at own_y1).  elem_bytes 4 (fp32) or 1 (uint8).  Then any
+ * filter runs on buf through icl_band as in icl_*_sharded -- the generic
+ * peer-memory form of the halo exchange for every filter; icl_sepconv_peer
+ * goes further and reads the peers inside the filter kernel.  Ordering as
+ * icl_sepconv_peer.  Errors: geometry -> ICL_ERR_INVALID_ARG; rows not
+ * 4-byte aligned -> ICL_ERR_UNSUPPORTED. */
+icl_status icl_halo_pull(const icl_image* buf, int64_t global_height, int64_t buf_y0, int64_t own_y0,
+                         int64_t own_y1, const icl_image* up, const icl_image* down, int elem_bytes, void* stream);
+
 /* Separable convolution of the global rows [own_y0, own_y0 + own->height) of
  * an image of global_height rows whose row bands live on different GPUs.
  * own: this rank's rows ONLY (no halo rows); up / down: the neighbouring
@@ -283,19 +297,6 @@ icl_status icl_ipc_close(void* dev_ptr, uint64_t offset);
  * unchanged until they finish (bracket the call with a cross-rank barrier).
  * Errors: geometry (dst shape != own, neighbour missing or thinner than ry
  * rows where needed, radius > 15) -> ICL_ERR_INVALID_ARG. */
-/* Pull this rank's halo rows straight from the neighbours' bands (peer loads
- * in a copy kernel over NVLink; no NCCL, no staging): buf holds global rows
- * [buf_y0, buf_y0 + buf->height) with the owned rows [own_y0, own_y1) inside;
- * rows [buf_y0, own_y0) come from the last rows of `up` (the up neighbour's
- * owned rows, ending at own_y0), rows [own_y1, end) from the first rows of
- * `down` (starting at own_y1).  elem_bytes 4 (fp32) or 1 (uint8).  Then any
- * filter runs on buf through icl_band as in icl_*_sharded -- the generic
- * peer-memory form of the halo exchange for every filter; icl_sepconv_peer
- * goes further and reads the peers inside the filter kernel.  Ordering as
- * icl_sepconv_peer.  Errors: geometry -> ICL_ERR_INVALID_ARG; rows not
- * 4-byte aligned -> ICL_ERR_UNSUPPORTED. */
-icl_status icl_halo_pull(const icl_image* buf, int64_t global_height, int64_t buf_y0, int64_t own_y0,
-                         int64_t own_y1, const icl_image* up, const icl_image* down, int elem_bytes, void* stream);
 icl_status icl_sepconv_peer(const icl_image* own, const icl_image* dst, int64_t global_height, int64_t own_y0,
                             const icl_image* up, const icl_image* down, const float* taps_x, int rx,
                             const float* taps_y, int ry, icl_border border, float border_value, void* stream);
