@@ -503,6 +503,7 @@ def run_suite(args):
                        "input_gen_s": round(t_gen, 1)},
             "per_filter_mpx_s": {f: px_rank / (m * 1e-3) / 1e6 for f, m in med.items()},
             "per_filter_ms": med,
+            "per_filter_ms_min": {f: min(v) for f, v in per.items()},
             "roofline": {k: roof[dominant][k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
             "roofline_kernel": dominant,
             "rooflines": roof,
