@@ -197,3 +197,28 @@ def test_chain_errors():
     assert e.value.status == 2
     with pytest.raises((icl.IclError, ValueError, TypeError)):
         icl.blur_harris(a.cpu(), b.cpu(), [1.0], [1.0])  # device images only
+
+
+def test_chain_random_sweep():
+    """24 seeded random cases: shapes (incl. 1-row / 1-column), radii 0..3 per axis, blocks 1..5, both
+    borders and constants, both schedules -- bit-identical to the two calls."""
+    rng = np.random.default_rng(2024)
+    for case in range(24):
+        h, w = int(rng.integers(1, 90)), int(rng.integers(1, 700))
+        if case % 6 == 0:
+            h = 1
+        if case % 6 == 1:
+            w = 1
+        rx, ry, block = int(rng.integers(0, 4)), int(rng.integers(0, 4)), int(rng.integers(1, 6))
+        bb = ("constant", float(rng.choice([0.0, 0.6]))) if rng.random() < 0.5 else ("clamp", 0.0)
+        hb = ("constant", float(rng.choice([0.0, 0.2]))) if rng.random() < 0.5 else ("clamp", 0.0)
+        src = dev(synth.uniform_image(900 + case, h, w))
+        fx, gy = synth.signed_taps(case, rx), synth.gaussian_taps(ry)
+        thr = float(rng.random() * 0.01)
+        R0, m0 = two_calls(src, fx, gy, bb[0], bb[1], block, 0.04, hb[0], hb[1], thr)
+        R1, m1 = fused(src, fx, gy, bb[0], bb[1], block, 0.04, hb[0], hb[1], thr)
+        assert torch.equal(R0, R1) and torch.equal(m0, m1), (case, h, w, rx, ry, block, bb, hb)
+        ws = torch.empty(icl.blur_harris_workspace_bytes(w, h, 1, block) // 4 + 4, device=DEV)
+        R2, m2 = out_like(src), out_like(src, torch.uint8)
+        icl.blur_harris(src, R2, fx, gy, bb[0], bb[1], block, 0.04, hb[0], hb[1], mask=m2, threshold=thr, workspace=ws)
+        assert torch.equal(R0, R2) and torch.equal(m0, m2), case
