@@ -300,6 +300,17 @@ icl_status icl_halo_pull(const icl_image* buf, int64_t global_height, int64_t bu
 icl_status icl_sepconv_peer(const icl_image* own, const icl_image* dst, int64_t global_height, int64_t own_y0,
                             const icl_image* up, const icl_image* down, const float* taps_x, int rx,
                             const float* taps_y, int ry, icl_border border, float border_value, void* stream);
+/* Harris on one rank's rows, the same contract as icl_sepconv_peer: own holds
+ * only this rank's rows; the edge rows (floor(block/2)+1 above and
+ * block-floor(block/2) below, where a neighbour exists) run a kernel whose
+ * input loads resolve to the own band or directly to `up` / `down`; the rest
+ * runs on the ordinary Harris kernels.  Stitched responses and masks equal
+ * the unsharded icl_harris bit for bit (one fp32 order, per-stage boundary in
+ * GLOBAL coordinates).  Errors: geometry, block outside [1, 7] ->
+ * ICL_ERR_INVALID_ARG; otherwise as icl_harris. */
+icl_status icl_harris_peer(const icl_image* own, const icl_image* response, int64_t global_height, int64_t own_y0,
+                          const icl_image* up, const icl_image* down, int block, float k, icl_border border,
+                          float border_value, const icl_image* mask, float threshold, void* stream);
 
 /* ------------------------------------------------------------------------
  * Variant space + auto-tuner (§4, Table 1 lines

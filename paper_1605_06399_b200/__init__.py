@@ -33,7 +33,7 @@ EXPORTS = ("icl_sepconv", "icl_sepconv_workspace_bytes", "icl_harris", "icl_nlm"
            "icl_comm_destroy", "icl_sepconv_sharded", "icl_harris_sharded", "icl_nlm_sharded", "icl_conv2d_u8_sharded",
            "icl_tune_ann", "icl_ann_search", "icl_ann_fit", "icl_blur_harris", "icl_blur_harris_workspace_bytes",
            "icl_ipc_get_handle", "icl_ipc_open", "icl_ipc_close", "icl_sepconv_peer",
-           "icl_halo_pull", "icl_sepconv3d")
+           "icl_halo_pull", "icl_sepconv3d", "icl_harris_peer")
 
 # int evaluate(void* ctx, int index, double* value) -- icl_ann_search's callback
 EVAL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double))
@@ -121,6 +121,7 @@ def load_library(path: str = LIB_PATH):
         "icl_ipc_close": ([P, ctypes.c_uint64], I),
         "icl_sepconv_peer": ([img, img, I64, I64, img, img, P, I, P, I, I, F, P], I),
         "icl_halo_pull": ([img, I64, I64, I64, I64, img, img, I, P], I),
+        "icl_harris_peer": ([img, img, I64, I64, img, img, I, F, I, F, img, F, P], I),
         "icl_sepconv3d": ([img, img, P, I, P, I, P, I, I, F, P], I),
         "icl_tune_ann": ([ctypes.POINTER(icl_problem), I, I, ctypes.c_uint64, P, ctypes.POINTER(icl_variant_info)], I),
         "icl_ann_search": ([ctypes.POINTER(ctypes.c_double), I, I, EVAL_FN, P, I, I, ctypes.c_uint64,
@@ -505,6 +506,19 @@ def sepconv_peer(own, dst, global_height: int, own_y0: int, up: Optional[PeerIma
                                 ctypes.cast(fx, ctypes.c_void_p), len(fx) // 2, ctypes.cast(gy, ctypes.c_void_p),
                                 len(gy) // 2, BORDER[border], border_value, _stream(stream)))
     return dst
+
+
+def harris_peer(own, response, global_height: int, own_y0: int, up: Optional[PeerImage], down: Optional[PeerImage],
+                block: int = 5, k: float = 0.04, border: str = "clamp", border_value: float = 0.0, mask=None,
+                threshold: float = 0.0, stream=None):
+    """One rank's Harris rows, halo rows read in-kernel from the peers (icl_harris_peer)."""
+    lib = load_library()
+    o, r = _image(own), _image(response)
+    m = _image(mask, 1) if mask is not None else None
+    _check(lib.icl_harris_peer(ctypes.byref(o), ctypes.byref(r), global_height, own_y0,
+                               ctypes.byref(up.image) if up else None, ctypes.byref(down.image) if down else None,
+                               block, k, BORDER[border], border_value, _ref(m), threshold, _stream(stream)))
+    return response
 
 
 def halo_pull(buf, global_height: int, buf_y0: int, own_y0: int, own_y1: int, up: Optional[PeerImage],

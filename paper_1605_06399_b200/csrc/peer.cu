@@ -110,6 +110,80 @@ __global__ void __launch_bounds__(kEdgeTW) sep_edge_peer(EdgeParams p) {
   }
 }
 
+// Harris edge rows of a band whose input rows come from the own band or a
+// neighbour's band: the naive Harris kernel's per-output operations (the one
+// fp32 order of every Harris variant, harris.cu) with the row resolver above.
+struct HarrisEdgeParams {
+  RowSeg seg[3];
+  int W, Hg;
+  int border;
+  float cval;
+  int block;
+  float k, threshold;
+  char* dst;  // response row out_y0, image 0
+  int64_t dpitch, dbstride;
+  char* mask;  // nullable, row out_y0, image 0
+  int64_t mpitch, mbstride;
+  int out_y0, out_y1;
+};
+
+__device__ __forceinline__ float hread(const HarrisEdgeParams& p, int b, int x, int y) {
+  if (x < 0 || x >= p.W || y < 0 || y >= p.Hg) {
+    if (p.border == kBorderConstant) return p.cval;
+    x = clampi(x, 0, p.W - 1);
+    y = clampi(y, 0, p.Hg - 1);
+  }
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    const RowSeg& g = p.seg[s];
+    if (y >= g.y0 && y < g.y1)
+      return reinterpret_cast<const float*>(g.base + (int64_t)b * g.bstride + (int64_t)(y - g.y0) * g.pitch)[x];
+  }
+  return 0.0f;  // unreachable for a validated call
+}
+
+__device__ __forceinline__ void hsobel(const HarrisEdgeParams& p, int b, int qx, int qy, float& dx, float& dy) {
+  if (qx < 0 || qx >= p.W || qy < 0 || qy >= p.Hg) {  // per-stage boundary of dx / dy
+    if (p.border == kBorderConstant) { dx = 0.0f; dy = 0.0f; return; }
+    qx = clampi(qx, 0, p.W - 1);
+    qy = clampi(qy, 0, p.Hg - 1);
+  }
+  float hd[3], vd[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    hd[i] = __fsub_rn(hread(p, b, qx + 1, qy - 1 + i), hread(p, b, qx - 1, qy - 1 + i));
+    vd[i] = __fsub_rn(hread(p, b, qx - 1 + i, qy + 1), hread(p, b, qx - 1 + i, qy - 1));
+  }
+  dx = __fmaf_rn(2.0f, hd[1], __fadd_rn(hd[0], hd[2]));
+  dy = __fmaf_rn(2.0f, vd[1], __fadd_rn(vd[0], vd[2]));
+}
+
+__global__ void __launch_bounds__(256) harris_edge_peer(HarrisEdgeParams p) {
+  const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int y = p.out_y0 + blockIdx.y * 8 + (threadIdx.x >> 5);
+  const int b = blockIdx.z;
+  if (x >= p.W || y >= p.out_y1) return;
+  const int a = p.block / 2, bb = p.block - 1 - a;
+  float sxx = 0.0f, sxy = 0.0f, syy = 0.0f;
+  for (int ty = -a; ty <= bb; ++ty) {
+    float hxx = 0.0f, hxy = 0.0f, hyy = 0.0f;
+    for (int tx = -a; tx <= bb; ++tx) {
+      float dx, dy;
+      hsobel(p, b, x + tx, y + ty, dx, dy);
+      hxx = __fmaf_rn(dx, dx, hxx);
+      hxy = __fmaf_rn(dx, dy, hxy);
+      hyy = __fmaf_rn(dy, dy, hyy);
+    }
+    if (ty == -a) { sxx = hxx; sxy = hxy; syy = hyy; }
+    else { sxx = __fadd_rn(sxx, hxx); sxy = __fadd_rn(sxy, hxy); syy = __fadd_rn(syy, hyy); }
+  }
+  const float det = __fmaf_rn(sxx, syy, -__fmul_rn(sxy, sxy));
+  const float tr = __fadd_rn(sxx, syy);
+  const float R = __fmaf_rn(-p.k, __fmul_rn(tr, tr), det);
+  reinterpret_cast<float*>(p.dst + (int64_t)b * p.dbstride + (int64_t)(y - p.out_y0) * p.dpitch)[x] = R;
+  if (p.mask) p.mask[(int64_t)b * p.mbstride + (int64_t)(y - p.out_y0) * p.mpitch + x] = R > p.threshold ? 1 : 0;
+}
+
 // Copy rows of a neighbour's band (peer memory) into this rank's halo rows:
 // one thread per 16-byte (or 4-byte) chunk, rows x chunks x images.
 struct PullParams {
@@ -249,6 +323,96 @@ icl_status icl_sepconv_peer(const icl_image* own, const icl_image* dst, int64_t 
     return e == cudaSuccess ? ICL_OK : report_error(ICL_ERR_CUDA, cudaGetErrorString(e));
   };
   if (i1 <= i0) return edge(y0, y1);  // thin band: every row is an edge row
+  if ((st = edge(y0, i0))) return st;
+  return edge(i1, y1);
+}
+
+icl_status icl_harris_peer(const icl_image* own, const icl_image* response, int64_t global_height, int64_t own_y0,
+                          const icl_image* up, const icl_image* down, int block, float k, icl_border border,
+                          float border_value, const icl_image* mask, float threshold, void* stream) {
+  if (!own || !response) return report_error(ICL_ERR_INVALID_ARG, "null argument");
+  if (block < 1 || block > 7) return report_error(ICL_ERR_INVALID_ARG, "block must be in [1, 7]");
+  if (border != ICL_BORDER_CONSTANT && border != ICL_BORDER_CLAMP)
+    return report_error(ICL_ERR_INVALID_ARG, "border must be ICL_BORDER_CONSTANT or ICL_BORDER_CLAMP");
+  const int64_t H = global_height, y0 = own_y0, y1 = own_y0 + own->height;
+  if (H < 1 || H >= (1ll << 31) || y0 < 0 || y1 > H || response->height != own->height ||
+      response->width != own->width || response->batch != own->batch || own->width < 1 || own->height < 1 ||
+      own->batch < 1 || own->batch > 65535 || !own->data || !response->data)
+    return report_error(ICL_ERR_INVALID_ARG, "bad band geometry");
+  if (mask && mask->data && (mask->width != own->width || mask->height != own->height || mask->batch != own->batch))
+    return report_error(ICL_ERR_INVALID_ARG, "mask shape differs from the response");
+  const int a = block / 2, bb = block - 1 - a;
+  const int64_t hu = a + 1, hdn = bb + 1;  // input rows a response row needs above / below
+  const int64_t need_up = std::min<int64_t>(hu, y0), need_dn = std::min<int64_t>(hdn, H - y1);
+  auto check_nb = [&](const icl_image* nb, int64_t need, const char* which) -> icl_status {
+    if (need == 0) return ICL_OK;
+    if (!nb || !nb->data || nb->height < need || nb->width != own->width || nb->batch != own->batch)
+      return report_error(ICL_ERR_INVALID_ARG, which);
+    return ICL_OK;
+  };
+  icl_status st;
+  if ((st = check_nb(up, need_up, "up neighbour band missing or thinner than the halo"))) return st;
+  if ((st = check_nb(down, need_dn, "down neighbour band missing or thinner than the halo"))) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // rows needing no halo: the ordinary Harris kernels on the own band
+  const int64_t i0 = y0 + (y0 > 0 ? hu : 0), i1 = y1 - (y1 < H ? hdn : 0);
+  if (i1 > i0) {
+    icl_image dv = *response;
+    dv.data = static_cast<char*>(response->data) + (i0 - y0) * response->pitch_bytes;
+    dv.height = i1 - i0;
+    icl_image mv;
+    if (mask && mask->data) {
+      mv = *mask;
+      mv.data = static_cast<char*>(mask->data) + (i0 - y0) * mask->pitch_bytes;
+      mv.height = i1 - i0;
+    }
+    const icl_band bi{H, y0, i0};
+    if ((st = icl_harris(own, &dv, block, k, border, border_value, mask && mask->data ? &mv : nullptr, threshold, &bi,
+                         s)))
+      return st;
+  }
+  // edge rows: input rows from the own band or straight from the neighbours' bands
+  HarrisEdgeParams p;
+  memset(&p, 0, sizeof p);
+  auto seg = [](const icl_image* im, int64_t gy0) {
+    RowSeg g;
+    g.base = static_cast<const char*>(im->data);
+    g.pitch = im->pitch_bytes;
+    g.bstride = im->batch > 1 ? im->batch_stride_bytes : 0;
+    g.y0 = (int)gy0;
+    g.y1 = (int)(gy0 + im->height);
+    return g;
+  };
+  p.seg[1] = seg(own, y0);
+  if (need_up) p.seg[0] = seg(up, y0 - up->height);
+  if (need_dn) p.seg[2] = seg(down, y1);
+  p.W = (int)own->width;
+  p.Hg = (int)H;
+  p.border = border == ICL_BORDER_CLAMP ? kBorderClamp : kBorderConstant;
+  p.cval = border_value;
+  p.block = block;
+  p.k = k;
+  p.threshold = threshold;
+  p.dpitch = response->pitch_bytes;
+  p.dbstride = response->batch > 1 ? response->batch_stride_bytes : 0;
+  auto edge = [&](int64_t a0, int64_t a1) -> icl_status {
+    if (a1 <= a0) return ICL_OK;
+    p.dst = static_cast<char*>(response->data) + (a0 - y0) * response->pitch_bytes;
+    p.mask = nullptr;
+    if (mask && mask->data) {
+      p.mask = static_cast<char*>(mask->data) + (a0 - y0) * mask->pitch_bytes;
+      p.mpitch = mask->pitch_bytes;
+      p.mbstride = mask->batch > 1 ? mask->batch_stride_bytes : 0;
+    }
+    p.out_y0 = (int)a0;
+    p.out_y1 = (int)a1;
+    dim3 grd((unsigned)((own->width + 31) / 32), (unsigned)((a1 - a0 + 7) / 8), (unsigned)own->batch);
+    harris_edge_peer<<<grd, 256, 0, s>>>(p);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? ICL_OK : report_error(ICL_ERR_CUDA, cudaGetErrorString(e));
+  };
+  if (i1 <= i0) return edge(y0, y1);
   if ((st = edge(y0, i0))) return st;
   return edge(i1, y1);
 }

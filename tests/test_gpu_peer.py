@@ -86,6 +86,55 @@ def test_sepconv_peer_bands_equal_unsharded(n, H, W, B, rx, ry, border, cval):
     mp.spawn(_worker, args=(n, _free_port(), H, W, B, rx, ry, border, cval), nprocs=n, join=True)
 
 
+def _harris_worker(rank, n, port, H, W, block, border, cval):
+    """icl_harris_peer: own rows only, edge rows read in-kernel from the neighbours' bands."""
+    import paper_1605_06399_b200 as icl
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=n)
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    full = synth.rect_scene(90, H, W)
+    rows = -(-H // n)
+    r0, r1 = rank * rows, min(H, (rank + 1) * rows)
+    buf = torch.full((r1 - r0, W + 4), float("nan"), device=dev)
+    own = buf[:, :W]
+    own.copy_(torch.from_numpy(full[r0:r1]))
+    torch.cuda.synchronize()
+    meta = [None] * n
+    dist.all_gather_object(meta, icl.ipc_handle(buf) + (r1 - r0,))
+    nb = {}
+    for q in (rank - 1, rank + 1):
+        if 0 <= q < n:
+            h, off, hgt = meta[q]
+            nb[q] = icl.PeerImage(h, off, W, hgt, W + 4)
+    dist.barrier()
+    out = torch.full((r1 - r0, W), float("nan"), device=dev)
+    m = torch.full((r1 - r0, W), 77, dtype=torch.uint8, device=dev)
+    icl.harris_peer(own, out, H, r0, nb.get(rank - 1), nb.get(rank + 1), block, 0.04, border, cval, mask=m,
+                    threshold=0.01)
+    torch.cuda.synchronize()
+    dist.barrier()
+    parts = [None] * n
+    dist.all_gather_object(parts, (out.cpu().numpy(), m.cpu().numpy()))
+    if rank == 0:
+        src = torch.from_numpy(full).to(dev)
+        ref = torch.empty_like(src)
+        mref = torch.empty(H, W, dtype=torch.uint8, device=dev)
+        icl.harris(src, ref, block, 0.04, border, cval, mask=mref, threshold=0.01)
+        np.testing.assert_array_equal(np.concatenate([p[0] for p in parts]), ref.cpu().numpy())
+        np.testing.assert_array_equal(np.concatenate([p[1] for p in parts]), mref.cpu().numpy())
+    for p in nb.values():
+        p.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,block,border,cval", [(2, 5, "clamp", 0.0), (3, 2, "constant", 0.3), (3, 7, "clamp", 0.0)])
+def test_harris_peer_bands_equal_unsharded(n, block, border, cval):
+    mp.spawn(_harris_worker, args=(n, _free_port(), 97, 203, block, border, cval), nprocs=n, join=True)
+
+
 def _pull_worker(rank, n, port, H, W, filt):
     """Halo rows pulled from the neighbours' owned rows (icl_halo_pull), then the ordinary band call."""
     import paper_1605_06399_b200 as icl
