@@ -125,6 +125,11 @@ def test_new_entry_points_validate_on_the_host():
     st = lib.icl_sepconv_peer(ctypes.byref(band), ctypes.byref(out), 16, 8, None, None, tp, 1, tp, 1, 0, 0.0, None)
     assert st == 1 and b"neighbour" in lib.icl_last_error()
     assert lib.icl_halo_pull(ctypes.byref(band), 16, 0, 0, 8, None, None, 2, None) == 1
+    st = lib.icl_harris_peer(ctypes.byref(band), ctypes.byref(out), 16, 8, None, None, 5, 0.04, 1, 0.0, None, 0.0,
+                             None)
+    assert st == 1 and b"neighbour" in lib.icl_last_error()
+    assert lib.icl_harris_peer(ctypes.byref(band), ctypes.byref(out), 16, 0, None, None, 9, 0.04, 1, 0.0, None, 0.0,
+                               None) == 1  # block > 7
     # model-guided tuning: n1 < 1
     prob = icl.icl_problem()
     assert lib.icl_tune_ann(ctypes.byref(prob), 0, 1, 0, None, None) == 1
