@@ -495,6 +495,18 @@ class PeerImage:
             self.ptr = None
 
 
+class LocalBand:
+    """A neighbour band that is plain device memory of this process (same interface as PeerImage):
+    for single-process use and tests of the peer paths without IPC."""
+
+    def __init__(self, t):
+        self.tensor = t  # keeps the memory alive
+        self.image = _image(t)
+
+    def close(self):
+        pass
+
+
 def sepconv_peer(own, dst, global_height: int, own_y0: int, up: Optional[PeerImage], down: Optional[PeerImage],
                  taps_x, taps_y, border: str = "constant", border_value: float = 0.0, stream=None):
     """One rank's rows of a row-band sharded sepconv, halo rows read in-kernel from the peers (icl_sepconv_peer)."""

@@ -188,6 +188,40 @@ def test_halo_pull_bands_equal_unsharded(n, filt):
     mp.spawn(_pull_worker, args=(n, _free_port(), 150, 203, filt), nprocs=n, join=True)
 
 
+@pytest.mark.parametrize("nb", [2, 3, 5])
+def test_peer_paths_in_one_process(nb):
+    """The bands of one image in one process, neighbours passed as plain device memory
+    (icl.LocalBand): sepconv_peer and harris_peer stitched == unsharded, bit for bit."""
+    import paper_1605_06399_b200 as icl
+    DEV = torch.device("cuda:0")
+    H, W = 120, 333
+    full = synth.rect_scene(95, H, W)
+    rows = -(-H // nb)
+    cuts = [(k * rows, min(H, (k + 1) * rows)) for k in range(nb)]
+    bands = [torch.from_numpy(np.ascontiguousarray(full[a:b])).to(DEV) for a, b in cuts]
+    f = synth.gaussian_taps(3)
+    src = torch.from_numpy(full).to(DEV)
+    ref_s, ref_h = torch.empty_like(src), torch.empty_like(src)
+    ref_m = torch.empty(H, W, dtype=torch.uint8, device=DEV)
+    icl.sepconv(src, ref_s, f, f, "clamp")
+    icl.harris(src, ref_h, 5, 0.04, "constant", 0.2, mask=ref_m, threshold=0.01)
+    out_s, out_h, out_m = [], [], []
+    for k, (a, b) in enumerate(cuts):
+        up = icl.LocalBand(bands[k - 1]) if k > 0 else None
+        dn = icl.LocalBand(bands[k + 1]) if k + 1 < nb else None
+        o = torch.empty(b - a, W, device=DEV)
+        icl.sepconv_peer(bands[k], o, H, a, up, dn, f, f, "clamp")
+        out_s.append(o)
+        oh = torch.empty(b - a, W, device=DEV)
+        om = torch.empty(b - a, W, dtype=torch.uint8, device=DEV)
+        icl.harris_peer(bands[k], oh, H, a, up, dn, 5, 0.04, "constant", 0.2, mask=om, threshold=0.01)
+        out_h.append(oh)
+        out_m.append(om)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(out_s), ref_s)
+    assert torch.equal(torch.cat(out_h), ref_h) and torch.equal(torch.cat(out_m), ref_m)
+
+
 def test_sepconv_peer_single_rank_and_errors():
     import paper_1605_06399_b200 as icl
     dev = torch.device("cuda:0")

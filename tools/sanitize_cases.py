@@ -93,4 +93,15 @@ for shape in [(5, 13, 70), (17, 20, 3)]:
                 icl.sepconv3d(v, o, fx, fx, fx, border, 0.5)
         torch.cuda.synchronize()
     icl.force_variant("sepconv3d", None)
+# peer paths with neighbours as local device memory (edge kernels reading the neighbour bands)
+full = synth.rect_scene(9, 90, 130)
+bands = [torch.from_numpy(np.ascontiguousarray(full[a:b])).to(dev) for a, b in ((0, 30), (30, 60), (60, 90))]
+for k, (a, b) in enumerate(((0, 30), (30, 60), (60, 90))):
+    up = icl.LocalBand(bands[k - 1]) if k > 0 else None
+    dn = icl.LocalBand(bands[k + 1]) if k < 2 else None
+    o = torch.empty(b - a, 130, device=dev)
+    m = torch.empty(b - a, 130, dtype=torch.uint8, device=dev)
+    icl.sepconv_peer(bands[k], o, 90, a, up, dn, synth.gaussian_taps(7), synth.gaussian_taps(7), "constant", 0.5)
+    icl.harris_peer(bands[k], o, 90, a, up, dn, 7, 0.04, "clamp", 0.0, mask=m, threshold=0.1)
+torch.cuda.synchronize()
 print("sanitize cases done")
