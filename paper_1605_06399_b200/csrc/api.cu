@@ -385,7 +385,7 @@ static int default_variant(const Prepared& pc) {
       if (pc.pixels < (1 << 16)) return variant_id(pc.f, "stream_nt32_s16_v4");
       // 240-column strips: short row segments keep enough CTAs in flight up to one 4096^2 image
       // (1024^2 24.5 vs 34.8 us, 2048^2 30.7 vs 66 us, 4096^2 76 vs 90 us; 8 x 4096^2 prefers s64)
-      return variant_id(pc.f, pc.pixels <= (1 << 21) ? "shfl_nw2_s8" : pc.pixels <= (1 << 25) ? "shfl_nw2_s16" : "shfl_nw2_s64");
+      return variant_id(pc.f, pc.pixels <= (1 << 21) ? "shfl_nw2_s8" : pc.pixels <= (1 << 25) ? "shfl_nw2_s16" : "shfl_nw2_s32");
     case ICL_FILTER_NLM:
       if (nlm_x2_supported(pc.nlm.P, pc.nlm.S)) return variant_id(pc.f, "boxsum_x2");
       if (nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return variant_id(pc.f, "boxsum_r8");
