@@ -57,8 +57,10 @@ def measured_peaks():
 
 
 # variant -> kernel-name fragments (to attach ncu counters only to the kernel they were measured on)
-KERNEL_OF = {"boxsum_x2": ("nlm_box_x2",), "boxsum_r8": ("nlm_box_r8",), "stream_nt64_s16_v4": ("sep_stream<2, 64",),
-             "shfl_nw2_s64": ("harris_shfl<5, 2>",)}
+# (the S = segment-rows variants of one family launch the same kernel function)
+KERNEL_OF = {"boxsum_x2": ("nlm_box_x2",), "boxsum_r8": ("nlm_box_r8",),
+             **{f"stream_nt64_s{s}_v4": ("sep_stream<2, 64",) for s in (16, 32, 64, 128)},
+             **{f"shfl_nw2_s{s}": ("harris_shfl<5, 2>",) for s in (8, 16, 32, 64, 128)}}
 
 
 def ncu_traffic():
