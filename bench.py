@@ -180,6 +180,11 @@ def dist_env():
 
 def init_dist(ws, backend):
     import torch.distributed as dist
+    if ws > 1:
+        # NCCL's init lines ("... nRanks N ...") stay visible on stderr, so a reader can check the
+        # communicator sizes the run really used
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if ws > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("gloo" if ONE_GPU else backend)
@@ -516,6 +521,14 @@ def run_suite(args):
         }
         if not args.no_small:
             line["small_configs"] = small_configs(dev)
+    if not args.no_16k:
+        # configs[3] at this N (every rank takes part: the exchange is collective)
+        del u, hs, ns, o_sep, o_har, o_mask, o_nlm
+        torch.cuda.empty_cache()
+        k16 = sepconv16k_keys(ws, rank, local, dist, args.steps)
+        if rank == 0:
+            line["sepconv16k_row_bands"] = k16
+    if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -576,20 +589,17 @@ def small_configs(dev):
     return out
 
 
-def run_sepconv_bands(args):
-    """BASELINE.json configs[3]: one S x S fp32 image, separable Gaussian radius r,
-    row-band sharded over the ranks with an NCCL halo exchange (dist.halo_exchange)
-    overlapped with the interior rows.  Strong scaling (the image is fixed)."""
+def time_sepconv_bands(S, r, steps, warmup, ws, rank, local, dist, halo="nccl", torch_comm=False):
+    """BASELINE.json configs[3] core: one S x S fp32 image, separable Gaussian radius r, row-band
+    sharded over the ws ranks; the halo exchange (NCCL in libicl.so by default) overlapped with the
+    interior rows.  Input pre-sharded (each rank fills its own rows on the device, untimed, like
+    the paper's transfer exclusion PAPER.md:581-582).  Returns a dict with the max-over-ranks step
+    time and how it ran; every rank must call it."""
     import torch
 
     import paper_1605_06399_b200 as icl
     from paper_1605_06399_b200 import dist as icd
-    ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist = init_dist(ws, "nccl")
-    icl.load_library()
-    S, r = args.size, args.radius
     band = icd.partition(S, ws, rank, r, r)
     buf = torch.empty(band.buf_rows, S, device=dev)
     # own rows from the device generator (synth.uniform_image stream), halos by exchange
@@ -602,14 +612,18 @@ def run_sepconv_bands(args):
     def call(src, dst, b, st):
         icl.sepconv(src, dst, fx, fx, "constant", band=b, stream=st)
 
-    peer = ws > 1 and args.halo == "peer"
-    native = ws > 1 and not args.torch_comm and not peer
+    # one GPU shared by every rank (ICL_BENCH_ONE_GPU): NCCL refuses two ranks on one device, so
+    # the functional check takes the peer-load path (CUDA IPC works between processes of one GPU)
+    if ONE_GPU and ws > 1 and halo == "nccl" and not torch_comm:
+        halo = "peer"
+    peer = ws > 1 and halo == "peer"
+    native = ws > 1 and not torch_comm and not peer
     ncomm = icl.Comm(ws, rank) if native else None  # icl_sepconv_sharded: NCCL halo exchange in libicl.so
+    nbr = {}
     if peer:  # icl_sepconv_peer: own rows only, the halo read in-kernel from the neighbours (CUDA IPC)
         own = buf[band.own_slice]
         meta = [None] * ws
         dist.all_gather_object(meta, icl.ipc_handle(buf) + (band.r0 - band.s0,))
-        nbr = {}
         for q in (rank - 1, rank + 1):
             if 0 <= q < ws:
                 qb = icd.partition(S, ws, q, r, r)
@@ -629,7 +643,7 @@ def run_sepconv_bands(args):
         icd.run_band(call, buf, out, band, (lambda: icd.halo_exchange(buf, band)) if ws > 1 else (lambda: None),
                      stream=stream, comm_stream=comm if ws > 1 else None)
 
-    for _ in range(max(3, args.warmup)):
+    for _ in range(max(3, warmup)):
         step()
     torch.cuda.synchronize(dev)
     if ws > 1:
@@ -638,14 +652,94 @@ def run_sepconv_bands(args):
     with ClockSampler(local) as clk:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             step()
         b.record(stream)
         torch.cuda.synchronize(dev)
     launches = icl.launch_count() - n0
     if ws > 1:
         dist.barrier()
-    step_ms = max_over_ranks(a.elapsed_time(b) / args.steps, ws, dev)
+    step_ms = max_over_ranks(a.elapsed_time(b) / steps, ws, dev)
+    res = {"ms": step_ms, "launches": launches, "clocks": clk.summary(), "halo_rows": [band.up, band.down],
+           "exchange": ("icl_sepconv_peer (halo rows loaded in-kernel from the peers, CUDA IPC)"
+                        if peer else "icl_sepconv_sharded (NCCL in libicl.so)" if native else
+                        "torch.distributed batch_isend_irecv" if ws > 1 else "none (one rank holds the image)"),
+           "variant": icl.variant_names("sepconv")[icl.last_variant("sepconv")]}
+    if ncomm is not None:
+        ncomm.close()
+    if peer:
+        dist.barrier()  # no rank frees its band while a peer may still read it
+        for p in nbr.values():
+            p.close()
+    del buf, out
+    return res
+
+
+def sepconv16k_keys(ws, rank, local, dist, steps, radii=(2, 15), S=16384):
+    """configs[3] keys of the default line at this N: per radius the row-band sharded 16384^2
+    sepconv through icl_sepconv_sharded (strong scaling), its Mpx/s, and -- from the same run --
+    the unsharded single-GPU time T(1) of the whole image on rank 0's GPU, so
+    E(N) = T(1) / (N * T(N)) is readable from one line (the driver computes its own scaling
+    from the per-N values)."""
+    import torch
+
+    import paper_1605_06399_b200 as icl
+    dev = torch.device("cuda", local)
+    hbm, _ = measured_peaks()
+    out = {}
+    for r in radii:
+        k = max(5, steps)
+        t1 = None
+        if ws > 1:
+            # T(1): the whole image on one GPU (rank 0), the others wait at the barrier
+            if rank == 0:
+                img = torch.empty(S, S, device=dev)
+                icl.fill_uniform(img, 4)
+                o = torch.empty_like(img)
+                fx = synth.gaussian_taps(r)
+                st = torch.cuda.current_stream(dev)
+                for _ in range(3):
+                    icl.sepconv(img, o, fx, fx, "constant", stream=st)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                for _ in range(k):
+                    icl.sepconv(img, o, fx, fx, "constant", stream=st)
+                b.record(st)
+                torch.cuda.synchronize(dev)
+                t1 = a.elapsed_time(b) / k
+                del img, o
+            dist.barrier()
+        res = time_sepconv_bands(S, r, k, 3, ws, rank, local, dist)
+        if ws == 1:
+            t1 = res["ms"]
+        px = S * S
+        e = {"ms": res["ms"], "mpx_s": px / (res["ms"] * 1e-3) / 1e6, "n_gpus": ws,
+             "per_gpu_GBps": 8 * px / ws / (res["ms"] * 1e-3) / 1e9, "exchange": res["exchange"],
+             "variant": res["variant"], "launches": res["launches"], "halo_rows": res["halo_rows"]}
+        e["per_gpu_frac_of_measured_hbm"] = e["per_gpu_GBps"] / hbm
+        if t1 is not None:
+            e["t1_ms_same_run"] = t1
+            e["E_vs_same_run_t1"] = t1 / (ws * res["ms"])
+        out[f"r{r}"] = e
+        torch.cuda.empty_cache()
+    return out
+
+
+def run_sepconv_bands(args):
+    """BASELINE.json configs[3]: one S x S fp32 image, separable Gaussian radius r,
+    row-band sharded over the ranks with the halo exchange overlapped with the interior
+    rows.  Strong scaling (the image is fixed)."""
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = init_dist(ws, "nccl")
+    import paper_1605_06399_b200 as icl
+    icl.load_library()
+    S, r = args.size, args.radius
+    res = time_sepconv_bands(S, r, args.steps, args.warmup, ws, rank, local, dist, halo=args.halo,
+                             torch_comm=args.torch_comm)
+    step_ms = res["ms"]
     px = S * S
     value = px / (step_ms * 1e-3) / 1e6
     hbm, hbm_kind = measured_peaks()
@@ -657,24 +751,13 @@ def run_sepconv_bands(args):
             "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": "sepconv16k (BASELINE.json configs[3])", "size": [S, S], "radius": r,
-                       "border": "constant", "halo_rows": [band.up, band.down],
-                       "exchange": ("icl_sepconv_peer (halo rows loaded in-kernel from the peers, CUDA IPC)"
-                                    if peer else "icl_sepconv_sharded (NCCL in libicl.so)" if native else
-                                    "torch.distributed batch_isend_irecv" if ws > 1 else "none"),
-                       "variant":
-                           icl.variant_names("sepconv")[icl.last_variant("sepconv")],
-                       "l2": "input 1 GiB >> L2; no flush"},
+                       "border": "constant", "halo_rows": res["halo_rows"], "exchange": res["exchange"],
+                       "variant": res["variant"], "l2": "input 1 GiB >> L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": None, "peak_kind": hbm_kind},
-            "gpu_launches": launches, "clocks": clk.summary(), "e2e": None, "cpu_baseline": None,
+            "gpu_launches": res["launches"], "clocks": res["clocks"], "e2e": None, "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
-    if ncomm is not None:
-        ncomm.close()
-    if peer:
-        dist.barrier()  # no rank frees its band while a peer may still read it
-        for p in nbr.values():
-            p.close()
     if ws > 1:
         dist.destroy_process_group()
     return 0
@@ -989,6 +1072,27 @@ def run_chain(args):
     return 0
 
 
+def relaunch(n):
+    """`--gpus N` without a launcher: re-exec this command under torch.distributed.run with N ranks
+    (one process per GPU, 127.0.0.1 rendezvous on a free port) and return its exit code."""
+    import socket
+    import subprocess
+    if not ONE_GPU:
+        import torch
+        have = torch.cuda.device_count()
+        if have < n:
+            print(f"bench.py: --gpus {n} but only {have} CUDA device(s) visible "
+                  f"(ICL_BENCH_ONE_GPU=1 runs every rank on cuda:0 as a functional check)", file=sys.stderr)
+            return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    print("bench.py: launching " + " ".join(cmd[1:]), file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -1004,6 +1108,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tune", action="store_true")
     ap.add_argument("--no-small", action="store_true", help="suite: skip the configs[0..2] latency block")
+    ap.add_argument("--no-16k", action="store_true",
+                    help="suite: skip the configs[3] keys (16384^2 row-band sepconv at r = 2 and 15)")
     ap.add_argument("--torch-comm", action="store_true", help="sepconv16k: exchange halos via torch.distributed")
     ap.add_argument("--halo", default="nccl", choices=["nccl", "peer"],
                     help="sepconv16k, N > 1: NCCL send/recv (icl_sepconv_sharded) or in-kernel peer loads "
@@ -1011,6 +1117,13 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1:
+        return relaunch(args.gpus)
+    if ws_env is not None and int(ws_env) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}; launch one rank per GPU "
+              f"(torch.distributed.run --nproc-per-node {args.gpus}) or drop --gpus", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "conv2d8k":

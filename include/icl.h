@@ -198,6 +198,18 @@ icl_status icl_shard_plan(int64_t global_height, int nranks, int rank, int up, i
 icl_status icl_comm_unique_id(void* id128);
 icl_status icl_comm_init(icl_comm** comm, int nranks, int rank, const void* id128);
 icl_status icl_comm_destroy(icl_comm* comm);
+/* In-process loopback transport (test plumbing for the exchange path, SURVEY.md
+ * §4(vi)): creates `nranks` communicators of ONE process on the current
+ * device, written to comms[0..nranks-1].  The icl_*_sharded calls on them run
+ * the same pack -> exchange -> unpack as over NCCL, the ncclSend / ncclRecv
+ * pair replaced by device copies through per-(src, dst) mailboxes with NCCL's
+ * matching and completion semantics.  Every rank must be driven by its OWN
+ * host thread (a recv blocks the calling thread until the peer's matching
+ * send is posted; a peer that never calls -> ICL_ERR_NCCL after 120 s).
+ * nranks outside [1, ICL_LOCAL_MAX_RANKS] -> ICL_ERR_INVALID_ARG.  Each comm
+ * is released with icl_comm_destroy. */
+#define ICL_LOCAL_MAX_RANKS 16
+icl_status icl_comm_init_local(icl_comm** comms, int nranks);
 /* buf: the rank's band buffer (rows [s0, s1) of the global image, own rows
  * filled by the caller, halo rows filled by the call; device memory, batch
  * allowed); dst (and Harris mask): the rank's rows [r0, r1).  Shapes that do

@@ -30,7 +30,7 @@ EXPORTS = ("icl_sepconv", "icl_sepconv_workspace_bytes", "icl_harris", "icl_nlm"
            "icl_variant_count", "icl_variant_name", "icl_force_variant", "icl_last_variant",
            "icl_launch_count", "icl_transfer_bytes", "icl_last_error", "icl_version", "icl_fill_uniform",
            "icl_halo_rows", "icl_shard_band", "icl_shard_plan", "icl_comm_unique_id", "icl_comm_init",
-           "icl_comm_destroy", "icl_sepconv_sharded", "icl_harris_sharded", "icl_nlm_sharded", "icl_conv2d_u8_sharded",
+           "icl_comm_destroy", "icl_comm_init_local", "icl_sepconv_sharded", "icl_harris_sharded", "icl_nlm_sharded", "icl_conv2d_u8_sharded",
            "icl_tune_ann", "icl_ann_search", "icl_ann_fit", "icl_blur_harris", "icl_blur_harris_workspace_bytes",
            "icl_ipc_get_handle", "icl_ipc_open", "icl_ipc_close", "icl_sepconv_peer",
            "icl_halo_pull", "icl_sepconv3d", "icl_harris_peer")
@@ -110,6 +110,7 @@ def load_library(path: str = LIB_PATH):
         "icl_comm_unique_id": ([P], I),
         "icl_comm_init": ([ctypes.POINTER(P), I, I, P], I),
         "icl_comm_destroy": ([P], I),
+        "icl_comm_init_local": ([ctypes.POINTER(P), I], I),
         "icl_sepconv_sharded": ([P, img, img, I64, P, I, P, I, I, F, P], I),
         "icl_harris_sharded": ([P, img, img, I64, I, F, I, F, img, F, P], I),
         "icl_nlm_sharded": ([P, img, img, I64, I, I, F, I, F, P], I),
@@ -331,6 +332,20 @@ class Comm:
         _check(lib.icl_comm_init(ctypes.byref(self._c), nranks, rank, uid))
         self.nranks, self.rank = nranks, rank
 
+    @classmethod
+    def local_group(cls, nranks: int) -> list:
+        """`nranks` communicators of this process over the in-process loopback transport
+        (icl_comm_init_local); drive each from its own thread."""
+        arr = (ctypes.c_void_p * nranks)()
+        _check(load_library().icl_comm_init_local(arr, nranks))
+        out = []
+        for k in range(nranks):
+            c = cls.__new__(cls)
+            c._c = ctypes.c_void_p(arr[k])
+            c.nranks, c.rank = nranks, k
+            out.append(c)
+        return out
+
     def close(self):
         if self._c:
             _check(load_library().icl_comm_destroy(self._c))
@@ -483,11 +498,14 @@ class PeerImage:
     """A neighbour's band mapped with icl_ipc_open (close() unmaps it)."""
 
     def __init__(self, handle: bytes, offset: int, width: int, height: int, pitch_elems: int, batch: int = 1,
-                 batch_stride_elems: int = 0):
+                 batch_stride_elems: int = 0, elem_size: int = 4):
+        """Pitch and batch stride are in elements of `elem_size` bytes (4: fp32 bands, 1: uint8)."""
+        if elem_size not in (1, 4):
+            raise ValueError("elem_size must be 1 or 4")
         p = ctypes.c_void_p(0)
         _check(load_library().icl_ipc_open(handle, offset, ctypes.byref(p)))
         self.ptr, self.offset = p.value, offset
-        self.image = icl_image(self.ptr, width, height, pitch_elems * 4, batch, batch_stride_elems * 4)
+        self.image = icl_image(self.ptr, width, height, pitch_elems * elem_size, batch, batch_stride_elems * elem_size)
 
     def close(self):
         if self.ptr:

@@ -19,6 +19,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <deque>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -103,6 +106,17 @@ bool partition(int64_t H, int N, int k, int up, int down, Band* b) {
   return !(N > 1 && b->r1 - b->r0 < std::max(up, down));
 }
 
+// The call is collective, so validity must be the same answer on every rank: reject the
+// configuration when ANY rank's band is thinner than the halo (in practice the last one),
+// not only when the calling rank's is -- otherwise a valid neighbour would post a send /
+// recv that the rejecting rank never matches.
+bool config_valid(int64_t H, int N, int up, int down) {
+  Band t;
+  for (int k = 0; k < N; ++k)
+    if (!partition(H, N, k, up, down, &t)) return false;
+  return true;
+}
+
 struct PlanEntry {
   int peer;
   int64_t send0, send1, recv0, recv1;
@@ -113,14 +127,14 @@ int exchange_plan(const Band& b, PlanEntry out[2]) {
   int n = 0;
   if (b.r0 < b.r1 && b.rank > 0) {
     Band prev;
-    partition(b.H, b.N, b.rank - 1, b.up, b.down, &prev);
-    PlanEntry e{b.rank - 1, b.r0, prev.s1, b.s0, b.r0};
-    if (e.send1 > e.send0 || e.recv1 > e.recv0) out[n++] = e;
+    if (partition(b.H, b.N, b.rank - 1, b.up, b.down, &prev)) {
+      PlanEntry e{b.rank - 1, b.r0, prev.s1, b.s0, b.r0};
+      if (e.send1 > e.send0 || e.recv1 > e.recv0) out[n++] = e;
+    }
   }
   if (b.rank < b.N - 1) {
     Band nxt;
-    partition(b.H, b.N, b.rank + 1, b.up, b.down, &nxt);
-    if (nxt.r0 < nxt.r1) {
+    if (partition(b.H, b.N, b.rank + 1, b.up, b.down, &nxt) && nxt.r0 < nxt.r1) {
       PlanEntry e{b.rank + 1, nxt.s0, b.r1, b.r1, b.s1};
       if (e.send1 > e.send0 || e.recv1 > e.recv0) out[n++] = e;
     }
@@ -150,7 +164,31 @@ icl_image rows_of(const icl_image* im, int64_t row0, int64_t nrows) {
 
 using namespace icl;
 
+// In-process loopback transport (icl_comm_init_local): N communicators of ONE process, every
+// rank driven by its own host thread, exchanging the packed halo rows by device copies through
+// per-(src, dst) mailboxes instead of ncclSend / ncclRecv.  It keeps NCCL's matching and
+// completion semantics -- a recv waits for the peer's matching send to be POSTED, copies after
+// the sender's packed rows are ready (event), and a send completes (on the sender's comm
+// stream) only after the receiver's copy -- so run_sharded's pack -> exchange -> unpack runs
+// unchanged at N = 2..8 on one GPU (NCCL refuses two ranks on one device).  Test plumbing for
+// the exchange path, not a product transport.
+struct LocalMsg {
+  const void* src = nullptr;
+  size_t bytes = 0;
+  cudaEvent_t ready = nullptr;  // sender's packed rows complete
+  cudaEvent_t done = nullptr;   // receiver's copy complete
+  bool acked = false;
+};
+
+struct LocalGroup {
+  int n = 0, refs = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<LocalMsg*> box[ICL_LOCAL_MAX_RANKS][ICL_LOCAL_MAX_RANKS];  // [src][dst], FIFO per pair
+};
+
 struct icl_comm {
+  LocalGroup* lg = nullptr;  // non-null: in-process loopback transport
   ncclComm_t nc = nullptr;
   int nranks = 1, rank = 0;
   cudaStream_t cs = nullptr;
@@ -163,14 +201,75 @@ namespace {
 using BandCall = std::function<icl_status(const icl_image* src, const icl_image* dst, const icl_image* mask,
                                           const icl_band* band, cudaStream_t s)>;
 
+// The grouped send / recv of one run_sharded call over the loopback transport: post every
+// send, then serve every recv (host-wait for the peer's post, device copy after its ready
+// event), then wait for the receivers' copies of this rank's sends.  Every rank posts before
+// it blocks, so the group cannot deadlock.
+icl_status local_exchange(icl_comm* c, const PlanEntry* plan, int np, const size_t* off, int64_t row_bytes) {
+  LocalGroup* g = c->lg;
+  LocalMsg* sent[2] = {nullptr, nullptr};
+  cudaError_t e;
+  for (int q = 0; q < np; ++q) {
+    const size_t sb = (size_t)((plan[q].send1 - plan[q].send0) * row_bytes);
+    if (!sb) continue;
+    LocalMsg* m = new LocalMsg();
+    m->src = c->stage + off[2 * q];
+    m->bytes = sb;
+    if ((e = cudaEventCreateWithFlags(&m->ready, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&m->done, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventRecord(m->ready, c->cs)) != cudaSuccess) {
+      delete m;
+      return report_error(ICL_ERR_CUDA, cudaGetErrorString(e));
+    }
+    sent[q] = m;
+    std::lock_guard<std::mutex> lk(g->mu);
+    g->box[c->rank][plan[q].peer].push_back(m);
+    g->cv.notify_all();
+  }
+  const auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(120);
+  for (int q = 0; q < np; ++q) {
+    const size_t rb = (size_t)((plan[q].recv1 - plan[q].recv0) * row_bytes);
+    if (!rb) continue;
+    std::unique_lock<std::mutex> lk(g->mu);
+    auto& bx = g->box[plan[q].peer][c->rank];
+    if (!g->cv.wait_until(lk, deadline, [&] { return !bx.empty(); }))
+      return report_error(ICL_ERR_NCCL, "local transport: the peer never posted its send (is every rank calling?)");
+    LocalMsg* m = bx.front();
+    bx.pop_front();
+    lk.unlock();
+    if (m->bytes != rb) return report_error(ICL_ERR_NCCL, "local transport: send / recv sizes differ");
+    cudaStreamWaitEvent(c->cs, m->ready, 0);
+    if ((e = cudaMemcpyAsync(c->stage + off[2 * q + 1], m->src, rb, cudaMemcpyDeviceToDevice, c->cs)) != cudaSuccess)
+      return report_error(ICL_ERR_CUDA, cudaGetErrorString(e));
+    cudaEventRecord(m->done, c->cs);
+    lk.lock();
+    m->acked = true;
+    g->cv.notify_all();
+  }
+  for (int q = 0; q < np; ++q) {
+    LocalMsg* m = sent[q];
+    if (!m) continue;
+    {
+      std::unique_lock<std::mutex> lk(g->mu);
+      if (!g->cv.wait_until(lk, deadline, [&] { return m->acked; }))
+        return report_error(ICL_ERR_NCCL, "local transport: the peer never received this rank's send");
+    }
+    cudaStreamWaitEvent(c->cs, m->done, 0);  // the send completes once the peer's copy has run
+    cudaEventDestroy(m->ready);  // released by the driver once the pending work completes
+    cudaEventDestroy(m->done);
+    delete m;
+  }
+  return ICL_OK;
+}
+
 // Exchange the halo rows of `buf` and run the filter on the rank's rows of `dst`.
 icl_status run_sharded(icl_comm* c, const icl_image* buf, const icl_image* dst, const icl_image* mask, int64_t H,
                        int up, int down, int elem, const BandCall& call, cudaStream_t user) {
   if (!c) return report_error(ICL_ERR_INVALID_ARG, "null comm");
   if (!buf || !dst || !buf->data || !dst->data) return report_error(ICL_ERR_INVALID_ARG, "null image");
   Band b;
-  if (!partition(H, c->nranks, c->rank, up, down, &b))
-    return report_error(ICL_ERR_INVALID_ARG, "row band thinner than the halo");
+  if (!partition(H, c->nranks, c->rank, up, down, &b) || !config_valid(H, c->nranks, up, down))
+    return report_error(ICL_ERR_INVALID_ARG, "a row band (this rank's or another's) is thinner than the halo");
   if (buf->height != b.s1 - b.s0 || dst->height != b.r1 - b.r0) {
     char m[200];
     snprintf(m, sizeof m, "rank %d: band buffer must hold rows [%lld, %lld) and dst rows [%lld, %lld)", c->rank,
@@ -216,17 +315,22 @@ icl_status run_sharded(icl_comm* c, const icl_image* buf, const icl_image* dst, 
       cudaMemcpy2DAsync(c->stage + off[2 * q] + img * n * rowb, rowb, rows2d(img, plan[q].send0), buf->pitch_bytes,
                         rowb, n, cudaMemcpyDeviceToDevice, c->cs);
   }
-  ncclResult_t r = g_nccl.groupStart();
-  if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
-  for (int q = 0; q < np && r == ncclSuccess; ++q) {
-    const size_t sb = (size_t)((plan[q].send1 - plan[q].send0) * rowb * B);
-    const size_t rb = (size_t)((plan[q].recv1 - plan[q].recv0) * rowb * B);
-    if (sb) r = g_nccl.send(c->stage + off[2 * q], sb, ncclUint8, plan[q].peer, c->nc, c->cs);
-    if (r == ncclSuccess && rb) r = g_nccl.recv(c->stage + off[2 * q + 1], rb, ncclUint8, plan[q].peer, c->nc, c->cs);
+  if (c->lg) {
+    icl_status xs = local_exchange(c, plan, np, off, rowb * B);
+    if (xs != ICL_OK) return xs;
+  } else {
+    ncclResult_t r = g_nccl.groupStart();
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
+    for (int q = 0; q < np && r == ncclSuccess; ++q) {
+      const size_t sb = (size_t)((plan[q].send1 - plan[q].send0) * rowb * B);
+      const size_t rb = (size_t)((plan[q].recv1 - plan[q].recv0) * rowb * B);
+      if (sb) r = g_nccl.send(c->stage + off[2 * q], sb, ncclUint8, plan[q].peer, c->nc, c->cs);
+      if (r == ncclSuccess && rb) r = g_nccl.recv(c->stage + off[2 * q + 1], rb, ncclUint8, plan[q].peer, c->nc, c->cs);
+    }
+    ncclResult_t r2 = g_nccl.groupEnd();
+    if (r != ncclSuccess) return nccl_fail(r, "ncclSend/ncclRecv");
+    if (r2 != ncclSuccess) return nccl_fail(r2, "ncclGroupEnd");
   }
-  ncclResult_t r2 = g_nccl.groupEnd();
-  if (r != ncclSuccess) return nccl_fail(r, "ncclSend/ncclRecv");
-  if (r2 != ncclSuccess) return nccl_fail(r2, "ncclGroupEnd");
   for (int q = 0; q < np; ++q) {  // unpack
     const int64_t n = plan[q].recv1 - plan[q].recv0;
     for (int64_t img = 0; img < B && n > 0; ++img)
@@ -334,9 +438,44 @@ icl_status icl_comm_init(icl_comm** comm, int nranks, int rank, const void* id) 
   return ICL_OK;
 }
 
+icl_status icl_comm_init_local(icl_comm** comms, int nranks) {
+  if (!comms || nranks < 1 || nranks > ICL_LOCAL_MAX_RANKS)
+    return report_error(ICL_ERR_INVALID_ARG, "nranks must be in [1, ICL_LOCAL_MAX_RANKS]");
+  LocalGroup* g = new LocalGroup();
+  g->n = nranks;
+  for (int k = 0; k < nranks; ++k) {
+    icl_comm* c = new icl_comm();
+    c->lg = g;
+    c->nranks = nranks;
+    c->rank = k;
+    cudaError_t e;
+    if ((e = cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming)) != cudaSuccess) {
+      for (int j = 0; j < k; ++j) icl_comm_destroy(comms[j]);
+      if (c->cs) cudaStreamDestroy(c->cs);
+      delete c;
+      if (k == 0) delete g;
+      return report_error(ICL_ERR_CUDA, cudaGetErrorString(e));
+    }
+    g->refs++;
+    comms[k] = c;
+  }
+  return ICL_OK;
+}
+
 icl_status icl_comm_destroy(icl_comm* comm) {
   if (!comm) return ICL_OK;
   if (comm->cs) cudaStreamSynchronize(comm->cs);
+  if (comm->lg) {
+    LocalGroup* g = comm->lg;
+    bool last;
+    {
+      std::lock_guard<std::mutex> lk(g->mu);
+      last = --g->refs == 0;
+    }
+    if (last) delete g;
+  }
   ncclResult_t r = comm->nc ? g_nccl.commDestroy(comm->nc) : ncclSuccess;
   if (comm->fork) cudaEventDestroy(comm->fork);
   if (comm->join) cudaEventDestroy(comm->join);

@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(256) nlm_boxsum(NlmParams p) {
         float d = hv[j];
 #pragma unroll
         for (int t = 1; t < PW; ++t) d = __fadd_rn(d, hv[j + t]);
-        const float w = ex2_approx(-__fmul_rn(d, p.coef));
+        const float w = ex2_approx(-__fmul_rn(fmaxf(d, 0.0f), p.coef));
         num[j] = __fmaf_rn(w, qc[j * UW], num[j]);
         den[j] = __fadd_rn(den[j], w);
       }

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(256, 3) nlm_box_r16(NlmParams p) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           if (j > 0) d = __fadd_rn(__fadd_rn(d, hv[j + 2 * P]), -hv[j - 1]);
-          const float w = ex2_approx(__fmul_rn(d, nc));
+          const float w = ex2_approx(__fmul_rn(fmaxf(d, 0.0f), nc));  // sliding sums can round below 0
           num[j] = __fmaf_rn(w, qc[j * UW], num[j]);
           den[j] = __fadd_rn(den[j], w);
         }

@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(256, 2) nlm_box_x2(NlmParams p, int ntx, int n
 #pragma unroll
         for (int j = 0; j < RUN; ++j) {
           if (j > 0) d = f2_add(f2_add(d, hv[j + 2 * P]), make_float2(-hv[j - 1].x, -hv[j - 1].y));
-          const float2 t = f2_mul(d, nc);
+          // sliding sums can round below 0; a negative d with a tiny h would give w = inf
+          const float2 t = f2_mul(make_float2(fmaxf(d.x, 0.0f), fmaxf(d.y, 0.0f)), nc);
           const float2 w = make_float2(ex2_approx(t.x), ex2_approx(t.y));
           num[j] = f2_fma(w, qc[j * UW], num[j]);
           den[j] = f2_add(den[j], w);

@@ -21,6 +21,8 @@
 // static, pre-sharded input such as BASELINE configs[3]).
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cmath>
+#include <cstdio>
 
 #include <algorithm>
 #include <cstring>
@@ -249,12 +251,37 @@ icl_status icl_ipc_close(void* dev_ptr, uint64_t offset) {
   return e == cudaSuccess ? ICL_OK : report_error(ICL_ERR_CUDA, cudaGetErrorString(e));
 }
 
+// Descriptor checks every peer entry point runs up front (own / dst / neighbour bands), so a
+// thin band whose interior call is skipped never launches an edge kernel on unchecked
+// descriptors.
+static icl_status check_peer_image(const icl_image* im, int64_t elem, const char* name) {
+  char m[160];
+  if (!im || !im->data) {
+    snprintf(m, sizeof m, "%s: null image", name);
+    return report_error(ICL_ERR_INVALID_ARG, m);
+  }
+  if (im->width < 1 || im->height < 1 || im->batch < 1 || im->pitch_bytes < im->width * elem ||
+      im->pitch_bytes % elem != 0 ||
+      (im->batch > 1 && im->batch_stride_bytes < im->pitch_bytes * im->height)) {
+    snprintf(m, sizeof m, "%s: bad width / height / pitch / batch stride", name);
+    return report_error(ICL_ERR_INVALID_ARG, m);
+  }
+  return ICL_OK;
+}
+
 icl_status icl_sepconv_peer(const icl_image* own, const icl_image* dst, int64_t global_height, int64_t own_y0,
                             const icl_image* up, const icl_image* down, const float* taps_x, int rx,
                             const float* taps_y, int ry, icl_border border, float border_value, void* stream) {
   if (!own || !dst || !taps_x || !taps_y) return report_error(ICL_ERR_INVALID_ARG, "null argument");
   if (rx < 0 || ry < 0 || rx > kMaxRadius || ry > kMaxRadius)
     return report_error(ICL_ERR_INVALID_ARG, "radius outside [0, 15]");
+  if (border != ICL_BORDER_CONSTANT && border != ICL_BORDER_CLAMP)
+    return report_error(ICL_ERR_INVALID_ARG, "border must be ICL_BORDER_CONSTANT or ICL_BORDER_CLAMP");
+  if (std::isnan(border_value)) return report_error(ICL_ERR_INVALID_ARG, "border_value is NaN");
+  {
+    icl_status st0;
+    if ((st0 = check_peer_image(own, 4, "own")) || (st0 = check_peer_image(dst, 4, "dst"))) return st0;
+  }
   const int64_t H = global_height, y0 = own_y0, y1 = own_y0 + own->height;
   if (H < 1 || H >= (1ll << 31) || y0 < 0 || y1 > H || dst->height != own->height || dst->width != own->width ||
       dst->batch != own->batch || own->width < 1 || own->height < 1 || own->batch < 1 || own->batch > 65535)
@@ -263,7 +290,8 @@ icl_status icl_sepconv_peer(const icl_image* own, const icl_image* dst, int64_t 
   const int64_t need_up = std::min<int64_t>(ry, y0), need_dn = std::min<int64_t>(ry, H - y1);
   auto check_nb = [&](const icl_image* nb, int64_t need, const char* which) -> icl_status {
     if (need == 0) return ICL_OK;
-    if (!nb || !nb->data || nb->height < need || nb->width != own->width || nb->batch != own->batch)
+    if (!nb || !nb->data || nb->height < need || nb->width != own->width || nb->batch != own->batch ||
+        check_peer_image(nb, 4, which) != ICL_OK)
       return report_error(ICL_ERR_INVALID_ARG, which);
     return ICL_OK;
   };
@@ -334,6 +362,11 @@ icl_status icl_harris_peer(const icl_image* own, const icl_image* response, int6
   if (block < 1 || block > 7) return report_error(ICL_ERR_INVALID_ARG, "block must be in [1, 7]");
   if (border != ICL_BORDER_CONSTANT && border != ICL_BORDER_CLAMP)
     return report_error(ICL_ERR_INVALID_ARG, "border must be ICL_BORDER_CONSTANT or ICL_BORDER_CLAMP");
+  if (std::isnan(border_value) || std::isnan(k)) return report_error(ICL_ERR_INVALID_ARG, "border_value or k is NaN");
+  {
+    icl_status st0;
+    if ((st0 = check_peer_image(own, 4, "own")) || (st0 = check_peer_image(response, 4, "response"))) return st0;
+  }
   const int64_t H = global_height, y0 = own_y0, y1 = own_y0 + own->height;
   if (H < 1 || H >= (1ll << 31) || y0 < 0 || y1 > H || response->height != own->height ||
       response->width != own->width || response->batch != own->batch || own->width < 1 || own->height < 1 ||
@@ -346,7 +379,8 @@ icl_status icl_harris_peer(const icl_image* own, const icl_image* response, int6
   const int64_t need_up = std::min<int64_t>(hu, y0), need_dn = std::min<int64_t>(hdn, H - y1);
   auto check_nb = [&](const icl_image* nb, int64_t need, const char* which) -> icl_status {
     if (need == 0) return ICL_OK;
-    if (!nb || !nb->data || nb->height < need || nb->width != own->width || nb->batch != own->batch)
+    if (!nb || !nb->data || nb->height < need || nb->width != own->width || nb->batch != own->batch ||
+        check_peer_image(nb, 4, which) != ICL_OK)
       return report_error(ICL_ERR_INVALID_ARG, which);
     return ICL_OK;
   };
@@ -419,7 +453,8 @@ icl_status icl_harris_peer(const icl_image* own, const icl_image* response, int6
 
 icl_status icl_halo_pull(const icl_image* buf, int64_t global_height, int64_t buf_y0, int64_t own_y0,
                          int64_t own_y1, const icl_image* up, const icl_image* down, int elem_bytes, void* stream) {
-  if (!buf || !buf->data || (elem_bytes != 1 && elem_bytes != 4)) return report_error(ICL_ERR_INVALID_ARG, "bad buffer");
+  if (!buf || !buf->data || (elem_bytes != 1 && elem_bytes != 4) || check_peer_image(buf, elem_bytes, "buf") != ICL_OK)
+    return report_error(ICL_ERR_INVALID_ARG, "bad buffer");
   const int64_t H = global_height, s0 = buf_y0, s1 = buf_y0 + buf->height;
   if (H < 1 || s0 < 0 || s1 > H || own_y0 < s0 || own_y1 > s1 || own_y0 > own_y1 || buf->batch < 1 ||
       buf->batch > 65535)
@@ -429,8 +464,8 @@ icl_status icl_halo_pull(const icl_image* buf, int64_t global_height, int64_t bu
   auto pull = [&](const icl_image* nb, int64_t nb_y0, int64_t g0, int64_t g1) -> icl_status {
     if (g1 <= g0) return ICL_OK;
     if (!nb || !nb->data || nb->width != buf->width || nb->batch != buf->batch || g0 < nb_y0 ||
-        g1 > nb_y0 + nb->height)
-      return report_error(ICL_ERR_INVALID_ARG, "neighbour band does not hold the halo rows");
+        g1 > nb_y0 + nb->height || check_peer_image(nb, elem_bytes, "neighbour") != ICL_OK)
+      return report_error(ICL_ERR_INVALID_ARG, "neighbour band does not hold the halo rows (rows, pitch or stride)");
     PullParams p;
     p.src = static_cast<const char*>(nb->data) + (g0 - nb_y0) * nb->pitch_bytes;
     p.spitch = nb->pitch_bytes;

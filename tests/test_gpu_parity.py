@@ -364,6 +364,27 @@ def test_nlm_limits():
     np.testing.assert_allclose(host(d[:30, :40]), np.float32(0.4), rtol=1e-6)
 
 
+@pytest.mark.parametrize("P,S", [(0, 1), (0, 5), (1, 3), (1, 5), (2, 5), (3, 4)])
+def test_nlm_tiny_h_quantized(P, S):
+    """sliding patch sums ((h + new^2) - old^2) can round below zero; with a tiny h a
+    negative distance would give w = +inf and a NaN output.  Quantised k/255 pixels make equal
+    patches common (d = 0 exactly in the definition); every variant must return the input
+    (h -> 0 limit, SURVEY.md §8(c) pin) and match the oracle."""
+    rng = np.random.default_rng(100 + 10 * P + S)
+    img = (rng.integers(0, 256, (61, 83)) / 255.0).astype(np.float32)
+    img[20:40, 10:50] = np.float32(7 / 255)  # flat block: many exactly-equal patches
+    src = to_dev(img)
+
+    def call():
+        dst = empty_like_dev(61, 83)
+        icl.nlm(src, dst, P, S, 1e-6, "clamp")
+        return host(dst)
+
+    for name, o in run_all_variants("nlm", call).items():
+        assert np.isfinite(o).all(), name
+        check_nlm(o, img, P, S, 1e-6, "clamp", 0.0)
+
+
 @pytest.mark.parametrize("border", ["constant", "clamp"])
 def test_nlm_bands(border):
     H, W, P, S = 90, 75, 2, 5
