@@ -244,6 +244,9 @@ static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
     const bool ok_border = sv.border == kBorderClamp || sv.cval == 0.0f;
     if (!tex_eligible(sv, sv.Hg - sv.y0, bt, pc.f == ICL_FILTER_CONV2D ? 1 : 4, ok_border)) return false;
   }
+  if (pc.f == ICL_FILTER_SEPCONV && !pc.sep.pad_rows_ok &&
+      (v.kind == K_STREAM || v.kind == K_BULK || v.kind == K_TILE2 || v.kind == K_TEX))
+    return false;  // padded-radius variant in a band without max(rx, ry) halo rows
   if (pc.f == ICL_FILTER_SEPCONV && v.kind == K_STREAM &&
       sep_stream_smem_bytes(v.nt, pc.sep.rx > pc.sep.ry ? pc.sep.rx : pc.sep.ry) > 227 * 1024)
     return false;
@@ -488,6 +491,11 @@ static icl_status prep_sepconv(const icl_image* src, const icl_image* dst, const
   pc->sep.gy = ty;
   pc->sep.workspace = ws;
   pc->sep.workspace_bytes = wsb;
+  {
+    const int64_t R = std::max(rx, ry), Hg = pc->sep.src.Hg, sy0 = pc->sep.src.y0, dy0 = pc->sep.dst.y0;
+    const int64_t lo = std::max<int64_t>(0, dy0 - R), hi = std::min<int64_t>(Hg - 1, dy0 + dst->height - 1 + R);
+    pc->sep.pad_rows_ok = lo >= sy0 && hi <= sy0 + src->height - 1;
+  }
   if (ws && wsb) {
     Range w{reinterpret_cast<uintptr_t>(ws), reinterpret_cast<uintptr_t>(ws) + wsb};
     if (overlap(w, byte_range(src, 4)) || overlap(w, byte_range(dst, 4)))

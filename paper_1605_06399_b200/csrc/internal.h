@@ -23,6 +23,10 @@ struct SepCall {
   const float* gy;  // host, 2ry+1
   void* workspace;
   size_t workspace_bytes;
+  // the src rows cover R = max(rx, ry) rows around the dst rows (always true without a band):
+  // the fused variants pad the taps to R and READ those rows (times a zero tap), so in a band
+  // holding only ry halo rows they are ineligible (they would read outside the band buffer)
+  bool pad_rows_ok;
 };
 
 struct HarrisCall {

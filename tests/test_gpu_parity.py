@@ -217,6 +217,38 @@ def test_sepconv_bands_bit_exact_all_variants_r9(border):
             np.testing.assert_array_equal(host(dst), ref[a:b], err_msg=f"{name} band {a}:{b}")
 
 
+@pytest.mark.parametrize("rx,ry", [(2, 1), (7, 2), (15, 0), (1, 3)])
+def test_sepconv_bands_unequal_radii_stay_inside_the_buffer(rx, ry):
+    """A band holding only ry halo rows with rx > ry: the fused variants pad the taps to
+    max(rx, ry) and would read rows outside the band buffer (found by the N-rank loopback
+    exchange); they are ineligible there, and every variant that runs must equal the unsharded
+    call.  The band buffer sits between NaN guard rows, so any such read shows up as NaN."""
+    H, W = 150, 260
+    img = synth.uniform_image(31 + rx, H, W)
+    fx, gy = synth.gaussian_taps(rx), synth.gaussian_taps(ry)
+    full = empty_like_dev(H, W)
+    icl.sepconv(to_dev(img), full, fx, gy, "clamp")
+    ref = host(full)
+    G = 16
+    for vid, name in [(None, "default")] + list(variants("sepconv")):
+        if name == "naive_2pass":
+            continue
+        icl.force_variant("sepconv", vid)
+        for a, b in ((0, 1), (1, 60), (60, 61), (61, 149), (149, 150)):
+            s0, s1 = max(0, a - ry), min(H, b + ry)
+            big = torch.full((s1 - s0 + 2 * G, W), float("nan"), device=DEV)
+            big[G:G + s1 - s0] = torch.from_numpy(img[s0:s1]).to(DEV)
+            dst = empty_like_dev(b - a, W)
+            try:
+                icl.sepconv(big[G:G + s1 - s0], dst, fx, gy, "clamp", band=(H, s0, a))
+            except icl.IclError as e:
+                if e.status in (3, 4):
+                    continue
+                raise
+            np.testing.assert_array_equal(host(dst), ref[a:b], err_msg=f"{name} band {a}:{b}")
+    icl.force_variant("sepconv", None)
+
+
 @pytest.mark.parametrize("border", ["constant", "clamp"])
 def test_sepconv_bands_bit_exact(border):
     """Row bands (icl_band) stitched == the unsharded call, bit for bit."""
