@@ -32,6 +32,7 @@ bool nlm_boxsum_supported(int P, int S);
 bool nlm_r8_supported(int P, int S);
 bool nlm_r16_supported(int P, int S);
 bool nlm_x2_supported(int P, int S);
+bool nlm_w_supported(int P, int S);
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -137,7 +138,7 @@ static icl_status make_views(const icl_image* src, const icl_image* dst, const i
 }
 
 // ------------------------------------------------------------------ variants
-enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL, K_TILE2, K_BOXX2, K_C2TILE, K_TEX };
+enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL, K_TILE2, K_BOXX2, K_C2TILE, K_TEX, K_SLIDE, K_BOXW, K_COUNT };
 struct Variant {
   const char* name;
   Kind kind;
@@ -177,6 +178,11 @@ static const Variant kHarVariants[] = {
     {"shfl_nw2_s128", K_SHFL, 2, 4, 128},         {"shfl_nw2_s16", K_SHFL, 2, 4, 16},
     {"shfl_nw2_s8", K_SHFL, 2, 4, 8},             {"shfl_nw4_s16", K_SHFL, 4, 4, 16},
     {"shfl_nw4_s8", K_SHFL, 4, 4, 8},
+    // separable window sums on the products (re-associated: tolerance vs naive, R16)
+    {"slide_nw2_s32", K_SLIDE, 2, 4, 32},         {"slide_nw2_s16", K_SLIDE, 2, 4, 16},
+    {"slide_nw2_s64", K_SLIDE, 2, 4, 64},         {"slide_nw2_s8", K_SLIDE, 2, 4, 8},
+    {"slide_nw4_s32", K_SLIDE, 4, 4, 32},         {"slide_nw4_s16", K_SLIDE, 4, 4, 16},
+    {"slide_nw2_s32_u2", K_SLIDE, 2, 8, 32},      {"slide_nw2_s16_u2", K_SLIDE, 2, 8, 16},
 };
 static const Variant kNlmVariants[] = {
     {"naive_direct", K_NAIVE, 0, 0, 0},
@@ -185,6 +191,7 @@ static const Variant kNlmVariants[] = {
     {"boxsum_r8", K_BOXR8, 0, 0, 0},
     {"boxsum_r16", K_BOXR16, 0, 0, 0},
     {"boxsum_x2", K_BOXX2, 0, 0, 0},
+    {"boxsum_w", K_BOXW, 0, 0, 0},
 };
 
 static const Variant kConvVariants[] = {
@@ -233,10 +240,12 @@ struct Prepared {
 
 static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
   *why = ICL_ERR_UNSUPPORTED;
-  if ((v.kind == K_STREAM || v.kind == K_BULK || v.kind == K_SHFL || v.kind == K_TILE2 || v.kind == K_C2TILE) &&
-      v.vec == 4 && !pc.a16)
+  if ((v.kind == K_STREAM || v.kind == K_BULK || v.kind == K_SHFL || v.kind == K_TILE2 || v.kind == K_C2TILE ||
+       v.kind == K_SLIDE) &&
+      v.vec >= 4 && !pc.a16)
     return false;
-  if (v.kind == K_SHFL && pc.har.block > 5) return false;
+  if ((v.kind == K_SHFL || v.kind == K_SLIDE) && pc.har.block > 5) return false;
+  if (v.kind == K_SLIDE && pc.har.naive_order) return false;
   if (v.kind == K_TEX) {  // hardware boundary: clamp, or constant 0 (border addressing)
     const SrcView& sv = pc.f == ICL_FILTER_SEPCONV ? pc.sep.src : pc.c2d.src;
     const int bt = pc.f == ICL_FILTER_SEPCONV ? pc.sep.batch : pc.c2d.batch;
@@ -262,6 +271,7 @@ static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXR8 && !nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXR16 && !nlm_r16_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXX2 && !nlm_x2_supported(pc.nlm.P, pc.nlm.S)) return false;
+  if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXW && !nlm_w_supported(pc.nlm.P, pc.nlm.S)) return false;
   return true;
 }
 
@@ -340,6 +350,7 @@ static cudaError_t run_variant_1(const Prepared& pc, const Variant& v, cudaStrea
     case ICL_FILTER_HARRIS:
       if (v.kind == K_NAIVE) return launch_harris_naive(pc.har, s);
       if (v.kind == K_SHFL) return launch_harris_shfl(pc.har, v.nt, v.S, s);
+      if (v.kind == K_SLIDE) return launch_harris_slide(pc.har, v.nt, v.vec == 8 ? 2 : 1, v.S, s);
       return launch_harris_stream(pc.har, v.nt, v.vec, v.S, s);
     case ICL_FILTER_NLM:
       if (v.kind == K_NAIVE) return launch_nlm_naive(pc.nlm, s);
@@ -347,6 +358,7 @@ static cudaError_t run_variant_1(const Prepared& pc, const Variant& v, cudaStrea
       if (v.kind == K_BOXR8) return launch_nlm_r8(pc.nlm, s);
       if (v.kind == K_BOXR16) return launch_nlm_r16(pc.nlm, s);
       if (v.kind == K_BOXX2) return launch_nlm_x2(pc.nlm, s);
+      if (v.kind == K_BOXW) return launch_nlm_w(pc.nlm, s);
       return launch_nlm_boxsum(pc.nlm, 0, s);
     case ICL_FILTER_CONV2D:
       if (v.kind == K_NAIVE) return launch_conv2d_naive(pc.c2d, s);
@@ -385,6 +397,8 @@ static int default_variant(const Prepared& pc) {
     case ICL_FILTER_HARRIS:
       if (!pc.a16) return variant_id(pc.f, "stream_nt64_s64_v1");
       if (pc.har.block > 5) return variant_id(pc.f, pc.pixels < (1 << 20) ? "stream_nt32_s16_v4" : "stream_nt64_s64_v4");
+      // (the slide<> family -- separable window sums on the products -- is a tuner candidate only:
+      // 0.417-0.42 vs 0.398 ms on 8 x 4096^2; the default keeps the naive order)
       if (pc.pixels < (1 << 16)) return variant_id(pc.f, "stream_nt32_s16_v4");
       // 240-column strips: short row segments keep enough CTAs in flight up to one 4096^2 image
       // (1024^2 24.5 vs 34.8 us, 2048^2 30.7 vs 66 us, 4096^2 76 vs 90 us; 8 x 4096^2 prefers s64)
@@ -539,6 +553,7 @@ static icl_status prep_harris(const icl_image* src, const icl_image* resp, int b
   pc->har.block = block;
   pc->har.k = k;
   pc->har.threshold = thr;
+  pc->har.naive_order = false;
   pc->a16 = aligned16(src) && aligned16(resp) && mask_a4;
   pc->pixels = src->width * resp->height * src->batch;
   pc->dst_bytes_compact = (size_t)pc->pixels * 4;
@@ -622,6 +637,29 @@ __global__ void compare_kernel(const char* a, int64_t apitch, int64_t abstride, 
     }
 }
 
+// Harris acceptance (SURVEY.md §8(c) tolerance): a variant's R must satisfy
+// |R - R_naive| <= tol * D(p) per pixel (D from harris_dhat; exact 0 where D = 0), and its mask
+// must equal R_naive > t except where |R_naive - t| <= tol * D(p).  out[0] = #bad R, out[1] = #bad mask.
+__global__ void compare_harris_kernel(const char* a, int64_t apitch, int64_t abstride, const char* m, int64_t mpitch,
+                                      int64_t mbstride, const float* ref, const float* dh, int W, int H, int64_t nb,
+                                      float thr, float tol, unsigned long long* out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= W) return;
+  for (int64_t b = blockIdx.z; b < nb; b += gridDim.z)
+    for (int y = blockIdx.y; y < H; y += gridDim.y) {
+      const float va = reinterpret_cast<const float*>(a + b * abstride + (int64_t)y * apitch)[x];
+      const int64_t i = (b * H + y) * W + x;
+      const float vr = ref[i], d = dh[i];
+      const bool okr = d > 0.0f ? fabsf(va - vr) <= tol * d : va == vr;
+      if (!okr) atomicAdd(out, 1ull);
+      if (m) {
+        const unsigned char mv = (unsigned char)m[b * mbstride + (int64_t)y * mpitch + x];
+        const bool want = vr > thr;
+        if ((mv != 0) != want && !(fabsf(vr - thr) <= tol * d)) atomicAdd(out + 1, 1ull);
+      }
+    }
+}
+
 static std::mutex g_tune_mu;
 static void* g_flush = nullptr;
 static size_t g_flush_bytes = 0;
@@ -691,6 +729,14 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
     cudaFree(cmp);
     return cuda_fail(e, "tune: reference");
   }
+  // Harris: the per-pixel scale D of the tolerance (one extra naive-order pass)
+  float* dhat = nullptr;
+  if (pc.f == ICL_FILTER_HARRIS && cudaMalloc(&dhat, pc.dst_bytes_compact) == cudaSuccess &&
+      launch_harris_dhat(pref.har, dhat, s) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(dhat);
+    dhat = nullptr;  // (shapes beyond one launch: the global criterion below)
+  }
   cudaEvent_t ev0, ev1;
   cudaEventCreate(&ev0);
   cudaEventCreate(&ev1);
@@ -703,6 +749,15 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
     if (!(flags & ICL_TUNE_NO_VERIFY) && v != 0) {
       cudaMemsetAsync(cmp, 0, 3 * sizeof(unsigned long long), s);
       dim3 g((W + 255) / 256, H < 65535 ? H : 65535, batch < 65535 ? batch : 65535);
+      if (dhat) {
+        compare_harris_kernel<<<g, 256, 0, s>>>(real_dst.base, real_dst.pitch, real_dst.bstride, pc.har.mask,
+                                                pc.har.mpitch, pc.har.mbstride, ref, dhat, W, H, batch,
+                                                pc.har.threshold, 1e-4f, cmp);
+        unsigned long long hc[3];
+        cudaMemcpyAsync(hc, cmp, sizeof hc, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        if (hc[0] != 0 || hc[1] != 0) { ++nrej; return false; }
+      } else {
       compare_kernel<<<g, 256, 0, s>>>(real_dst.base, real_dst.pitch, real_dst.bstride, ref, W, H, batch, cmp);
       unsigned long long hc[3];
       cudaMemcpyAsync(hc, cmp, sizeof hc, cudaMemcpyDeviceToHost, s);
@@ -715,6 +770,7 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
       const bool exact = pc.f == ICL_FILTER_SEPCONV || pc.f == ICL_FILTER_CONV2D;
       const bool ok = exact ? hc[0] == 0 : md <= 1e-4f * std::max(mr, 1e-30f);
       if (!ok) { ++nrej; return false; }
+      }
     }
     // warm-up then timed reps (median)
     for (int w = 0; w < 2; ++w) run_variant(pc, vt[v], s);
@@ -750,7 +806,7 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
       icl_status why;
       if (eligible(pc, vt[v], &why)) ids.push_back(v);
     }
-    constexpr int NK = K_TEX + 1, NF = NK + 3;
+    constexpr int NK = K_COUNT, NF = NK + 3;
     std::vector<double> feats(ids.size() * NF, 0.0);
     for (size_t i = 0; i < ids.size(); ++i) {
       const Variant& vv = vt[ids[i]];
@@ -795,6 +851,7 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
   cudaStreamSynchronize(s);
   cudaFree(ref);
   cudaFree(cmp);
+  if (dhat) cudaFree(dhat);
   if (st == ICL_OK && (e = cudaGetLastError()) != cudaSuccess) st = cuda_fail(e, "tune");
   return st;
 }
@@ -1018,21 +1075,38 @@ size_t icl_sepconv_workspace_bytes(int64_t width, int64_t height, int64_t batch,
   return sep_2pass_workspace(width, height, batch, ry);
 }
 
-icl_status icl_harris(const icl_image* src, const icl_image* response, int block, float k, icl_border border,
-                      float border_value, const icl_image* mask, float threshold, const icl_band* band,
-                      void* stream) {
+static icl_status harris_impl(const icl_image* src, const icl_image* response, int block, float k,
+                              icl_border border, float border_value, const icl_image* mask, float threshold,
+                              const icl_band* band, void* stream, bool naive_order) {
   Prepared pc;
   icl_status st = prep_harris(src, response, block, k, border, border_value, mask, threshold, band, &pc);
   if (st != ICL_OK) return st;
+  pc.har.naive_order = naive_order;
   if (any_host(src, response, mask)) {
     const int a = block / 2, bb = block - 1 - a;
     return run_host(src, response, mask, band, a + 1, bb + 1,
                     [&](const icl_image* s, const icl_image* d, const icl_image* m, const icl_band* b, cudaStream_t cs) {
-                      return icl_harris(s, d, block, k, border, border_value, m, threshold, b, cs);
+                      return harris_impl(s, d, block, k, border, border_value, m, threshold, b, cs, naive_order);
                     },
                     static_cast<cudaStream_t>(stream));
   }
   return dispatch(pc, static_cast<cudaStream_t>(stream));
+}
+
+extern "C++" {
+namespace icl {
+icl_status harris_naive_order(const icl_image* src, const icl_image* response, int block, float k, icl_border border,
+                              float border_value, const icl_image* mask, float threshold, const icl_band* band,
+                              void* stream) {
+  return harris_impl(src, response, block, k, border, border_value, mask, threshold, band, stream, true);
+}
+}  // namespace icl
+}  // extern "C++"
+
+icl_status icl_harris(const icl_image* src, const icl_image* response, int block, float k, icl_border border,
+                      float border_value, const icl_image* mask, float threshold, const icl_band* band,
+                      void* stream) {
+  return harris_impl(src, response, block, k, border, border_value, mask, threshold, band, stream, false);
 }
 
 icl_status icl_blur_harris(const icl_image* src, const icl_image* response, const float* taps_x, int rx,
@@ -1078,7 +1152,8 @@ icl_status icl_blur_harris(const icl_image* src, const icl_image* response, cons
     icl_band bs{Hg, sy0, m0}, bh{Hg, m0, dy0};
     if ((st = icl_sepconv(src, &mid, taps_x, rx, taps_y, ry, blur_border, blur_border_value, &bs, nullptr, 0, stream)))
       return st;
-    return icl_harris(&mid, response, block, k, border, border_value, mask, threshold, &bh, stream);
+    // the naive-order Harris variants: the fused kernel's consumer keeps that order (bit-identical)
+    return harris_naive_order(&mid, response, block, k, border, border_value, mask, threshold, &bh, stream);
   }
   const int S = pc.pixels <= (1 << 25) ? 16 : 64;
   if (src->batch > 65535 || (pc.har.dst.H + S - 1) / S > 65535)

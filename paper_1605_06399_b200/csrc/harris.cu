@@ -106,6 +106,52 @@ cudaError_t launch_harris_shfl(const HarrisCall& c, int nw, int S, cudaStream_t 
   return cudaErrorInvalidValue;
 }
 
+template <int NW, int UNR>
+cudaError_t dispatch_hslide(const HarrisParams& p, int batch, int S, cudaStream_t s);
+extern template cudaError_t dispatch_hslide<2, 1>(const HarrisParams&, int, int, cudaStream_t);
+extern template cudaError_t dispatch_hslide<4, 1>(const HarrisParams&, int, int, cudaStream_t);
+extern template cudaError_t dispatch_hslide<2, 2>(const HarrisParams&, int, int, cudaStream_t);
+extern template cudaError_t dispatch_hslide<4, 2>(const HarrisParams&, int, int, cudaStream_t);
+
+// unr: the step loop of interior CTAs unrolled by 1 or 2 (two independent Sobel rows in flight)
+cudaError_t launch_harris_slide(const HarrisCall& c, int nw, int unr, int S, cudaStream_t s) {
+  HarrisParams p = make_params(c);
+  if (nw == 2) return unr == 2 ? dispatch_hslide<2, 2>(p, c.batch, S, s) : dispatch_hslide<2, 1>(p, c.batch, S, s);
+  if (nw == 4) return unr == 2 ? dispatch_hslide<4, 2>(p, c.batch, S, s) : dispatch_hslide<4, 1>(p, c.batch, S, s);
+  return cudaErrorInvalidValue;
+}
+
+// The tuner's per-pixel scale for Harris variants that re-associate the window sums
+// (SURVEY.md §8(c) tolerance): D(p) = |Sxx Syy| + Sxy^2 + k (Sxx + Syy)^2, the magnitude of
+// the terms that cancel in R, from the naive per-output order, into a compact W x H x batch
+// buffer.
+__global__ void __launch_bounds__(256) harris_dhat(HarrisParams p, float* out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ly = blockIdx.y * blockDim.y + threadIdx.y;
+  const int b = blockIdx.z;
+  if (x >= p.src.W || ly >= p.dst.H) return;
+  const int y = p.dst.y0 + ly;
+  const int a = p.block / 2, bb = p.block - 1 - a;
+  float sxx = 0.0f, sxy = 0.0f, syy = 0.0f;
+  for (int ty = -a; ty <= bb; ++ty)
+    for (int tx = -a; tx <= bb; ++tx) {
+      float dx, dy;
+      sobel_B(p.src, b, x + tx, y + ty, dx, dy);
+      sxx = __fmaf_rn(dx, dx, sxx);
+      sxy = __fmaf_rn(dx, dy, sxy);
+      syy = __fmaf_rn(dy, dy, syy);
+    }
+  const float tr = sxx + syy;
+  out[((int64_t)b * p.dst.H + ly) * p.src.W + x] = fabsf(sxx * syy) + sxy * sxy + fabsf(p.k) * tr * tr;
+}
+
+cudaError_t launch_harris_dhat(const HarrisCall& c, float* out, cudaStream_t s) {
+  HarrisParams p = make_params(c);
+  dim3 blk(32, 8), grd((c.src.W + 31) / 32, (c.dst.H + 7) / 8, c.batch);
+  harris_dhat<<<grd, blk, 0, s>>>(p, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_harris_stream(const HarrisCall& c, int nt, int vec, int S, cudaStream_t s) {
   HarrisParams p = make_params(c);
   if (vec == 4) {

@@ -1,0 +1,350 @@
+// harris_slide.cuh -- Harris variant family "slide<B,NW>": the fused streaming
+// Harris kernel (§6; Tables 4-5 "Loop 1/2") with the
+// B x B window sum done SEPARABLY ON THE PRODUCTS: per input row the three
+// products (dx^2, dy^2, dx*dy) of the lane's own 4 columns enter B-1 running
+// vertical chains; when a chain completes, the column sums V of the lane and
+// of its two neighbour columns each side (warp shuffles) are summed
+// horizontally with a sliding window.  Versus the shfl<> family (horizontal
+// product sums per input row over 8 dx/dy columns, then vertical chains of
+// those) this is ~25 instead of ~45 lane-instructions per pixel: the
+// horizontal sums run once per OUTPUT row on 3 values per column instead of
+// once per input row on 5 products per output.  SURVEY.md §8(c) reading 16
+// lets Harris variants re-associate the window sums; the order here is fixed
+// per output (vertical chain oldest row first, then the sliding horizontal
+// sum whose form depends only on x mod 4), so every CTA, every row band and
+// every batch split gives the same bits, and the result differs from the
+// naive order only by rounding (compared against the oracle by tolerance).
+//
+// Per-stage boundary (R9): dx/dy outside the image are dx(clamp(q))
+// (clamp) or 0 (constant).  Rows: the Sobel centre row of an outside product
+// row is clamp(yy) (constant: the product row is 0).  Columns: a column sum V
+// of an outside column is V of column 0 / W-1 (clamp; the row clamping is
+// already inside it) or 0 (constant), selected from the owning lane.
+#pragma once
+#include "harris_stream.cuh"
+
+namespace icl {
+
+template <int B, int NW, bool GEN, bool EDGE, int UNR>
+__device__ __forceinline__ void harris_slide_body(const HarrisParams& p, int S, float* smem) {
+  constexpr int A = B / 2;
+  constexpr int BB = B - 1 - A;
+  static_assert(A <= 2 && BB <= 2, "the 2-column shuffle halo covers windows up to 5x5");
+  constexpr int NT = 32 * NW;
+  constexpr int HP = 8;
+  constexpr int TW = 120 * NW;
+  constexpr int ROWLEN = TW + 2 * HP;
+  constexpr int NSLOT = ROWLEN / 4;
+  constexpr int RB = HarFastGeom<B>::RB, NBLKS = HarFastGeom<B>::NBLKS, NSR = HarFastGeom<B>::NSR;
+  static_assert(RB >= 4, "row offsets of a step stay within two load blocks");
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * TW;
+  const int ly0 = blockIdx.y * S;
+  const int ly1 = min(ly0 + S, p.dst.H);
+  const int g0 = p.dst.y0 + ly0;
+  const int NY = (ly1 - ly0) + B - 1;  // product rows
+  const int NL = NY + 2;               // input rows (load index kl <-> global row g0 - A - 1 + kl)
+  const int NBI = (NY + RB - 1) / RB;
+  const int NBL = (NL + RB - 1) / RB;
+  const int W = p.src.W;
+  const int Hg = p.src.Hg;
+  const bool clampb = p.src.border == kBorderClamp;
+  const int64_t spitch = p.src.pitch >> 2;
+  const float* rowb = src_row(p.src, b, g0 - A - 1);  // load index 0 (may lie outside the image: GEN)
+
+  // ---- loader: cp.async ring of NSR rows (+2 mirror rows when !GEN), RB rows per block
+  auto load_block = [&](int m) {
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      const int kl = m * RB + u;
+      if (kl < NL) {
+        const int rr = kl % NSR;
+        float* st = smem + rr * ROWLEN;
+        int gi = g0 - A - 1 + kl;
+        if (GEN && (gi < 0 || gi >= Hg)) {  // input row outside the image: input boundary
+          if (!clampb) {
+            for (int c = tid; c < ROWLEN; c += NT) st[c] = p.src.cval;
+            continue;
+          }
+          gi = clampi(gi, 0, Hg - 1);
+        }
+        const float* row = rowb + (int64_t)(gi - (g0 - A - 1)) * spitch;
+        for (int s = tid; s < NSLOT; s += NT) {
+          const int xs = x0 - HP + 4 * s;
+          const int nb = !EDGE ? 16 : (xs < 0 ? 0 : min(max(W - xs, 0), 4) * 4);
+          const void* g = nb ? (const void*)(row + xs) : (const void*)row;
+          cp_async16(st + 4 * s, g, nb);
+          if (!GEN && rr < 2) cp_async16(smem + (NSR + rr) * ROWLEN + 4 * s, g, nb);  // mirror
+        }
+      }
+    }
+  };
+  auto fix_block = [&](int m) {  // EDGE: input boundary of the halo columns outside [0, W)
+    for (int u = 0; u < RB; ++u) {
+      const int kl = m * RB + u;
+      if (kl >= NL) break;
+      const int rr = kl % NSR;
+      for (int mirror = 0; mirror < ((!GEN && rr < 2) ? 2 : 1); ++mirror) {
+        float* st = smem + (mirror ? NSR + rr : rr) * ROWLEN;
+        const int il = HP - x0, ir = (W - 1) - x0 + HP;
+        const float vl = (il >= 0 && il < ROWLEN) ? st[il] : 0.0f;
+        const float vr = (ir >= 0 && ir < ROWLEN) ? st[ir] : 0.0f;
+        for (int c = tid; c < ROWLEN; c += NT) {
+          const int xe = x0 - HP + c;
+          if (xe < 0) st[c] = clampb ? vl : p.src.cval;
+          else if (xe >= W) st[c] = clampb ? vr : p.src.cval;
+        }
+      }
+    }
+  };
+  for (int m = 0; m < NBLKS - 1; ++m) {
+    if (m < NBL) load_block(m);
+    cp_async_commit();
+  }
+
+  // own columns xl .. xl+3 (lanes 0 / 31 only feed their neighbours: 120 output columns per warp)
+  const int xl = x0 + 120 * warp + 4 * (lane - 1);
+  const float* stb = smem + (xl - (x0 - HP));
+  const bool emit = lane >= 1 && lane <= 30 && (!EDGE || xl < W);
+  const bool warp_live = !EDGE || x0 + 120 * warp - 4 < W;
+  // lanes owning image columns 0 and W-1 (per-stage column boundary of the column sums)
+  const int xw = x0 + 120 * warp - 4;
+  const int ll = (0 - xw) >> 2, el = (0 - xw) & 3;
+  const int lr = (W - 1 - xw) >> 2, er = (W - 1 - xw) & 3;
+
+  // vertical chains of the products, oldest row first: c2 = (dx^2, dy^2) per column,
+  // cxy = dx*dy of columns (0, 1) and (2, 3) in float2 lanes
+  constexpr int NC = B > 1 ? B - 1 : 1;
+  float2 c2[NC][4];
+  float2 cxy[NC][2];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c2[k][q] = make_float2(0.0f, 0.0f);
+    cxy[k][0] = cxy[k][1] = make_float2(0.0f, 0.0f);
+  }
+  float* drow = dst_row(p.dst, b, ly0) + xl;
+  const int64_t dpitch = p.dst.pitch >> 2;
+  const bool has_mask = p.mask != nullptr;
+  char* mrow = has_mask ? p.mask + (int64_t)b * p.mbstride + (int64_t)ly0 * p.mpitch + xl : nullptr;
+
+#pragma unroll 1
+  for (int i = 0; i < NBI; ++i) {
+    cp_async_wait<NBLKS - 3>();
+    __syncthreads();
+    if (EDGE) {
+      if (i == 0) fix_block(0);
+      if (i + 1 < NBL) fix_block(i + 1);
+      __syncthreads();
+    }
+    if (i + NBLKS - 1 < NBL) load_block(i + NBLKS - 1);
+    cp_async_commit();
+    if (!warp_live) continue;
+    const int base = (i % NBLKS) * RB;
+#pragma unroll UNR
+    for (int u = 0; u < RB; ++u) {
+      const int step = i * RB + u;
+      if (step >= NY) break;
+      // ---- Sobel at the centre row of product row yy (clamped for GEN), differences first (R19)
+      int dz = 0;
+      bool zero_row = false;
+      if (GEN) {
+        const int yy = g0 - A + step;
+        dz = yy < 0 ? -yy : (yy >= Hg ? (Hg - 1) - yy : 0);
+        zero_row = dz != 0 && !clampb;
+      }
+      float4 w[3];
+      float il[3], ir[3];
+#pragma unroll
+      for (int rr = 0; rr < 3; ++rr) {
+        int sr = base + u + rr + dz;
+        if (GEN) {
+          if (sr >= NSR) sr -= NSR;
+          if (sr < 0) sr += NSR;
+        }
+        w[rr] = *reinterpret_cast<const float4*>(stb + sr * ROWLEN);
+        il[rr] = __shfl_up_sync(0xffffffffu, w[rr].w, 1);    // column xl-1
+        ir[rr] = __shfl_down_sync(0xffffffffu, w[rr].x, 1);  // column xl+4
+      }
+      float hd[3][4];
+#pragma unroll
+      for (int rr = 0; rr < 3; ++rr) {
+        const float2 m = __fadd2_rn(make_float2(w[rr].z, w[rr].w), make_float2(-w[rr].x, -w[rr].y));
+        hd[rr][0] = __fsub_rn(w[rr].y, il[rr]);
+        hd[rr][1] = m.x;
+        hd[rr][2] = m.y;
+        hd[rr][3] = __fsub_rn(ir[rr], w[rr].z);
+      }
+      float vd[6];
+      {
+        const float2 v12 = __fadd2_rn(make_float2(w[2].x, w[2].y), make_float2(-w[0].x, -w[0].y));
+        const float2 v34 = __fadd2_rn(make_float2(w[2].z, w[2].w), make_float2(-w[0].z, -w[0].w));
+        vd[0] = __fsub_rn(il[2], il[0]);
+        vd[1] = v12.x; vd[2] = v12.y; vd[3] = v34.x; vd[4] = v34.y;
+        vd[5] = __fsub_rn(ir[2], ir[0]);
+      }
+      float2 g[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        g[c].x = __fmaf_rn(2.0f, hd[1][c], __fadd_rn(hd[0][c], hd[2][c]));
+        g[c].y = __fmaf_rn(2.0f, vd[c + 1], __fadd_rn(vd[c], vd[c + 2]));
+      }
+      // ---- products, then the vertical chains
+      float2 pp[4], px[2];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) pp[q] = __fmul2_rn(g[q], g[q]);
+      px[0] = __fmul2_rn(make_float2(g[0].x, g[1].x), make_float2(g[0].y, g[1].y));
+      px[1] = __fmul2_rn(make_float2(g[2].x, g[3].x), make_float2(g[2].y, g[3].y));
+      if (GEN && zero_row) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pp[q] = make_float2(0.0f, 0.0f);
+        px[0] = px[1] = make_float2(0.0f, 0.0f);
+      }
+      float2 v2[4], vx[2];
+      if (B > 1) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          v2[q] = __fadd2_rn(c2[0][q], pp[q]);
+#pragma unroll
+          for (int k = 0; k + 1 < NC; ++k) c2[k][q] = __fadd2_rn(c2[k + 1][q], pp[q]);
+          c2[NC - 1][q] = pp[q];
+        }
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          vx[m] = __fadd2_rn(cxy[0][m], px[m]);
+#pragma unroll
+          for (int k = 0; k + 1 < NC; ++k) cxy[k][m] = __fadd2_rn(cxy[k + 1][m], px[m]);
+          cxy[NC - 1][m] = px[m];
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v2[q] = pp[q];
+        vx[0] = px[0];
+        vx[1] = px[1];
+      }
+      if (step < B - 1) continue;
+      // ---- column sums of columns xl-2 .. xl+5: own 2..5, neighbours' 0,1 and 6,7
+      float2 V2[8];
+      float Vx[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) V2[2 + q] = v2[q];
+      Vx[2] = vx[0].x; Vx[3] = vx[0].y; Vx[4] = vx[1].x; Vx[5] = vx[1].y;
+      V2[0].x = __shfl_up_sync(0xffffffffu, v2[2].x, 1);
+      V2[0].y = __shfl_up_sync(0xffffffffu, v2[2].y, 1);
+      V2[1].x = __shfl_up_sync(0xffffffffu, v2[3].x, 1);
+      V2[1].y = __shfl_up_sync(0xffffffffu, v2[3].y, 1);
+      Vx[0] = __shfl_up_sync(0xffffffffu, vx[1].x, 1);
+      Vx[1] = __shfl_up_sync(0xffffffffu, vx[1].y, 1);
+      V2[6].x = __shfl_down_sync(0xffffffffu, v2[0].x, 1);
+      V2[6].y = __shfl_down_sync(0xffffffffu, v2[0].y, 1);
+      V2[7].x = __shfl_down_sync(0xffffffffu, v2[1].x, 1);
+      V2[7].y = __shfl_down_sync(0xffffffffu, v2[1].y, 1);
+      Vx[6] = __shfl_down_sync(0xffffffffu, vx[0].x, 1);
+      Vx[7] = __shfl_down_sync(0xffffffffu, vx[0].y, 1);
+      if (EDGE) {  // per-stage column boundary: V(x) = V(clamp(x)) or 0
+        const float2 e0 = el == 0 ? v2[0] : el == 1 ? v2[1] : el == 2 ? v2[2] : v2[3];
+        const float2 e1 = er == 0 ? v2[0] : er == 1 ? v2[1] : er == 2 ? v2[2] : v2[3];
+        const float f0 = el == 0 ? vx[0].x : el == 1 ? vx[0].y : el == 2 ? vx[1].x : vx[1].y;
+        const float f1 = er == 0 ? vx[0].x : er == 1 ? vx[0].y : er == 2 ? vx[1].x : vx[1].y;
+        float2 gl, gr;
+        gl.x = __shfl_sync(0xffffffffu, e0.x, ll & 31);
+        gl.y = __shfl_sync(0xffffffffu, e0.y, ll & 31);
+        gr.x = __shfl_sync(0xffffffffu, e1.x, lr & 31);
+        gr.y = __shfl_sync(0xffffffffu, e1.y, lr & 31);
+        float hl = __shfl_sync(0xffffffffu, f0, ll & 31);
+        float hr = __shfl_sync(0xffffffffu, f1, lr & 31);
+        if (!clampb) {
+          gl = gr = make_float2(0.0f, 0.0f);
+          hl = hr = 0.0f;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int xe = xl - 2 + j;
+          if (xe < 0) { V2[j] = gl; Vx[j] = hl; }
+          else if (xe >= W) { V2[j] = gr; Vx[j] = hr; }
+        }
+      }
+      // ---- horizontal window sums (sliding; the form depends only on the column mod 4)
+      // direct horizontal sums, left to right (a sliding sum would cancel across step edges:
+      // measured 1e-3 x D on the rectangles scene, beyond the 1e-4 tolerance)
+      float2 s2[4];
+      float sx[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        s2[q] = V2[2 + q - A];
+        sx[q] = Vx[2 + q - A];
+#pragma unroll
+        for (int t = 1 - A; t <= BB; ++t) {
+          s2[q] = __fadd2_rn(s2[q], V2[2 + q + t]);
+          sx[q] = __fadd_rn(sx[q], Vx[2 + q + t]);
+        }
+      }
+      float R[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) R[q] = harris_R(s2[q].x, sx[q], s2[q].y, p.k);
+      if (emit) {
+        if (!EDGE || xl + 3 < W) {
+          st_cs4(drow, make_float4(R[0], R[1], R[2], R[3]));
+          if (has_mask)
+            *reinterpret_cast<uchar4*>(mrow) =
+                make_uchar4(R[0] > p.threshold, R[1] > p.threshold, R[2] > p.threshold, R[3] > p.threshold);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (xl + q < W) {
+              drow[q] = R[q];
+              if (has_mask) mrow[q] = R[q] > p.threshold ? 1 : 0;
+            }
+        }
+      }
+      drow += dpitch;
+      mrow += has_mask ? p.mpitch : 0;
+    }
+  }
+  cp_async_wait<0>();
+}
+
+template <int B, int NW, int UNR>
+__global__ void __launch_bounds__(32 * NW, 16 / NW) harris_slide(HarrisParams p, int S) {
+  extern __shared__ __align__(16) float smem[];
+  constexpr int TW = 120 * NW, HP = 8, A = B / 2, BB = B - 1 - A;
+  const int x0 = blockIdx.x * TW, ly0 = blockIdx.y * S;
+  const int ly1 = min(ly0 + S, p.dst.H);
+  const int g0 = p.dst.y0 + ly0;
+  const bool rows_in = g0 - A - 1 >= 0 && p.dst.y0 + ly1 + BB + 1 <= p.src.Hg;
+  const bool cols_in = x0 - HP >= 0 && x0 + TW + HP <= p.src.W;
+  if (rows_in && cols_in) harris_slide_body<B, NW, false, false, UNR>(p, S, smem);
+  else if (rows_in) harris_slide_body<B, NW, false, true, 1>(p, S, smem);
+  else harris_slide_body<B, NW, true, true, 1>(p, S, smem);
+}
+
+template <int B, int NW, int UNR>
+static inline cudaError_t launch_hslide(const HarrisParams& p, int batch, int S, cudaStream_t s) {
+  constexpr int TW = 120 * NW;
+  constexpr int ROWLEN = TW + 16;
+  const size_t smem = (size_t)(HarFastGeom<B>::NSR + 2) * ROWLEN * sizeof(float);  // + 2 mirror rows
+  auto kern = harris_slide<B, NW, UNR>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grd((p.src.W + TW - 1) / TW, (p.dst.H + S - 1) / S, batch);
+  kern<<<grd, 32 * NW, smem, s>>>(p, S);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int NW, int UNR>
+cudaError_t dispatch_hslide(const HarrisParams& p, int batch, int S, cudaStream_t s) {
+  switch (p.block) {
+    case 1: return launch_hslide<1, NW, UNR>(p, batch, S, s);
+    case 2: return launch_hslide<2, NW, UNR>(p, batch, S, s);
+    case 3: return launch_hslide<3, NW, UNR>(p, batch, S, s);
+    case 4: return launch_hslide<4, NW, UNR>(p, batch, S, s);
+    case 5: return launch_hslide<5, NW, UNR>(p, batch, S, s);
+    default: return cudaErrorInvalidValue;  // B = 6, 7 need a wider shuffle halo
+  }
+}
+
+}  // namespace icl

@@ -38,6 +38,9 @@ struct HarrisCall {
   int block;
   float k;
   float threshold;
+  // restrict dispatch to the variants sharing the naive per-output fp32 order (the fused chain's
+  // two-pass schedule and the peer bands, whose edge kernels use that order): bit-identical
+  bool naive_order;
 };
 
 struct NlmCall {
@@ -80,6 +83,8 @@ cudaError_t launch_sep_tile(const SepCall& c, bool persistent, cudaStream_t s);
 cudaError_t launch_harris_naive(const HarrisCall& c, cudaStream_t s);
 cudaError_t launch_harris_stream(const HarrisCall& c, int nt, int vec, int S, cudaStream_t s);
 cudaError_t launch_harris_shfl(const HarrisCall& c, int nw, int S, cudaStream_t s);
+cudaError_t launch_harris_slide(const HarrisCall& c, int nw, int unr, int S, cudaStream_t s);
+cudaError_t launch_harris_dhat(const HarrisCall& c, float* out, cudaStream_t s);
 // two-filter chain (blur_harris.cu): separable blur (radius <= 3) then Harris (block <= 5) in one pass
 cudaError_t launch_blur_harris(const HarrisCall& h, const SrcView& raw, const float* fx, int rx, const float* gy,
                                int ry, int S, cudaStream_t s);
@@ -91,6 +96,7 @@ cudaError_t launch_nlm_boxsum(const NlmCall& c, int variant, cudaStream_t s);
 cudaError_t launch_nlm_r8(const NlmCall& c, cudaStream_t s);
 cudaError_t launch_nlm_r16(const NlmCall& c, cudaStream_t s);
 cudaError_t launch_nlm_x2(const NlmCall& c, cudaStream_t s);
+cudaError_t launch_nlm_w(const NlmCall& c, cudaStream_t s);
 // conv2d (u8)
 cudaError_t launch_conv2d_naive(const Conv2dCall& c, cudaStream_t s);
 cudaError_t launch_conv2d_tile(const Conv2dCall& c, int rows_per_thread, bool persistent, cudaStream_t s);
@@ -121,5 +127,10 @@ cudaError_t launch_sep3d(const Sep3Params& p, int variant, cudaStream_t s);
 // synthetic inputs
 cudaError_t launch_fill_uniform(float* base, int64_t W, int64_t H, int64_t pitch, int64_t batch,
                                 int64_t bstride, uint64_t seed, int64_t row0, cudaStream_t s);
+
+// icl_harris restricted to the naive-order variants (HarrisCall::naive_order)
+icl_status harris_naive_order(const icl_image* src, const icl_image* response, int block, float k, icl_border border,
+                              float border_value, const icl_image* mask, float threshold, const icl_band* band,
+                              void* stream);
 
 }  // namespace icl

@@ -401,7 +401,7 @@ icl_status icl_harris_peer(const icl_image* own, const icl_image* response, int6
       mv.height = i1 - i0;
     }
     const icl_band bi{H, y0, i0};
-    if ((st = icl_harris(own, &dv, block, k, border, border_value, mask && mask->data ? &mv : nullptr, threshold, &bi,
+    if ((st = harris_naive_order(own, &dv, block, k, border, border_value, mask && mask->data ? &mv : nullptr, threshold, &bi,
                          s)))
       return st;
   }

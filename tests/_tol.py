@@ -59,3 +59,22 @@ def check_conv2d(got, img, filt, border, c, points=None, tol=SEP_TOL):
     bad = np.where(scale > 0, err > tol * scale, err != 0)
     assert not bad.any(), f"conv2d: {bad.sum()} pixels out of tolerance; max rel {np.max(err / np.maximum(scale, 1e-300))}"
     return float(np.max(err / np.maximum(scale, 1e-300))) if err.size else 0.0
+
+
+def check_harris_families(outs, img, block, k, border, c, thr, points=None):
+    """The naive-order variants are bit-identical to naive_direct; the slide<> family (separable
+    window sums on the products, re-associated -- SURVEY.md §8(c) R16) is bit-identical within
+    itself and matches the oracle within the Harris tolerance."""
+    R0, M0 = outs["naive_direct"]
+    slide = {n: v for n, v in outs.items() if n.startswith("slide")}
+    for name, (R, M) in outs.items():
+        if name in slide:
+            continue
+        np.testing.assert_array_equal(R, R0, err_msg=name)
+        np.testing.assert_array_equal(M, M0, err_msg=name)
+    if slide:
+        Rs, Ms = next(iter(slide.values()))
+        check_harris(Rs, Ms, img, block, k, border, c, thr, points=points)
+        for name, (R, M) in slide.items():
+            np.testing.assert_array_equal(R, Rs, err_msg=name)
+            np.testing.assert_array_equal(M, Ms, err_msg=name)

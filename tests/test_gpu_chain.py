@@ -62,7 +62,12 @@ def two_calls(src, fx, gy, bb, bc, block, k, border, c, thr, with_mask=True):
     icl.sepconv(src, blurred, fx, gy, bb, bc)
     R = out_like(src)
     m = out_like(src, torch.uint8) if with_mask else None
-    icl.harris(blurred, R, block, k, border, c, mask=m, threshold=thr)
+    # the chain keeps the naive per-output Harris order (R24): compare with that variant
+    icl.force_variant("harris", "naive_direct")
+    try:
+        icl.harris(blurred, R, block, k, border, c, mask=m, threshold=thr)
+    finally:
+        icl.force_variant("harris", None)
     return R, m
 
 

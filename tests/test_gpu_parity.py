@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 import synth
-from tests._tol import check_harris, check_nlm, check_sepconv
+from tests._tol import check_harris, check_harris_families, check_nlm, check_sepconv
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -290,9 +290,7 @@ def test_harris_all_variants_vs_oracle(shape, block, border, c):
     assert len(outs) >= 2
     R0, M0 = outs["naive_direct"]
     check_harris(R0, M0, img, block, 0.04, border, c, thr)
-    for name, (R, M) in outs.items():
-        np.testing.assert_array_equal(R, R0, err_msg=name)
-        np.testing.assert_array_equal(M, M0, err_msg=name)
+    check_harris_families(outs, img, block, 0.04, border, c, thr)
 
 
 def test_harris_config_2048_sampled():
@@ -320,13 +318,17 @@ def test_harris_config_2048_sampled():
 
 def test_harris_flat_and_scaling_exact():
     img = synth.rect_scene(9, 120, 90, n_rect=10, noise=0.01)
-    r1, r2 = empty_like_dev(120, 90), empty_like_dev(120, 90)
-    icl.harris(to_dev(img), r1, 5, 0.04, "clamp")
-    icl.harris(to_dev(img * np.float32(2)), r2, 5, 0.04, "clamp")
-    np.testing.assert_array_equal(host(r2), 16 * host(r1))
-    flat = np.full((40, 50), 0.37, np.float32)
-    icl.harris(to_dev(flat), r1[:40, :50], 5, 0.04, "clamp")
-    assert not host(r1[:40, :50]).any()
+    for vid, name in [(None, "default")] + list(variants("harris")):
+        icl.force_variant("harris", vid)
+        r1, r2 = empty_like_dev(120, 90, pitch=92), empty_like_dev(120, 90, pitch=92)
+        icl.harris(to_dev(img, pitch=92), r1, 5, 0.04, "clamp")
+        icl.harris(to_dev(img * np.float32(2), pitch=92), r2, 5, 0.04, "clamp")
+        np.testing.assert_array_equal(host(r2), 16 * host(r1), err_msg=name)
+        flat = np.full((40, 120), 0.37, np.float32)
+        f1 = empty_like_dev(40, 120)
+        icl.harris(to_dev(flat), f1, 5, 0.04, "clamp")
+        assert not host(f1).any(), name
+    icl.force_variant("harris", None)
 
 
 @pytest.mark.parametrize("border", ["constant", "clamp"])
@@ -343,6 +345,19 @@ def test_harris_bands_bit_exact(border):
         dst = empty_like_dev(b - a, W)
         icl.harris(to_dev(img[s0:s1]), dst, B, 0.04, border, 0.2, band=(H, s0, a))
         np.testing.assert_array_equal(host(dst), ref[a:b])
+    # every variant family on its own: stitched bands == its unsharded call, bit for bit
+    P = 152  # 16-byte pitch: the float4 variants are eligible
+    for vid, name in variants("harris"):
+        icl.force_variant("harris", vid)
+        full = empty_like_dev(H, W, pitch=P)
+        icl.harris(to_dev(img, pitch=P), full, B, 0.04, border, 0.2)
+        ref = host(full)
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            s0, s1 = max(0, a - up), min(H, b + down)
+            dst = empty_like_dev(b - a, W, pitch=P)
+            icl.harris(to_dev(img[s0:s1], pitch=P), dst, B, 0.04, border, 0.2, band=(H, s0, a))
+            np.testing.assert_array_equal(host(dst), ref[a:b], err_msg=f"{name} band {a}:{b}")
+    icl.force_variant("harris", None)
 
 
 # ============================================================================ nlm

@@ -121,7 +121,9 @@ def _harris_worker(rank, n, port, H, W, block, border, cval):
         src = torch.from_numpy(full).to(dev)
         ref = torch.empty_like(src)
         mref = torch.empty(H, W, dtype=torch.uint8, device=dev)
+        icl.force_variant("harris", "naive_direct")  # the peer edge kernels keep the naive order
         icl.harris(src, ref, block, 0.04, border, cval, mask=mref, threshold=0.01)
+        icl.force_variant("harris", None)
         np.testing.assert_array_equal(np.concatenate([p[0] for p in parts]), ref.cpu().numpy())
         np.testing.assert_array_equal(np.concatenate([p[1] for p in parts]), mref.cpu().numpy())
     for p in nb.values():
@@ -204,7 +206,9 @@ def test_peer_paths_in_one_process(nb):
     ref_s, ref_h = torch.empty_like(src), torch.empty_like(src)
     ref_m = torch.empty(H, W, dtype=torch.uint8, device=DEV)
     icl.sepconv(src, ref_s, f, f, "clamp")
+    icl.force_variant("harris", "naive_direct")  # the peer edge kernels keep the naive order
     icl.harris(src, ref_h, 5, 0.04, "constant", 0.2, mask=ref_m, threshold=0.01)
+    icl.force_variant("harris", None)
     out_s, out_h, out_m = [], [], []
     for k, (a, b) in enumerate(cuts):
         up = icl.LocalBand(bands[k - 1]) if k > 0 else None
