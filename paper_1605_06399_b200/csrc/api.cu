@@ -191,7 +191,9 @@ static const Variant kNlmVariants[] = {
     {"boxsum_r8", K_BOXR8, 0, 0, 0},
     {"boxsum_r16", K_BOXR16, 0, 0, 0},
     {"boxsum_x2", K_BOXX2, 0, 0, 0},
-    {"boxsum_w", K_BOXW, 0, 0, 0},
+    {"boxsum_w", K_BOXW, 0, 0, 1},
+    {"boxsum_w_u2", K_BOXW, 0, 0, 2},
+    {"boxsum_w_uf", K_BOXW, 0, 0, 11},
 };
 
 static const Variant kConvVariants[] = {
@@ -271,7 +273,9 @@ static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXR8 && !nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXR16 && !nlm_r16_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXX2 && !nlm_x2_supported(pc.nlm.P, pc.nlm.S)) return false;
-  if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXW && !nlm_w_supported(pc.nlm.P, pc.nlm.S)) return false;
+  if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXW &&
+      (!nlm_w_supported(pc.nlm.P, pc.nlm.S) || (v.S != 1 && !(pc.nlm.P == 2 && pc.nlm.S == 5))))
+    return false;
   return true;
 }
 
@@ -358,7 +362,7 @@ static cudaError_t run_variant_1(const Prepared& pc, const Variant& v, cudaStrea
       if (v.kind == K_BOXR8) return launch_nlm_r8(pc.nlm, s);
       if (v.kind == K_BOXR16) return launch_nlm_r16(pc.nlm, s);
       if (v.kind == K_BOXX2) return launch_nlm_x2(pc.nlm, s);
-      if (v.kind == K_BOXW) return launch_nlm_w(pc.nlm, s);
+      if (v.kind == K_BOXW) return launch_nlm_w(pc.nlm, v.S, s);
       return launch_nlm_boxsum(pc.nlm, 0, s);
     case ICL_FILTER_CONV2D:
       if (v.kind == K_NAIVE) return launch_conv2d_naive(pc.c2d, s);

@@ -45,7 +45,7 @@ struct WGeom {
   static_assert(UW % 4 == 2 && HS % 4 == 2, "conflict-free strides");
 };
 
-template <int P, int S>
+template <int P, int S, int UOY>
 __global__ void __launch_bounds__(128, 2) nlm_box_w(NlmParams p, int ntx, int nty, int ntiles, int nhalf) {
   using G_ = WGeom<P, S>;
   constexpr int TW = G_::TW, TH = G_::TH, HR = G_::HR, UW = G_::UW, UW0 = G_::UW0, UH = G_::UH, HS = G_::HS;
@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(128, 2) nlm_box_w(NlmParams p, int ntx, int nt
     for (int c = 0; c < 4 + 2 * P; ++c) up1[c] = urow[c];
   }
 
-#pragma unroll 1
+  // UOY: the search-row loop unrolled (2, or 2S+1 = fully: the window shifts become renames)
+#pragma unroll UOY
   for (int oy = -S; oy <= S; ++oy) {
     // ---------------- phase A: H rows hr, 4-column segments
     for (int item = tid; item < HROWS * (TW / 4); item += NT) {
@@ -206,11 +207,11 @@ __global__ void __launch_bounds__(128, 2) nlm_box_w(NlmParams p, int ntx, int nt
   }
 }
 
-template <int P, int S>
+template <int P, int S, int UOY = 1>
 inline cudaError_t launch_w(const NlmParams& p, int batch, cudaStream_t s) {
   using G = WGeom<P, S>;
   static_assert(G::smem_bytes <= 113 * 1024, "two CTAs per SM");
-  auto kern = nlm_box_w<P, S>;
+  auto kern = nlm_box_w<P, S, UOY>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::smem_bytes);
   if (e != cudaSuccess) return e;
   const int ntx = (p.src.W + G::TW - 1) / G::TW, nty = (p.dst.H + G::TH - 1) / G::TH;

@@ -7,7 +7,8 @@ set -u
 TAG=${1:-r01}; shift || true
 OUT=gpurun_out/ncu_$TAG
 mkdir -p $OUT
-BENCH="python bench.py --steps 2 --warmup 3 --batch 2 --no-e2e --no-cpu-baseline --no-tune --no-small"
+BATCH=${ICL_NCU_BATCH:-8}  # the bench default launch (8 x 4096^2 per filter): traffic is read from THE timed launch shape
+BENCH="python bench.py --steps 2 --warmup 3 --batch $BATCH --no-e2e --no-cpu-baseline --no-tune --no-small --no-16k"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $BENCH > $OUT/launches_bench.log 2>&1
 echo "launch list rc=$?"
 REGEXES=("$@")

@@ -18,8 +18,10 @@ ap.add_argument("--tag", default="")
 ap.add_argument("reports", nargs="+", help="filter=path.ncu-rep")
 a = ap.parse_args()
 out = {"_note": ("dram__bytes_read.sum + dram__bytes_write.sum per pixel from one ncu --set full capture per "
-                 f"kernel ({a.tag}); bench.py scales by the pixels of its launch. Writes still dirty in L2 at "
-                 "kernel end are not counted, so traffic can read slightly below the algorithmic 8 / 9 B/px.")}
+                 f"kernel ({a.tag}) of the SAME launch bench.py times (8 x 4096^2 per filter), so "
+                 "bytes_per_px x pixels is that launch's DRAM traffic. Reads are the algorithmic 4 B/px (no "
+                 "re-reads); writes read up to ~60 MB short because output lines still dirty in the 126 MB L2 "
+                 "at kernel end are written back after it (outside the kernel's counters).")}
 for spec in a.reports:
     f, path = spec.split("=", 1)
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -35,7 +37,8 @@ for spec in a.reports:
 
     def pct(key):
         return round(float(d[key][0]), 1) if key in d else None
-    out[f] = {"bytes_per_px": round((rd + wr) / a.px, 3), "kernel": d["Kernel Name"][0], "report": os.path.basename(path),
+    out[f] = {"bytes_per_px": round((rd + wr) / a.px, 3), "read_bytes_per_px": round(rd / a.px, 3),
+              "write_bytes_per_px": round(wr / a.px, 3), "captured_px": a.px, "kernel": d["Kernel Name"][0], "report": os.path.basename(path),
               "fma_pipe_cycles_pct": pct("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
               "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
               "smem_wavefronts_pct": pct("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),

@@ -17,7 +17,7 @@ ap.add_argument('--batch', type=int, default=8)
 ap.add_argument('--param', type=int, default=None, help="harris block / sepconv radius / nlm search radius")
 ap.add_argument('--reps', type=int, default=20)
 ap.add_argument('variants', nargs='*')
-a = ap.parse_args()
+a = ap.parse_intermixed_args()
 dev = torch.device('cuda:0')
 srcs = [torch.empty(a.batch, a.size, a.size, device=dev) for _ in range(2)]
 for i, s in enumerate(srcs):
