@@ -192,8 +192,6 @@ static const Variant kNlmVariants[] = {
     {"boxsum_r16", K_BOXR16, 0, 0, 0},
     {"boxsum_x2", K_BOXX2, 0, 0, 0},
     {"boxsum_w", K_BOXW, 0, 0, 1},
-    {"boxsum_w_u2", K_BOXW, 0, 0, 2},
-    {"boxsum_w_uf", K_BOXW, 0, 0, 11},
 };
 
 static const Variant kConvVariants[] = {
@@ -273,9 +271,7 @@ static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXR8 && !nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXR16 && !nlm_r16_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXX2 && !nlm_x2_supported(pc.nlm.P, pc.nlm.S)) return false;
-  if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXW &&
-      (!nlm_w_supported(pc.nlm.P, pc.nlm.S) || (v.S != 1 && !(pc.nlm.P == 2 && pc.nlm.S == 5))))
-    return false;
+  if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXW && !nlm_w_supported(pc.nlm.P, pc.nlm.S)) return false;
   return true;
 }
 
@@ -392,10 +388,14 @@ static int default_variant(const Prepared& pc) {
         // the vertical halo 2R is re-read per S output rows: S grows with R;
         // from R = 7 the register ring of stream<R> limits occupancy and the
         // shared-memory tile kernel wins (16384^2 sweep)
+        // (round 2: FFMA2 in both passes of stream<> moved its crossover with tile64p to R = 9;
+        // 16384^2: R = 5 / 6 / 7 / 8 in 0.426 / 0.468 / 0.579 / 0.673 ms)
         const int R = pc.sep.rx > pc.sep.ry ? pc.sep.rx : pc.sep.ry;
         if (R <= 2) return variant_id(pc.f, "stream_nt64_s16_v4");
         if (R <= 4) return variant_id(pc.f, "stream_nt64_s32_v4");
-        if (R <= 6) return variant_id(pc.f, "stream_nt64_s64_v4");
+        if (R <= 5) return variant_id(pc.f, "stream_nt64_s64_v4");
+        if (R <= 6) return variant_id(pc.f, "stream_nt128_s64_v4");
+        if (R <= 8) return variant_id(pc.f, "stream_nt64_s128_v4");
         return variant_id(pc.f, "tile64p_v4");
       }
     case ICL_FILTER_HARRIS:

@@ -172,25 +172,43 @@ __global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
           const float4 w = reinterpret_cast<const float4*>(st + 4 * tid)[q];
           v[4 * q] = w.x; v[4 * q + 1] = w.y; v[4 * q + 2] = w.z; v[4 * q + 3] = w.w;
         }
-        float t[4];
+        // row pass, two outputs per FFMA2: input v[k] feeds output c with tap k-c and output c+1
+        // with tap k-c-1 -- the tap pair (fx[i], fx[i-1]) from the parameter bank, the input
+        // broadcast.  Each lane runs exactly its output's FMA chain over i = 0..2R (from 0.0f), so
+        // the result is the scalar chain's, bit for bit; the chain ends run as scalar FFMAs.
+        float2 t01, t23;
+        {
+          constexpr int B0 = HP - R;
+          t01.x = __fmaf_rn(p.fx[0], v[B0], 0.0f);
+          t23.x = __fmaf_rn(p.fx[0], v[B0 + 2], 0.0f);
+          t01.y = 0.0f;
+          t23.y = 0.0f;
+          if (R == 0) {
+            t01.y = __fmaf_rn(p.fx[0], v[B0 + 1], 0.0f);
+            t23.y = __fmaf_rn(p.fx[0], v[B0 + 3], 0.0f);
+          } else {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          float a = 0.0f;
-#pragma unroll
-          for (int ii = 0; ii < P; ++ii) a = __fmaf_rn(p.fx[ii], v[HP - R + c + ii], a);
-          t[c] = a;
+            for (int i = 1; i <= 2 * R; ++i) {
+              const float va = v[B0 + i], vb = v[B0 + 2 + i];
+              t01 = __ffma2_rn(make_float2(va, va), p.fxp[i], t01);
+              t23 = __ffma2_rn(make_float2(vb, vb), p.fxp[i], t23);
+            }
+            t01.y = __fmaf_rn(p.fx[2 * R], v[B0 + 2 * R + 1], t01.y);
+            t23.y = __fmaf_rn(p.fx[2 * R], v[B0 + 2 * R + 3], t23.y);
+          }
         }
-        ring[u % P] = make_float4(t[0], t[1], t[2], t[3]);
+        ring[u % P] = make_float4(t01.x, t01.y, t23.x, t23.y);
         if (k >= 2 * R) {
-          float o[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          // column pass: two columns per FFMA2 (the tap broadcast), each lane its scalar chain
+          float2 o01 = make_float2(0.0f, 0.0f), o23 = make_float2(0.0f, 0.0f);
 #pragma unroll
           for (int j = 0; j < P; ++j) {
             const float4 rr = ring[(u + 1 + j) % P];
-            o[0] = __fmaf_rn(p.gy[j], rr.x, o[0]);
-            o[1] = __fmaf_rn(p.gy[j], rr.y, o[1]);
-            o[2] = __fmaf_rn(p.gy[j], rr.z, o[2]);
-            o[3] = __fmaf_rn(p.gy[j], rr.w, o[3]);
+            const float2 g = make_float2(p.gy[j], p.gy[j]);
+            o01 = __ffma2_rn(g, make_float2(rr.x, rr.y), o01);
+            o23 = __ffma2_rn(g, make_float2(rr.z, rr.w), o23);
           }
+          const float o[4] = {o01.x, o01.y, o23.x, o23.y};
           if (VEC == 4 && xc + 3 < W) {
             st_cs4(drow + xc, make_float4(o[0], o[1], o[2], o[3]));
           } else {
