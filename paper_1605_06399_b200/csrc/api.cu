@@ -14,6 +14,7 @@
 #include <cstring>
 #include <fstream>
 #include <functional>
+#include <deque>
 #include <map>
 #include <mutex>
 #include <sstream>
@@ -138,11 +139,12 @@ static icl_status make_views(const icl_image* src, const icl_image* dst, const i
 }
 
 // ------------------------------------------------------------------ variants
-enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL, K_TILE2, K_BOXX2, K_C2TILE, K_TEX, K_SLIDE, K_BOXW, K_COUNT };
+enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL, K_TILE2, K_BOXX2, K_C2TILE, K_TEX, K_SLIDE, K_BOXW, K_PMAP, K_COUNT };
 struct Variant {
   const char* name;
   Kind kind;
   int nt, vec, S;
+  PmapCfg pm;  // K_PMAP: the paper's Table-1 configuration (pmap.cu)
 };
 
 static const Variant kSepVariants[] = {
@@ -209,10 +211,54 @@ static const Variant kSep3Variants[] = {
     {"tile64x16", K_TILE2, 256, 1, 64},
 };
 
+// The paper's Table-1 space for the one-pixel-per-logical-thread kernels (pmap.cu), appended to
+// the sepconv and Harris tables: CTA shape x coarsening x (mapping, local memory) x unroll =
+// 6 x 6 x 4 x 2 = 288 configurations per filter.  Name: pm_w<wx>x<wy>_c<cx>x<cy>_<map>_l<0|1>_u<1|4>
+// with map = blk (blocked) / int (interleaved) / iwg (interleaved in the work-group; with local
+// memory the interleaving is within the work-group).
+static void append_pmap(std::vector<Variant>* out) {
+  static std::deque<std::string> names;  // storage for the generated names (built once)
+  const int wg[][2] = {{32, 4}, {64, 2}, {128, 1}, {16, 8}, {32, 8}, {64, 4}};
+  const int co[][2] = {{1, 1}, {2, 1}, {4, 1}, {1, 2}, {2, 2}, {1, 4}};
+  const int ml[][2] = {{kMapBlocked, 0}, {kMapInterleaved, 0}, {kMapBlocked, 1}, {kMapInWG, 1}};
+  const char* mname[] = {"blk", "int", "iwg"};
+  for (auto& w : wg)
+    for (auto& c : co)
+      for (auto& m : ml)
+        for (int u : {1, 4}) {
+          char buf[64];
+          snprintf(buf, sizeof buf, "pm_w%dx%d_c%dx%d_%s_l%d_u%d", w[0], w[1], c[0], c[1], mname[m[0]], m[1], u);
+          names.emplace_back(buf);
+          Variant v{};
+          v.name = names.back().c_str();
+          v.kind = K_PMAP;
+          v.nt = w[0] * w[1];
+          v.vec = c[0];
+          v.S = c[1];
+          v.pm = PmapCfg{w[0], w[1], c[0], c[1], m[0], m[1], u};
+          out->push_back(v);
+        }
+}
+
+template <size_t N>
+static std::vector<Variant> with_pmap(const Variant (&base)[N]) {
+  std::vector<Variant> t(base, base + N);
+  append_pmap(&t);
+  return t;
+}
+
 static const Variant* table(icl_filter f, int* n) {
   switch (f) {
-    case ICL_FILTER_SEPCONV: *n = (int)(sizeof kSepVariants / sizeof *kSepVariants); return kSepVariants;
-    case ICL_FILTER_HARRIS: *n = (int)(sizeof kHarVariants / sizeof *kHarVariants); return kHarVariants;
+    case ICL_FILTER_SEPCONV: {
+      static const std::vector<Variant> v = with_pmap(kSepVariants);
+      *n = (int)v.size();
+      return v.data();
+    }
+    case ICL_FILTER_HARRIS: {
+      static const std::vector<Variant> v = with_pmap(kHarVariants);
+      *n = (int)v.size();
+      return v.data();
+    }
     case ICL_FILTER_NLM: *n = (int)(sizeof kNlmVariants / sizeof *kNlmVariants); return kNlmVariants;
     case ICL_FILTER_CONV2D: *n = (int)(sizeof kConvVariants / sizeof *kConvVariants); return kConvVariants;
     case ICL_FILTER_SEPCONV3D: *n = (int)(sizeof kSep3Variants / sizeof *kSep3Variants); return kSep3Variants;
@@ -252,6 +298,12 @@ static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
     if (pc.f == ICL_FILTER_SEPCONV && (pc.sep.rx > 8 || pc.sep.ry > 8)) return false;
     const bool ok_border = sv.border == kBorderClamp || sv.cval == 0.0f;
     if (!tex_eligible(sv, sv.Hg - sv.y0, bt, pc.f == ICL_FILTER_CONV2D ? 1 : 4, ok_border)) return false;
+  }
+  if (v.kind == K_PMAP && v.pm.local) {  // the staged block + halo must fit in shared memory
+    const size_t t = pc.f == ICL_FILTER_SEPCONV
+                         ? (size_t)(v.pm.wx * v.pm.cx + 2 * pc.sep.rx) * (v.pm.wy * v.pm.cy + 2 * pc.sep.ry)
+                         : (size_t)(v.pm.wx * v.pm.cx + pc.har.block + 1) * (v.pm.wy * v.pm.cy + pc.har.block + 1);
+    if (t * sizeof(float) > 227 * 1024) return false;
   }
   if (pc.f == ICL_FILTER_SEPCONV && !pc.sep.pad_rows_ok &&
       (v.kind == K_STREAM || v.kind == K_BULK || v.kind == K_TILE2 || v.kind == K_TEX))
@@ -346,11 +398,13 @@ static cudaError_t run_variant_1(const Prepared& pc, const Variant& v, cudaStrea
       if (v.kind == K_BULK) return launch_sep_bulk(pc.sep, v.nt, v.S, s);
       if (v.kind == K_TILE2) return launch_sep_tile(pc.sep, v.S == 1, s);
       if (v.kind == K_TEX) return launch_sep_tex(pc.sep, s);
+      if (v.kind == K_PMAP) return launch_sep_pmap(pc.sep, v.pm, s);
       return launch_sep_stream(pc.sep, v.nt, v.vec, v.S, s);
     case ICL_FILTER_HARRIS:
       if (v.kind == K_NAIVE) return launch_harris_naive(pc.har, s);
       if (v.kind == K_SHFL) return launch_harris_shfl(pc.har, v.nt, v.S, s);
       if (v.kind == K_SLIDE) return launch_harris_slide(pc.har, v.nt, v.vec == 8 ? 2 : 1, v.S, s);
+      if (v.kind == K_PMAP) return launch_harris_pmap(pc.har, v.pm, s);
       return launch_harris_stream(pc.har, v.nt, v.vec, v.S, s);
     case ICL_FILTER_NLM:
       if (v.kind == K_NAIVE) return launch_nlm_naive(pc.nlm, s);
@@ -383,6 +437,9 @@ static int default_variant(const Prepared& pc) {
   switch (pc.f) {
     case ICL_FILTER_SEPCONV:
       if (!pc.a16) return variant_id(pc.f, pc.pixels < (1 << 20) ? "stream_nt64_s16_v1" : "stream_nt64_s64_v1");
+      // latency-bound small images (BASELINE configs[0], 512^2): the persistent tile kernel's single
+      // pass wins (6.8 vs 9.2 us per call, graph-replayed; tools/small_sweep.py)
+      if (pc.pixels <= (1 << 19)) return variant_id(pc.f, "tile64p_v4");
       if (pc.pixels < (1 << 20)) return variant_id(pc.f, "stream_nt32_s8_v4");
       {
         // the vertical halo 2R is re-read per S output rows: S grows with R;
@@ -746,6 +803,7 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
   cudaEventCreate(&ev1);
   int best = -1, ncand = 0, nrej = 0;
   float best_us = 0.0f;
+  float seen_best_us = 1e38f;
   // Time one variant: verify against the naive output, then the median of >= 10 launches.
   auto evaluate = [&](int v, float* med_out) -> bool {
     ++ncand;
@@ -776,11 +834,19 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
       if (!ok) { ++nrej; return false; }
       }
     }
-    // warm-up then timed reps (median)
+    // warm-up then timed reps (median).  A candidate whose first timed launches already take more
+    // than 2x the best median seen so far cannot win the 0.5% tie-break: it keeps the median of
+    // those (>= 3) launches and the remaining reps are skipped (the pm_* Table-1 space holds
+    // hundreds of such configurations; every candidate is still verified and timed)
     for (int w = 0; w < 2; ++w) run_variant(pc, vt[v], s);
     std::vector<float> ts;
     float total = 0.0f;
     for (int r = 0; r < 50 && (r < 10 || total < 50000.0f); ++r) {
+      if (r == 3 && seen_best_us < 1e30f) {
+        std::vector<float> t3(ts);
+        std::sort(t3.begin(), t3.end());
+        if (t3[1] > 2.0f * seen_best_us) break;
+      }
       if (flush && g_flush) cudaMemsetAsync(g_flush, r & 0xff, g_flush_bytes, s);
       cudaEventRecord(ev0, s);
       run_variant(pc, vt[v], s);
@@ -794,6 +860,7 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
     }
     std::sort(ts.begin(), ts.end());
     *med_out = ts[ts.size() / 2];
+    seen_best_us = std::min(seen_best_us, *med_out);
     return true;
   };
   if (ann_n1 <= 0) {  // exhaustive
@@ -810,7 +877,10 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
       icl_status why;
       if (eligible(pc, vt[v], &why)) ids.push_back(v);
     }
-    constexpr int NK = K_COUNT, NF = NK + 3;
+    // features: kind one-hot, log2 CTA threads, vector width / coarsening x, log2 segment rows /
+    // coarsening y, and the Table-1 axes of the pmap configurations (log2 wx, log2 wy, mapping
+    // one-hot, local memory, log2 unroll; 0 for the hand-built kinds)
+    constexpr int NK = K_COUNT, NF = NK + 3 + 7;
     std::vector<double> feats(ids.size() * NF, 0.0);
     for (size_t i = 0; i < ids.size(); ++i) {
       const Variant& vv = vt[ids[i]];
@@ -819,6 +889,13 @@ static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, ic
       x[NK] = std::log2(1.0 + vv.nt);
       x[NK + 1] = vv.vec;
       x[NK + 2] = std::log2(1.0 + vv.S);
+      if (vv.kind == K_PMAP) {
+        x[NK + 3] = std::log2((double)vv.pm.wx);
+        x[NK + 4] = std::log2((double)vv.pm.wy);
+        x[NK + 5 + vv.pm.map] = 1.0;
+        x[NK + 8] = vv.pm.local;
+        x[NK + 9] = std::log2((double)vv.pm.unr);
+      }
     }
     double bv = 0.0;
     int bi = -1;

@@ -133,4 +133,13 @@ icl_status harris_naive_order(const icl_image* src, const icl_image* response, i
                               float border_value, const icl_image* mask, float threshold, const icl_band* band,
                               void* stream);
 
+// The paper's Table-1 axes as a run-time configuration of one-pixel-per-logical-thread kernels
+// (pmap.cu): CTA (wx, wy), coarsening (cx, cy), mapping (Fig. 4), local memory, unroll factor.
+enum { kMapBlocked = 0, kMapInterleaved = 1, kMapInWG = 2 };
+struct PmapCfg {
+  int wx, wy, cx, cy, map, local, unr;
+};
+cudaError_t launch_sep_pmap(const SepCall& c, const PmapCfg& m, cudaStream_t s);
+cudaError_t launch_harris_pmap(const HarrisCall& c, const PmapCfg& m, cudaStream_t s);
+
 }  // namespace icl

@@ -78,3 +78,20 @@ def check_harris_families(outs, img, block, k, border, c, thr, points=None):
         for name, (R, M) in slide.items():
             np.testing.assert_array_equal(R, Rs, err_msg=name)
             np.testing.assert_array_equal(M, Ms, err_msg=name)
+
+
+def sampled_variants(names):
+    """(id, name) of every hand-built variant plus a fixed sample of the paper's Table-1 space
+    (pm_* configurations, 288 per filter; tests/test_gpu_pmap.py runs all of them): every 11th,
+    which visits every CTA shape, coarsening, mapping / local-memory pair and unroll factor."""
+    out = []
+    k = 0
+    for vid, n in enumerate(names):
+        if n.startswith("pm_"):
+            if k % 11 == 0:
+                out.append((vid, n))
+            k += 1
+        else:
+            out.append((vid, n))
+    return out
+
