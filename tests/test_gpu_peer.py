@@ -13,6 +13,7 @@ import numpy as np
 import pytest
 
 import synth
+from tests._tol import check_harris, check_nlm, check_sepconv
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -22,6 +23,18 @@ if not torch.cuda.is_available():
 
 import torch.distributed as dist  # noqa: E402
 import torch.multiprocessing as mp  # noqa: E402
+
+
+def _edge_points(H, W, cuts, seed, extra=400):
+    """Every pixel of the rows next to each band edge (where the halo came from a peer) plus
+    random pixels: what the oracle checks after the unsharded comparison."""
+    rng = np.random.default_rng(seed)
+    ys, xs = [rng.integers(0, H, extra)], [rng.integers(0, W, extra)]
+    for c in cuts:
+        for y in range(max(0, c - 3), min(H, c + 3)):
+            ys.append(np.full(W, y))
+            xs.append(np.arange(W))
+    return np.concatenate(xs), np.concatenate(ys)
 
 
 def _free_port():
@@ -69,6 +82,9 @@ def _worker(rank, n, port, H, W, B, rx, ry, border, cval):
         icl.sepconv(src, ref, fx, gy, border, cval)
         got = np.concatenate(parts, axis=1)
         np.testing.assert_array_equal(got, ref.cpu().numpy())
+        xs, ys = _edge_points(H, W, [k * rows for k in range(1, n)], 1, extra=200)
+        for b in range(B):  # and the CPU oracle on the edge rows
+            check_sepconv(got[b][ys, xs], full[b], fx, gy, border, cval, points=(xs, ys))
     for p in (up, down):
         if p:
             p.close()
@@ -124,8 +140,11 @@ def _harris_worker(rank, n, port, H, W, block, border, cval):
         icl.force_variant("harris", "naive_direct")  # the peer edge kernels keep the naive order
         icl.harris(src, ref, block, 0.04, border, cval, mask=mref, threshold=0.01)
         icl.force_variant("harris", None)
-        np.testing.assert_array_equal(np.concatenate([p[0] for p in parts]), ref.cpu().numpy())
-        np.testing.assert_array_equal(np.concatenate([p[1] for p in parts]), mref.cpu().numpy())
+        R, M = np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])
+        np.testing.assert_array_equal(R, ref.cpu().numpy())
+        np.testing.assert_array_equal(M, mref.cpu().numpy())
+        xs, ys = _edge_points(H, W, [k * rows for k in range(1, n)], 2)
+        check_harris(R[ys, xs], M[ys, xs], full, block, 0.04, border, cval, 0.01, points=(xs, ys))
     for p in nb.values():
         p.close()
     dist.barrier()
@@ -173,12 +192,17 @@ def _pull_worker(rank, n, port, H, W, filt):
     if rank == 0:
         src = torch.from_numpy(full).to(dev)
         ref = torch.empty_like(src)
+        got = np.concatenate(parts)
+        cuts = [icd.partition(H, n, k, up_rows, down_rows).r0 for k in range(1, n)]
+        xs, ys = _edge_points(H, W, cuts, 3, extra=200)
         if filt == "harris":
             icl.harris(src, ref, 5, 0.04, "clamp")
-            np.testing.assert_array_equal(np.concatenate(parts), ref.cpu().numpy())
+            np.testing.assert_array_equal(got, ref.cpu().numpy())
+            check_harris(got[ys, xs], None, full, 5, 0.04, "clamp", 0.0, 0.0, points=(xs, ys))
         else:  # box-sum tiles restart at band edges: equal to rounding
             icl.nlm(src, ref, 2, 5, 0.1, "clamp")
-            np.testing.assert_allclose(np.concatenate(parts), ref.cpu().numpy(), rtol=0, atol=2e-6)
+            np.testing.assert_allclose(got, ref.cpu().numpy(), rtol=0, atol=2e-6)
+            check_nlm(got[ys, xs], full, 2, 5, 0.1, "clamp", 0.0, points=(xs, ys))
     for p in nb.values():
         p.close()
     dist.barrier()
@@ -224,6 +248,10 @@ def test_peer_paths_in_one_process(nb):
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(out_s), ref_s)
     assert torch.equal(torch.cat(out_h), ref_h) and torch.equal(torch.cat(out_m), ref_m)
+    xs, ys = _edge_points(H, W, [a for a, _ in cuts[1:]], 4)
+    check_sepconv(torch.cat(out_s).cpu().numpy()[ys, xs], full, f, f, "clamp", 0.0, points=(xs, ys))
+    Rh, Mh = torch.cat(out_h).cpu().numpy(), torch.cat(out_m).cpu().numpy()
+    check_harris(Rh[ys, xs], Mh[ys, xs], full, 5, 0.04, "constant", 0.2, 0.01, points=(xs, ys))
 
 
 def test_sepconv_peer_single_rank_and_errors():
