@@ -128,6 +128,7 @@ static icl_status make_views(const icl_image* src, const icl_image* dst, const i
   sv->W = (int)src->width;
   sv->Hg = (int)Hg;
   sv->y0 = (int)sy0;
+  sv->Hl = (int)std::min<int64_t>(src->height, Hg - sy0);
   sv->border = border == ICL_BORDER_CLAMP ? kBorderClamp : kBorderConstant;
   sv->cval = cval;
   dv->base = static_cast<char*>(dst->data);

@@ -580,7 +580,8 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) blur_harris_kernel(BlurHarri
   const int g0 = bp.h.dst.y0 + ly0;
   // every raw row and column the CTA touches (Harris halo + blur radius) inside the image
   const bool interior = x0 - HP - 4 >= 0 && x0 + TW + HP + 4 <= bp.h.src.W && g0 - A - 1 - R >= 0 &&
-                        bp.h.dst.y0 + ly1 + BB + 1 + R <= bp.h.src.Hg &&
+                        bp.h.dst.y0 + ly1 + BB + 1 + R <= bp.h.src.Hg && g0 - A - 1 - R >= bp.h.src.y0 &&
+                        bp.h.dst.y0 + ly1 + BB + 1 + R <= bp.h.src.y0 + bp.h.src.Hl &&
                         ((bp.raw.pitch | (int64_t)bp.raw.base) & 15) == 0;
   if (interior) blur_harris_interior<R, B, NW>(bp, S, smem);
   else blur_harris_general<R, B, NW>(bp, S, smem);

@@ -21,6 +21,7 @@ struct SrcView {
   int y0;             // global row of local row 0
   int border;         // kBorderConstant / kBorderClamp
   float cval;         // constant border value
+  int Hl;             // rows held locally from y0 (a band buffer's rows; Hg - y0 .. for a whole image)
 };
 
 struct DstView {
@@ -47,6 +48,10 @@ __device__ __forceinline__ float read_B(const SrcView& s, int b, int x, int gy) 
     x = clampi(x, 0, s.W - 1);
     gy = clampi(gy, 0, s.Hg - 1);
   }
+  // a row outside the band buffer is never inside an output's stencil (make_views checks the
+  // stencil rows are held); tiles that over-reach the last output row read 0 there, not memory
+  // past the buffer
+  if ((unsigned)(gy - s.y0) >= (unsigned)s.Hl) return 0.0f;
   return __ldg(src_row(s, b, gy) + x);
 }
 

@@ -38,6 +38,7 @@ __device__ __forceinline__ float read_B8(const SrcView& s, int b, int x, int gy)
     x = clampi(x, 0, s.W - 1);
     gy = clampi(gy, 0, s.Hg - 1);
   }
+  if ((unsigned)(gy - s.y0) >= (unsigned)s.Hl) return 0.0f;  // (see read_B)
   const unsigned char* row =
       reinterpret_cast<const unsigned char*>(s.base + (int64_t)b * s.bstride + (int64_t)(gy - s.y0) * s.pitch);
   return (float)__ldg(row + x);
@@ -95,7 +96,8 @@ struct C2Tile {
   static constexpr int N = 2 * R + 1, NT = G::NT;
 
   __device__ static bool interior(const C2Params& p, int x0, int g0) {
-    return x0 - 16 >= 0 && x0 + TW + 16 <= p.src.W && g0 - R >= 0 && g0 + TH + R <= p.src.Hg;
+    return x0 - 16 >= 0 && x0 + TW + 16 <= p.src.W && g0 - R >= 0 && g0 + TH + R <= p.src.Hg &&
+           g0 - R >= p.src.y0 && g0 + TH + R <= p.src.y0 + p.src.Hl;  // (rows held by a band buffer)
   }
   // 16-byte cp.async of the byte tile (rows g0-R .., columns x0-16 ..); caller commits
   __device__ static void stage(const C2Params& p, int b, int x0, int g0, unsigned char* U8) {

@@ -48,7 +48,8 @@ __global__ void __launch_bounds__(256) sep_tile(SepParams p) {
   const int ly0 = blockIdx.y * TH;
   const int g0 = p.dst.y0 + ly0;
   const int W = p.src.W, Hg = p.src.Hg;
-  const bool interior = x0 - HP >= 0 && x0 + TW + HP <= W && g0 - R >= 0 && g0 + TH + R <= Hg;  // (variant requires 16-byte-aligned images)
+  const bool interior = x0 - HP >= 0 && x0 + TW + HP <= W && g0 - R >= 0 && g0 + TH + R <= Hg &&
+                        g0 - R >= p.src.y0 && g0 + TH + R <= p.src.y0 + p.src.Hl;  // (16-byte-aligned images; rows held)
 
   // ---------------- load the input tile
   if (interior) {
@@ -157,7 +158,8 @@ __global__ void __launch_bounds__(256, 2) sep_tile_p(SepParams p, int ntx, int n
     c.ly0 = ty * TH;
     c.x0 = (r - ty * ntx) * TW;
     const int g0 = p.dst.y0 + c.ly0;
-    c.interior = c.x0 - HP >= 0 && c.x0 + TW + HP <= W && g0 - R >= 0 && g0 + TH + R <= Hg;
+    c.interior = c.x0 - HP >= 0 && c.x0 + TW + HP <= W && g0 - R >= 0 && g0 + TH + R <= Hg &&
+                 g0 - R >= p.src.y0 && g0 + TH + R <= p.src.y0 + p.src.Hl;
     return c;
   };
   // interior tile: warp w copies rows w, w+8, ... ; lane v copies 16-byte vector v

@@ -16,6 +16,8 @@ for (h, w) in [(61, 53), (130, 517), (9, 300)]:
     ws = torch.empty(icl.sepconv_workspace_bytes(w, h, 1, 15) // 4 + 1, device=dev)
     for f in ("sepconv", "harris", "nlm"):
         for vid, name in enumerate(icl.variant_names(f)):
+            if name.startswith("pm_") and vid % 11:  # a sample of the 288 Table-1 configurations
+                continue
             icl.force_variant(f, vid)
             for border in ("constant", "clamp"):
                 try:
@@ -68,6 +70,31 @@ hm = torch.empty(100, 96, dtype=torch.uint8).pin_memory()
 icl.harris(hs, hd, 5, 0.04, "clamp", mask=hm, threshold=0.1)
 icl.nlm(hs, hd, 2, 5, 0.1, "clamp")
 torch.cuda.synchronize()
+# every variant through the host path: row bands in the library's exactly-sized staging buffers,
+# so a kernel reading rows past its band buffer shows up here (round 2: the tile kernels did)
+hs2 = torch.from_numpy(synth.uniform_image(6, 150, 200)).pin_memory()
+hd2 = torch.empty(150, 200).pin_memory()
+hm2 = torch.empty(150, 200, dtype=torch.uint8).pin_memory()
+for f in ("sepconv", "harris", "nlm"):
+    for vid, name in enumerate(icl.variant_names(f)):
+        if name.startswith("pm_") and vid % 11:
+            continue
+        icl.force_variant(f, vid)
+        for border in ("constant", "clamp"):
+            try:
+                if f == "sepconv":
+                    for r in (2, 9):
+                        fx = synth.gaussian_taps(r)
+                        icl.sepconv(hs2, hd2, fx, fx, border, 0.5)
+                elif f == "harris":
+                    icl.harris(hs2, hd2, 5, 0.04, border, 0.5, mask=hm2, threshold=0.1)
+                else:
+                    icl.nlm(hs2, hd2, 2, 5, 0.1, border, 0.5)
+            except icl.IclError as e:
+                if e.status not in (3, 4):
+                    raise
+        torch.cuda.synchronize()
+    icl.force_variant(f, None)
 del os.environ["ICL_HOST_CHUNK_ROWS"]
 # fused smoothing + Harris chain (and its two-pass schedule): ragged sizes, all radii, both borders
 for (h, w) in [(61, 52), (130, 516), (300, 200)]:

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--filters", default="sepconv,harris,nlm")
     ap.add_argument("--radius", type=int, default=2)
+    ap.add_argument("--all", action="store_true", help="include the 288 pm_* Table-1 configurations")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     B, S = a.batch, a.size
@@ -63,6 +64,8 @@ def main():
     for f in a.filters.split(","):
         for vid, name in enumerate(icl.variant_names(f)):
             if name.startswith("naive") and S * S * B > (1 << 24) and f == "nlm":
+                continue
+            if name.startswith("pm_") and not a.all:
                 continue
             icl.force_variant(f, vid)
             try:
