@@ -25,6 +25,16 @@
  *    is at  data + b*batch_stride_bytes + y*pitch_bytes + x*elem_size
  *    (x = column = contiguous axis = ImageCL idx; y = row = idy;
  *    PAPER.md:289-296).
+ *  - Environment (read once per process): ICL_TUNE_POLICY = off (default:
+ *    cached winner, else the built-in default variant) | on_miss (tune an
+ *    uncached problem at its first call) | require (ICL_ERR_NOT_TUNED when
+ *    uncached); ICL_TUNE_CACHE = path of a tune cache loaded before the first
+ *    call (when present and for this device/build) and saved after every
+ *    tuning; ICL_FORCE_VARIANT = "filter=variant[,filter=variant]" forces
+ *    variants process-wide (icl_force_variant, per thread, wins); ICL_LOG=1
+ *    prints every dispatch decision (problem key -> variant, reason) to
+ *    stderr; ICL_HOST_CHUNK_ROWS = rows per band of the host-image path.
+ *    Each filter call's enqueue is an NVTX range "icl <filter> <variant>".
  *  - Boundary conditions: reads outside the image return the nearest edge
  *    pixel (CLAMP) or `border_value` (CONSTANT) -- PAPER.md:303-308 and
  *    Fig. 3 (lines 311-327).  Boundaries are applied in GLOBAL image

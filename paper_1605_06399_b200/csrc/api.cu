@@ -4,6 +4,7 @@
 // SURVEY.md §8(a) a11).  No compute happens here: every step of the filters
 // runs in the kernels of sepconv.cu / harris.cu / nlm.cu.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -505,17 +506,77 @@ static const char* policy() {
 static icl_status tune_prepared(Prepared& pc, unsigned flags, cudaStream_t s, icl_variant_info* info, int ann_n1 = 0,
                                  int ann_topk = 0, uint64_t ann_seed = 0);
 
+// ---- environment (include/icl.h "Environment"): ICL_LOG, ICL_FORCE_VARIANT, ICL_TUNE_CACHE
+static bool env_log() {
+  static const bool on = [] {
+    const char* e = getenv("ICL_LOG");
+    return e && *e && strcmp(e, "0") != 0;
+  }();
+  return on;
+}
+
+static int variant_id(icl_filter f, const char* name);
+static const char* filter_name(icl_filter f) {
+  switch (f) {
+    case ICL_FILTER_SEPCONV: return "sepconv";
+    case ICL_FILTER_HARRIS: return "harris";
+    case ICL_FILTER_NLM: return "nlm";
+    case ICL_FILTER_CONV2D: return "conv2d";
+    case ICL_FILTER_SEPCONV3D: return "sepconv3d";
+  }
+  return "?";
+}
+
+// ICL_FORCE_VARIANT="harris=shfl_nw2_s32,nlm=boxsum_x2": process-wide forced variants (the
+// thread-local icl_force_variant wins over it); unknown names are reported once and ignored
+static int env_force(icl_filter f) {
+  static int ids[kNFilters] = {-1, -1, -1, -1, -1};
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = getenv("ICL_FORCE_VARIANT");
+    if (!e) return;
+    std::string spec(e);
+    size_t pos = 0;
+    while (pos < spec.size()) {
+      size_t end = spec.find(',', pos);
+      if (end == std::string::npos) end = spec.size();
+      const std::string item = spec.substr(pos, end - pos);
+      pos = end + 1;
+      const size_t eq = item.find('=');
+      if (eq == std::string::npos) continue;
+      const std::string fn = item.substr(0, eq), vn = item.substr(eq + 1);
+      for (int k = 0; k < kNFilters; ++k) {
+        if (fn != filter_name((icl_filter)k)) continue;
+        int n;
+        const Variant* vt = table((icl_filter)k, &n);
+        int id = -1;
+        for (int i = 0; i < n; ++i)
+          if (vn == vt[i].name) id = i;
+        if (id < 0) fprintf(stderr, "[icl] ICL_FORCE_VARIANT: no variant %s of %s (ignored)\n", vn.c_str(), fn.c_str());
+        ids[k] = id;
+      }
+    }
+  });
+  return (f >= 0 && f < kNFilters) ? ids[f] : -1;
+}
+
+static void env_cache_load();
+static void env_cache_save();
+
 static icl_status dispatch(Prepared& pc, cudaStream_t s) {
   if (pc.f < 0 || pc.f >= kNFilters) return fail(ICL_ERR_INVALID_ARG, "unknown filter");
+  env_cache_load();
   int n;
   const Variant* vt = table(pc.f, &n);
-  int vid = t_force[pc.f];
+  int vid = t_force[pc.f] >= 0 ? t_force[pc.f] : env_force(pc.f);
+  const char* why_s = "forced";
   icl_status why;
   if (vid >= 0) {
     if (vid >= n) return fail(ICL_ERR_INVALID_ARG, "forced variant %d out of range", vid);
     if (!eligible(pc, vt[vid], &why)) return fail(why, "forced variant %s is not eligible for this call", vt[vid].name);
   } else {
     vid = cache_lookup(pc.key);
+    why_s = "tune cache";
     if (vid >= n || (vid >= 0 && !eligible(pc, vt[vid], &why))) vid = -1;
     if (vid < 0) {
       const char* pol = policy();
@@ -525,13 +586,25 @@ static icl_status dispatch(Prepared& pc, cudaStream_t s) {
         icl_status st = tune_prepared(pc, 0, s, &info);
         if (st != ICL_OK) return st;
         t_last[pc.f] = info.variant_id;
+        if (env_log()) fprintf(stderr, "[icl] %s -> %s (tuned on miss)\n", pc.key.c_str(), info.name);
         return ICL_OK;  // the tuner leaves the winner's output in dst
       }
       vid = default_variant(pc);
-      if (!eligible(pc, vt[vid], &why)) vid = 0;
+      why_s = "default";
+      if (!eligible(pc, vt[vid], &why)) {
+        vid = 0;
+        why_s = "default ineligible -> naive";
+      }
     }
   }
+  if (env_log()) fprintf(stderr, "[icl] %s -> %s (%s)\n", pc.key.c_str(), vt[vid].name, why_s);
+  // NVTX range around the enqueue (free without a profiler attached): Nsight / ncu timelines show
+  // which variant each filter call ran
+  char rng[96];
+  snprintf(rng, sizeof rng, "icl %s %s", filter_name(pc.f), vt[vid].name);
+  nvtxRangePushA(rng);
   cudaError_t e = run_variant(pc, vt[vid], s);
+  nvtxRangePop();
   if (e != cudaSuccess) return cuda_fail(e, vt[vid].name);
   t_last[pc.f] = vid;
   return ICL_OK;
@@ -1372,8 +1445,36 @@ static icl_status tune_entry(const icl_problem* p, unsigned flags, void* stream,
       return fail(ICL_ERR_INVALID_ARG, "unknown filter");
   }
   if (st != ICL_OK) return st;
-  return tune_prepared(pc, flags, static_cast<cudaStream_t>(stream), chosen, n1, topk, seed);
+  env_cache_load();
+  const icl_status ts = tune_prepared(pc, flags, static_cast<cudaStream_t>(stream), chosen, n1, topk, seed);
+  if (ts == ICL_OK) env_cache_save();
+  return ts;
 }
+
+extern "C++" {
+namespace icl {
+// ICL_TUNE_CACHE=path: the tune cache persists across processes -- loaded (when the file exists
+// and matches this device/build) before the first dispatch, saved after every tuning
+static void env_cache_load() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* p = getenv("ICL_TUNE_CACHE");
+    if (!p || !*p) return;
+    FILE* f = fopen(p, "r");
+    if (!f) return;
+    fclose(f);
+    if (icl_tune_cache_load(p) != ICL_OK && env_log())
+      fprintf(stderr, "[icl] ICL_TUNE_CACHE %s not loaded: %s\n", p, icl_last_error());
+  });
+}
+
+static void env_cache_save() {
+  const char* p = getenv("ICL_TUNE_CACHE");
+  if (p && *p && icl_tune_cache_save(p) != ICL_OK && env_log())
+    fprintf(stderr, "[icl] ICL_TUNE_CACHE %s not saved: %s\n", p, icl_last_error());
+}
+}  // namespace icl
+}  // extern "C++"
 
 icl_status icl_tune_cache_save(const char* path) {
   if (!path) return fail(ICL_ERR_INVALID_ARG, "null path");
