@@ -106,7 +106,7 @@ def test_model_guided_tuner_finds_the_optimum_of_the_paper_space():
     best-predicted ones timed, the best measured returned.  On the 309-variant sepconv space
     (hand-built kernels + the 288 Table-1 configurations) it must land within 5% of the
     exhaustive optimum while timing fewer than half the variants."""
-    img = synth.uniform_image(7, 2048, 2048)
+    img = synth.uniform_image(7, 4096, 4096)  # ~0.14 ms per call: timing noise well below 5%
     src = torch.from_numpy(img).to(DEV)
     dst = torch.empty_like(src)
     f = synth.gaussian_taps(2)
@@ -114,7 +114,7 @@ def test_model_guided_tuner_finds_the_optimum_of_the_paper_space():
     ex = icl.tune("sepconv", src, dst, taps_x=f, taps_y=f, border="constant", force=True)
     n = len(icl.variant_names("sepconv"))
     icl.tune_cache_clear()
-    an = icl.tune("sepconv", src, dst, taps_x=f, taps_y=f, border="constant", ann=(60, 40, 3))
+    an = icl.tune("sepconv", src, dst, taps_x=f, taps_y=f, border="constant", ann=(60, 60, 3))
     icl.tune_cache_clear()
     assert an["n_candidates"] < n / 2, (an["n_candidates"], n)
     # re-time both winners side by side (the two tuner runs are seconds apart)
@@ -125,7 +125,7 @@ def test_model_guided_tuner_finds_the_optimum_of_the_paper_space():
         ts = []
         for _ in range(3):
             icl.sepconv(src, dst, f, f, "constant")
-        for _ in range(15):
+        for _ in range(31):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
             icl.sepconv(src, dst, f, f, "constant")
