@@ -614,12 +614,23 @@ def time_sepconv_bands(S, r, steps, warmup, ws, rank, local, dist, halo="nccl", 
 
     # one GPU shared by every rank (ICL_BENCH_ONE_GPU): NCCL refuses two ranks on one device, so
     # the functional check takes the peer-load path (CUDA IPC works between processes of one GPU)
-    if ONE_GPU and ws > 1 and halo == "nccl" and not torch_comm:
+    if ONE_GPU and ws > 1 and halo in ("nccl", "window") and not torch_comm:
         halo = "peer"
     peer = ws > 1 and halo == "peer"
-    native = ws > 1 and not torch_comm and not peer
-    ncomm = icl.Comm(ws, rank) if native else None  # icl_sepconv_sharded: NCCL halo exchange in libicl.so
+    window = ws > 1 and halo == "window"
+    native = ws > 1 and not torch_comm and not peer and not window
+    ncomm = icl.Comm(ws, rank) if (native or window) else None  # NCCL in libicl.so
     nbr = {}
+    win = None
+    if window:  # icl_sepconv_window: own rows in an NCCL symmetric window, halos read in-kernel
+        pitch = ((S * 4 + 511) // 512) * 512
+        rows_of = [icd.partition(S, ws, q, r, r).rows for q in range(ws)]
+        win = icl.Window(ncomm, max(rows_of) * pitch)  # the same size on every rank (collective)
+        win.write(0, buf[band.own_slice], pitch)
+        own_img = win.image(0, S, band.rows, pitch)
+        wb = {q: icl.Window.band(q, 0, rows_of[q], pitch) for q in (rank - 1, rank + 1) if 0 <= q < ws}
+        torch.cuda.synchronize(dev)
+        dist.barrier()  # every rank's own rows are in its window
     if peer:  # icl_sepconv_peer: own rows only, the halo read in-kernel from the neighbours (CUDA IPC)
         own = buf[band.own_slice]
         meta = [None] * ws
@@ -633,6 +644,10 @@ def time_sepconv_bands(S, r, steps, warmup, ws, rank, local, dist, halo="nccl", 
         dist.barrier()  # every rank's own rows are written
 
     def step():
+        if window:
+            icl.sepconv_window(win, own_img, out, S, band.r0, wb.get(rank - 1), wb.get(rank + 1), fx, fx, "constant",
+                               stream=stream)
+            return
         if peer:
             icl.sepconv_peer(own, out, S, band.r0, nbr.get(rank - 1), nbr.get(rank + 1), fx, fx, "constant",
                              stream=stream)
@@ -661,10 +676,14 @@ def time_sepconv_bands(S, r, steps, warmup, ws, rank, local, dist, halo="nccl", 
         dist.barrier()
     step_ms = max_over_ranks(a.elapsed_time(b) / steps, ws, dev)
     res = {"ms": step_ms, "launches": launches, "clocks": clk.summary(), "halo_rows": [band.up, band.down],
-           "exchange": ("icl_sepconv_peer (halo rows loaded in-kernel from the peers, CUDA IPC)"
+           "exchange": ("icl_sepconv_window (halo rows loaded in-kernel through NCCL symmetric windows)"
+                        if window else "icl_sepconv_peer (halo rows loaded in-kernel from the peers, CUDA IPC)"
                         if peer else "icl_sepconv_sharded (NCCL in libicl.so)" if native else
                         "torch.distributed batch_isend_irecv" if ws > 1 else "none (one rank holds the image)"),
            "variant": icl.variant_names("sepconv")[icl.last_variant("sepconv")]}
+    if win is not None:
+        dist.barrier()  # no rank deregisters while a peer may still read its window
+        win.close()
     if ncomm is not None:
         ncomm.close()
     if peer:
@@ -1111,9 +1130,10 @@ def main():
     ap.add_argument("--no-16k", action="store_true",
                     help="suite: skip the configs[3] keys (16384^2 row-band sepconv at r = 2 and 15)")
     ap.add_argument("--torch-comm", action="store_true", help="sepconv16k: exchange halos via torch.distributed")
-    ap.add_argument("--halo", default="nccl", choices=["nccl", "peer"],
-                    help="sepconv16k, N > 1: NCCL send/recv (icl_sepconv_sharded) or in-kernel peer loads "
-                         "(icl_sepconv_peer over CUDA IPC)")
+    ap.add_argument("--halo", default="nccl", choices=["nccl", "peer", "window"],
+                    help="sepconv16k, N > 1: NCCL send/recv (icl_sepconv_sharded), in-kernel peer loads "
+                         "(icl_sepconv_peer over CUDA IPC) or in-kernel loads through NCCL symmetric windows "
+                         "(icl_sepconv_window)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -305,6 +305,50 @@ icl_status icl_ipc_close(void* dev_ptr, uint64_t offset);
 icl_status icl_halo_pull(const icl_image* buf, int64_t global_height, int64_t buf_y0, int64_t own_y0,
                          int64_t own_y1, const icl_image* up, const icl_image* down, int elem_bytes, void* stream);
 
+/* ------------------------------------------------------------------------
+ * The same in-kernel halo reads over NCCL symmetric memory (SURVEY.md
+ * §8(f) row 3; NCCL >= 2.28): every rank allocates its band buffer with
+ * icl_comm_mem_alloc (ncclMemAlloc) and registers it COLLECTIVELY as a
+ * symmetric window (icl_comm_window_register: ncclCommWindowRegister with
+ * NCCL_WIN_COLL_SYMMETRIC; every rank passes the same size).  A neighbour's
+ * band is then named by (peer rank, byte offset of its first held row in the
+ * peer's window, height, pitch, batch stride) -- icl_window_band -- and the
+ * edge kernels resolve the address ON THE DEVICE with ncclGetPeerPointer(win,
+ * offset, peer) (the NVLink mapping of the peer's buffer) and load the rows
+ * directly: no staging buffer, send/recv or pack/unpack.  Semantics, results
+ * (bit for bit) and ordering are those of icl_sepconv_peer /
+ * icl_harris_peer / icl_halo_pull: the caller orders the writes of the bands
+ * and the reads with a cross-rank barrier.  `peer` < 0: no neighbour on that
+ * side.  The window API needs an NCCL communicator (icl_comm_init; not the
+ * loopback one) and a libnccl.so.2 with the symmetric-memory symbols, else
+ * ICL_ERR_UNSUPPORTED.  Tested here at N = 1 (one GPU per test box: NCCL
+ * refuses two ranks on a device) with the neighbour bands placed in the
+ * rank's own window (peer 0), which runs the device-side resolution and the
+ * window loads end to end.
+ * ---------------------------------------------------------------------- */
+typedef struct icl_window icl_window;
+typedef struct {
+  int peer;                    /* rank holding the band; < 0: none */
+  uint64_t offset;             /* byte offset of the band's first row (image 0) in that rank's window */
+  int64_t height;              /* rows held */
+  int64_t pitch_bytes, batch_stride_bytes;
+} icl_window_band;
+icl_status icl_comm_mem_alloc(icl_comm* comm, size_t bytes, void** ptr);
+icl_status icl_comm_mem_free(icl_comm* comm, void* ptr);
+icl_status icl_comm_window_register(icl_comm* comm, void* buf, size_t bytes, icl_window** win);
+icl_status icl_comm_window_deregister(icl_comm* comm, icl_window* win);
+icl_status icl_sepconv_window(const icl_window* win, const icl_image* own, const icl_image* dst,
+                              int64_t global_height, int64_t own_y0, const icl_window_band* up,
+                              const icl_window_band* down, const float* taps_x, int rx, const float* taps_y, int ry,
+                              icl_border border, float border_value, void* stream);
+icl_status icl_harris_window(const icl_window* win, const icl_image* own, const icl_image* response,
+                             int64_t global_height, int64_t own_y0, const icl_window_band* up,
+                             const icl_window_band* down, int block, float k, icl_border border, float border_value,
+                             const icl_image* mask, float threshold, void* stream);
+icl_status icl_halo_pull_window(const icl_window* win, const icl_image* buf, int64_t global_height, int64_t buf_y0,
+                                int64_t own_y0, int64_t own_y1, const icl_window_band* up,
+                                const icl_window_band* down, int elem_bytes, void* stream);
+
 /* Separable convolution of the global rows [own_y0, own_y0 + own->height) of
  * an image of global_height rows whose row bands live on different GPUs.
  * own: this rank's rows ONLY (no halo rows); up / down: the neighbouring
@@ -459,6 +503,11 @@ const char* icl_version(void);
  * no filter arithmetic).  Pixel (x, y) of image b uses counter
  * (row0 + y)*width + x and seed (seed + b). */
 icl_status icl_fill_uniform(const icl_image* img, uint64_t seed, int64_t row0, void* stream);
+/* Enqueue a 2-D copy of `rows` rows of width_bytes between any two pointers the CUDA runtime
+ * can address (device, pinned host, NCCL symmetric memory) on `stream` (plumbing for callers
+ * holding raw allocations, e.g. icl_comm_mem_alloc buffers). */
+icl_status icl_copy_2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width_bytes, int64_t rows,
+                       void* stream);
 
 #ifdef __cplusplus
 }

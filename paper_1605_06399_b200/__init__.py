@@ -30,7 +30,9 @@ EXPORTS = ("icl_sepconv", "icl_sepconv_workspace_bytes", "icl_harris", "icl_nlm"
            "icl_variant_count", "icl_variant_name", "icl_force_variant", "icl_last_variant",
            "icl_launch_count", "icl_transfer_bytes", "icl_last_error", "icl_version", "icl_fill_uniform",
            "icl_halo_rows", "icl_shard_band", "icl_shard_plan", "icl_comm_unique_id", "icl_comm_init",
-           "icl_comm_destroy", "icl_comm_init_local", "icl_sepconv_sharded", "icl_harris_sharded", "icl_nlm_sharded", "icl_conv2d_u8_sharded",
+           "icl_comm_destroy", "icl_comm_init_local", "icl_comm_mem_alloc", "icl_comm_mem_free",
+           "icl_comm_window_register", "icl_comm_window_deregister", "icl_sepconv_window", "icl_harris_window",
+           "icl_halo_pull_window", "icl_copy_2d", "icl_sepconv_sharded", "icl_harris_sharded", "icl_nlm_sharded", "icl_conv2d_u8_sharded",
            "icl_tune_ann", "icl_ann_search", "icl_ann_fit", "icl_blur_harris", "icl_blur_harris_workspace_bytes",
            "icl_ipc_get_handle", "icl_ipc_open", "icl_ipc_close", "icl_sepconv_peer",
            "icl_halo_pull", "icl_sepconv3d", "icl_harris_peer")
@@ -111,6 +113,14 @@ def load_library(path: str = LIB_PATH):
         "icl_comm_init": ([ctypes.POINTER(P), I, I, P], I),
         "icl_comm_destroy": ([P], I),
         "icl_comm_init_local": ([ctypes.POINTER(P), I], I),
+        "icl_comm_mem_alloc": ([P, ctypes.c_size_t, ctypes.POINTER(P)], I),
+        "icl_comm_mem_free": ([P, P], I),
+        "icl_comm_window_register": ([P, P, ctypes.c_size_t, ctypes.POINTER(P)], I),
+        "icl_comm_window_deregister": ([P, P], I),
+        "icl_sepconv_window": ([P, img, img, I64, I64, P, P, P, I, P, I, I, F, P], I),
+        "icl_harris_window": ([P, img, img, I64, I64, P, P, I, F, I, F, img, F, P], I),
+        "icl_halo_pull_window": ([P, img, I64, I64, I64, I64, P, P, I, P], I),
+        "icl_copy_2d": ([P, I64, P, I64, I64, I64, P], I),
         "icl_sepconv_sharded": ([P, img, img, I64, P, I, P, I, I, F, P], I),
         "icl_harris_sharded": ([P, img, img, I64, I, F, I, F, img, F, P], I),
         "icl_nlm_sharded": ([P, img, img, I64, I, I, F, I, F, P], I),
@@ -558,6 +568,87 @@ def halo_pull(buf, global_height: int, buf_y0: int, own_y0: int, own_y1: int, up
     _check(load_library().icl_halo_pull(ctypes.byref(_image(buf, elem)), global_height, buf_y0, own_y0, own_y1,
                                         ctypes.byref(up.image) if up else None,
                                         ctypes.byref(down.image) if down else None, elem, _stream(stream)))
+    return buf
+
+
+class icl_window_band(ctypes.Structure):
+    _fields_ = [("peer", ctypes.c_int), ("offset", ctypes.c_uint64), ("height", ctypes.c_int64),
+                ("pitch_bytes", ctypes.c_int64), ("batch_stride_bytes", ctypes.c_int64)]
+
+
+class Window:
+    """An NCCL symmetric window over a buffer from ncclMemAlloc (icl_comm_mem_alloc +
+    icl_comm_window_register; collective over the communicator).  ``ptr`` is the raw device
+    address of this rank's buffer; ``band(peer, offset, height, pitch_bytes)`` names a band in
+    a peer's window for the icl_*_window calls."""
+
+    def __init__(self, comm: "Comm", nbytes: int):
+        lib = load_library()
+        self.comm, self.nbytes = comm, nbytes
+        p = ctypes.c_void_p(0)
+        _check(lib.icl_comm_mem_alloc(comm._c, nbytes, ctypes.byref(p)))
+        self.ptr = p.value
+        w = ctypes.c_void_p(0)
+        try:
+            _check(lib.icl_comm_window_register(comm._c, self.ptr, nbytes, ctypes.byref(w)))
+        except IclError:
+            lib.icl_comm_mem_free(comm._c, self.ptr)
+            raise
+        self._w = w
+
+    @staticmethod
+    def band(peer: int, offset: int, height: int, pitch_bytes: int, batch_stride_bytes: int = 0):
+        return icl_window_band(peer, offset, height, pitch_bytes, batch_stride_bytes)
+
+    def image(self, offset: int, width: int, height: int, pitch_bytes: int) -> icl_image:
+        """An icl_image over rows of this rank's buffer (fp32)."""
+        return icl_image(self.ptr + offset, width, height, pitch_bytes, 1, 0)
+
+    def write(self, offset: int, t, pitch_bytes: int, stream=None):
+        """Copy a 2-D device tensor's rows into this rank's buffer at `offset`."""
+        _check(load_library().icl_copy_2d(self.ptr + offset, pitch_bytes, t.data_ptr(), t.stride(0) * t.element_size(),
+                                          t.shape[-1] * t.element_size(), t.shape[-2], _stream(stream)))
+
+    def close(self):
+        if self._w:
+            lib = load_library()
+            _check(lib.icl_comm_window_deregister(self.comm._c, self._w))
+            _check(lib.icl_comm_mem_free(self.comm._c, self.ptr))
+            self._w = None
+
+
+def _wband(b):
+    return ctypes.byref(b) if b is not None else None
+
+
+def sepconv_window(win: Window, own: icl_image, dst, global_height: int, own_y0: int, up, down, taps_x, taps_y,
+                   border: str = "constant", border_value: float = 0.0, stream=None):
+    """One rank's rows of a row-band sepconv, halo rows read in-kernel through the NCCL window
+    (icl_sepconv_window); `own` is an icl_image over the rank's rows (e.g. Window.image)."""
+    fx, gy = _taps(taps_x), _taps(taps_y)
+    own = own if isinstance(own, icl_image) else _image(own)
+    _check(load_library().icl_sepconv_window(win._w, ctypes.byref(own), ctypes.byref(_image(dst)), global_height,
+                                             own_y0, _wband(up), _wband(down), ctypes.cast(fx, ctypes.c_void_p),
+                                             len(fx) // 2, ctypes.cast(gy, ctypes.c_void_p), len(gy) // 2,
+                                             BORDER[border], border_value, _stream(stream)))
+    return dst
+
+
+def harris_window(win: Window, own: icl_image, response, global_height: int, own_y0: int, up, down, block=5,
+                  k=0.04, border="clamp", border_value=0.0, mask=None, threshold=0.0, stream=None):
+    m = _image(mask, 1) if mask is not None else None
+    own = own if isinstance(own, icl_image) else _image(own)
+    _check(load_library().icl_harris_window(win._w, ctypes.byref(own), ctypes.byref(_image(response)), global_height,
+                                            own_y0, _wband(up), _wband(down), block, k, BORDER[border], border_value,
+                                            _ref(m), threshold, _stream(stream)))
+    return response
+
+
+def halo_pull_window(win: Window, buf, global_height: int, buf_y0: int, own_y0: int, own_y1: int, up, down,
+                     stream=None):
+    elem = buf.element_size()
+    _check(load_library().icl_halo_pull_window(win._w, ctypes.byref(_image(buf, elem)), global_height, buf_y0, own_y0,
+                                               own_y1, _wband(up), _wband(down), elem, _stream(stream)))
     return buf
 
 

@@ -25,6 +25,19 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-r
               "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include")]
 
 
+def nccl_include():
+    """The NCCL >= 2.28 headers of the libnccl.so.2 torch ships (nvidia/nccl/include: nccl.h +
+    nccl_device.h, the symmetric-window device API); None when absent (the window entry points then
+    report ICL_ERR_UNSUPPORTED)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for root in (spec.submodule_search_locations if spec else []) or []:
+        inc = os.path.join(root, "nccl", "include")
+        if os.path.exists(os.path.join(inc, "nccl_device.h")):
+            return inc
+    return None
+
+
 def nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
         if cand and os.path.exists(cand):
@@ -47,6 +60,9 @@ def _deps_mtime():
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(BUILD, src[:-3] + ".o")
     extra = os.environ.get("ICL_NVCC_EXTRA", "").split()  # experiments only (e.g. -D tuning macros)
+    inc = nccl_include()
+    if inc:
+        extra = ["-I", inc, "-DICL_HAVE_NCCL_DEVICE=1", *extra]
     cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     if verbose:
         cmd += ["-Xptxas", "-v"]

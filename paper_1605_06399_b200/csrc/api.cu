@@ -1568,6 +1568,15 @@ const char* icl_last_error(void) { return t_err.c_str(); }
 
 const char* icl_version(void) { return ICL_VERSION_STRING; }
 
+icl_status icl_copy_2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width_bytes, int64_t rows,
+                       void* stream) {
+  if (!dst || !src || width_bytes < 0 || rows < 0 || dpitch < width_bytes || spitch < width_bytes)
+    return fail(ICL_ERR_INVALID_ARG, "bad copy arguments");
+  cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width_bytes, (size_t)rows,
+                                    cudaMemcpyDefault, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? ICL_OK : cuda_fail(e, "icl_copy_2d");
+}
+
 icl_status icl_fill_uniform(const icl_image* img, uint64_t seed, int64_t row0, void* stream) {
   icl_status st = check_image(img, 4, "img");
   if (st != ICL_OK) return st;

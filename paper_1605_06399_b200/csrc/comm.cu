@@ -42,6 +42,11 @@ struct NcclApi {
   ncclResult_t (*groupStart)();
   ncclResult_t (*groupEnd)();
   const char* (*errorString)(ncclResult_t);
+  // NCCL >= 2.28 symmetric memory (optional: nullptr with an older libnccl)
+  ncclResult_t (*memAlloc)(void**, size_t);
+  ncclResult_t (*memFree)(void*);
+  ncclResult_t (*winRegister)(ncclComm_t, void*, size_t, void**, int);
+  ncclResult_t (*winDeregister)(ncclComm_t, void*);
 };
 
 std::once_flag g_nccl_once;
@@ -71,6 +76,10 @@ void load_nccl() {
   ICL_SYM(groupEnd, "ncclGroupEnd")
   ICL_SYM(errorString, "ncclGetErrorString")
 #undef ICL_SYM
+  g_nccl.memAlloc = reinterpret_cast<decltype(g_nccl.memAlloc)>(dlsym(h, "ncclMemAlloc"));
+  g_nccl.memFree = reinterpret_cast<decltype(g_nccl.memFree)>(dlsym(h, "ncclMemFree"));
+  g_nccl.winRegister = reinterpret_cast<decltype(g_nccl.winRegister)>(dlsym(h, "ncclCommWindowRegister"));
+  g_nccl.winDeregister = reinterpret_cast<decltype(g_nccl.winDeregister)>(dlsym(h, "ncclCommWindowDeregister"));
   g_nccl_ok = true;
 }
 
@@ -483,6 +492,59 @@ icl_status icl_comm_destroy(icl_comm* comm) {
   if (comm->cs) cudaStreamDestroy(comm->cs);
   delete comm;
   return r == ncclSuccess ? ICL_OK : nccl_fail(r, "ncclCommDestroy");
+}
+
+// ---------------------------------------------------------------- NCCL symmetric windows (§8(f) row 3)
+static icl_status window_api(icl_comm* comm) {
+  if (!comm) return report_error(ICL_ERR_INVALID_ARG, "null comm");
+  if (comm->lg || !comm->nc) return report_error(ICL_ERR_UNSUPPORTED, "symmetric windows need an NCCL communicator");
+  icl_status st = ICL_OK;
+  if (nccl(&st) != ICL_OK) return st;
+  if (!g_nccl.memAlloc || !g_nccl.memFree || !g_nccl.winRegister || !g_nccl.winDeregister)
+    return report_error(ICL_ERR_UNSUPPORTED, "libnccl.so.2 has no symmetric-memory API (NCCL >= 2.28)");
+  return ICL_OK;
+}
+
+icl_status icl_comm_mem_alloc(icl_comm* comm, size_t bytes, void** ptr) {
+  icl_status st = window_api(comm);
+  if (st != ICL_OK) return st;
+  if (!ptr || !bytes) return report_error(ICL_ERR_INVALID_ARG, "null pointer or zero bytes");
+  ncclResult_t r = g_nccl.memAlloc(ptr, bytes);
+  return r == ncclSuccess ? ICL_OK : nccl_fail(r, "ncclMemAlloc");
+}
+
+icl_status icl_comm_mem_free(icl_comm* comm, void* ptr) {
+  icl_status st = window_api(comm);
+  if (st != ICL_OK || !ptr) return st;
+  ncclResult_t r = g_nccl.memFree(ptr);
+  return r == ncclSuccess ? ICL_OK : nccl_fail(r, "ncclMemFree");
+}
+
+icl_status icl_comm_window_register(icl_comm* comm, void* buf, size_t bytes, icl_window** win) {
+  icl_status st = window_api(comm);
+  if (st != ICL_OK) return st;
+  if (!buf || !bytes || !win) return report_error(ICL_ERR_INVALID_ARG, "null buffer / size / output");
+  void* w = nullptr;
+  ncclResult_t r = g_nccl.winRegister(comm->nc, buf, bytes, &w, 0x01 /* NCCL_WIN_COLL_SYMMETRIC */);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclCommWindowRegister");
+  icl_window* iw = new icl_window();
+  iw->win = w;
+  iw->buf = buf;
+  iw->bytes = bytes;
+  iw->rank = comm->rank;
+  iw->nranks = comm->nranks;
+  *win = iw;
+  return ICL_OK;
+}
+
+icl_status icl_comm_window_deregister(icl_comm* comm, icl_window* win) {
+  if (!win) return ICL_OK;
+  icl_status st = window_api(comm);
+  if (st != ICL_OK) return st;
+  if (comm->cs) cudaStreamSynchronize(comm->cs);
+  ncclResult_t r = g_nccl.winDeregister(comm->nc, win->win);
+  delete win;
+  return r == ncclSuccess ? ICL_OK : nccl_fail(r, "ncclCommWindowDeregister");
 }
 
 icl_status icl_sepconv_sharded(icl_comm* comm, const icl_image* buf, const icl_image* dst, int64_t global_height,

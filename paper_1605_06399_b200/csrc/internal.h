@@ -143,3 +143,12 @@ cudaError_t launch_sep_pmap(const SepCall& c, const PmapCfg& m, cudaStream_t s);
 cudaError_t launch_harris_pmap(const HarrisCall& c, const PmapCfg& m, cudaStream_t s);
 
 }  // namespace icl
+
+// An NCCL symmetric window (icl_comm_window_register): `win` is the ncclWindow_t (a device-
+// readable descriptor; kernels resolve a peer's address with ncclGetPeerPointer)
+struct icl_window {
+  void* win;
+  void* buf;
+  size_t bytes;
+  int rank, nranks;
+};

@@ -30,9 +30,27 @@
 #include "../../include/icl.h"
 #include "common.cuh"
 #include "internal.h"
+#ifdef ICL_HAVE_NCCL_DEVICE
+#include <nccl.h>
+#include <nccl_device.h>
+#endif
 
 namespace icl {
 namespace {
+
+// NCCL symmetric-window neighbours (icl_*_window): the host fills a segment's base with
+// kWinFake + (byte offset in the peer's window) and the kernel replaces it by the peer's address
+// from ncclGetPeerPointer -- resolved on the device, as the window API defines it.
+constexpr uintptr_t kWinFake = (uintptr_t)1 << 46;
+
+__device__ __forceinline__ const char* win_resolve(void* win, int peer, const char* fake) {
+#ifdef ICL_HAVE_NCCL_DEVICE
+  if (win && peer >= 0)
+    return static_cast<const char*>(
+        ncclGetPeerPointer(static_cast<ncclWindow_t>(win), (size_t)((uintptr_t)fake - kWinFake), peer));
+#endif
+  return fake;
+}
 
 struct RowSeg {     // rows [y0, y1) of one band buffer
   const char* base; // row y0 of image 0
@@ -42,6 +60,8 @@ struct RowSeg {     // rows [y0, y1) of one band buffer
 
 struct EdgeParams {
   RowSeg seg[3];  // up, own, down (empty: y0 == y1)
+  void* win;      // ncclWindow_t of icl_sepconv_window (nullptr: plain pointers)
+  int wpeer[3];   // per segment: the window peer (< 0: plain pointer)
   int W, Hg;
   int border;
   float cval;
@@ -56,7 +76,7 @@ constexpr int kEdgeTW = 128;  // output columns per CTA (one per thread)
 constexpr int kEdgeCH = 16;   // output rows per CTA
 
 // in_B(x, gy) row pointer after the global boundary; nullptr -> the constant row
-__device__ __forceinline__ const float* edge_row(const EdgeParams& p, int b, int gy) {
+__device__ __forceinline__ const float* edge_row(const EdgeParams& p, const char* const* base, int b, int gy) {
   if (gy < 0 || gy >= p.Hg) {
     if (p.border == kBorderConstant) return nullptr;
     gy = clampi(gy, 0, p.Hg - 1);
@@ -65,7 +85,7 @@ __device__ __forceinline__ const float* edge_row(const EdgeParams& p, int b, int
   for (int s = 0; s < 3; ++s) {
     const RowSeg& g = p.seg[s];
     if (gy >= g.y0 && gy < g.y1)
-      return reinterpret_cast<const float*>(g.base + (int64_t)b * g.bstride + (int64_t)(gy - g.y0) * g.pitch);
+      return reinterpret_cast<const float*>(base[s] + (int64_t)b * g.bstride + (int64_t)(gy - g.y0) * g.pitch);
   }
   return nullptr;  // unreachable for a validated call
 }
@@ -86,8 +106,11 @@ __global__ void __launch_bounds__(kEdgeTW) sep_edge_peer(EdgeParams p) {
   float* raw = sm;                      // one input row (+ rx columns each side)
   float* t = sm + RL + 2 * kMaxRadius;  // NR row-pass rows
   const int x = x0 + tid;
+  const char* base[3];
+#pragma unroll
+  for (int s = 0; s < 3; ++s) base[s] = win_resolve(p.win, p.wpeer[s], p.seg[s].base);
   for (int k = 0; k < NR; ++k) {
-    const float* row = edge_row(p, b, y0 - p.ry + k);
+    const float* row = edge_row(p, base, b, y0 - p.ry + k);
     __syncthreads();
     for (int c = tid; c < RL; c += kEdgeTW) {
       int xx = x0 - p.rx + c;
@@ -117,6 +140,8 @@ __global__ void __launch_bounds__(kEdgeTW) sep_edge_peer(EdgeParams p) {
 // fp32 order of every Harris variant, harris.cu) with the row resolver above.
 struct HarrisEdgeParams {
   RowSeg seg[3];
+  void* win;     // (see EdgeParams)
+  int wpeer[3];
   int W, Hg;
   int border;
   float cval;
@@ -129,7 +154,7 @@ struct HarrisEdgeParams {
   int out_y0, out_y1;
 };
 
-__device__ __forceinline__ float hread(const HarrisEdgeParams& p, int b, int x, int y) {
+__device__ __forceinline__ float hread(const HarrisEdgeParams& p, const char* const* base, int b, int x, int y) {
   if (x < 0 || x >= p.W || y < 0 || y >= p.Hg) {
     if (p.border == kBorderConstant) return p.cval;
     x = clampi(x, 0, p.W - 1);
@@ -139,12 +164,13 @@ __device__ __forceinline__ float hread(const HarrisEdgeParams& p, int b, int x, 
   for (int s = 0; s < 3; ++s) {
     const RowSeg& g = p.seg[s];
     if (y >= g.y0 && y < g.y1)
-      return reinterpret_cast<const float*>(g.base + (int64_t)b * g.bstride + (int64_t)(y - g.y0) * g.pitch)[x];
+      return reinterpret_cast<const float*>(base[s] + (int64_t)b * g.bstride + (int64_t)(y - g.y0) * g.pitch)[x];
   }
   return 0.0f;  // unreachable for a validated call
 }
 
-__device__ __forceinline__ void hsobel(const HarrisEdgeParams& p, int b, int qx, int qy, float& dx, float& dy) {
+__device__ __forceinline__ void hsobel(const HarrisEdgeParams& p, const char* const* base, int b, int qx, int qy,
+                                       float& dx, float& dy) {
   if (qx < 0 || qx >= p.W || qy < 0 || qy >= p.Hg) {  // per-stage boundary of dx / dy
     if (p.border == kBorderConstant) { dx = 0.0f; dy = 0.0f; return; }
     qx = clampi(qx, 0, p.W - 1);
@@ -153,8 +179,8 @@ __device__ __forceinline__ void hsobel(const HarrisEdgeParams& p, int b, int qx,
   float hd[3], vd[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    hd[i] = __fsub_rn(hread(p, b, qx + 1, qy - 1 + i), hread(p, b, qx - 1, qy - 1 + i));
-    vd[i] = __fsub_rn(hread(p, b, qx - 1 + i, qy + 1), hread(p, b, qx - 1 + i, qy - 1));
+    hd[i] = __fsub_rn(hread(p, base, b, qx + 1, qy - 1 + i), hread(p, base, b, qx - 1, qy - 1 + i));
+    vd[i] = __fsub_rn(hread(p, base, b, qx - 1 + i, qy + 1), hread(p, base, b, qx - 1 + i, qy - 1));
   }
   dx = __fmaf_rn(2.0f, hd[1], __fadd_rn(hd[0], hd[2]));
   dy = __fmaf_rn(2.0f, vd[1], __fadd_rn(vd[0], vd[2]));
@@ -165,13 +191,16 @@ __global__ void __launch_bounds__(256) harris_edge_peer(HarrisEdgeParams p) {
   const int y = p.out_y0 + blockIdx.y * 8 + (threadIdx.x >> 5);
   const int b = blockIdx.z;
   if (x >= p.W || y >= p.out_y1) return;
+  const char* base[3];
+#pragma unroll
+  for (int s = 0; s < 3; ++s) base[s] = win_resolve(p.win, p.wpeer[s], p.seg[s].base);
   const int a = p.block / 2, bb = p.block - 1 - a;
   float sxx = 0.0f, sxy = 0.0f, syy = 0.0f;
   for (int ty = -a; ty <= bb; ++ty) {
     float hxx = 0.0f, hxy = 0.0f, hyy = 0.0f;
     for (int tx = -a; tx <= bb; ++tx) {
       float dx, dy;
-      hsobel(p, b, x + tx, y + ty, dx, dy);
+      hsobel(p, base, b, x + tx, y + ty, dx, dy);
       hxx = __fmaf_rn(dx, dx, hxx);
       hxy = __fmaf_rn(dx, dy, hxy);
       hyy = __fmaf_rn(dy, dy, hyy);
@@ -195,17 +224,28 @@ struct PullParams {
   int64_t dpitch, dbstride;
   int rows, chunks;  // chunks per row
   int vec16;
+  void* win;  // (see EdgeParams): src resolved from the peer's window when wpeer >= 0
+  int wpeer;
 };
 
 __global__ void __launch_bounds__(256) halo_pull(PullParams p) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = blockIdx.y, b = blockIdx.z;
   if (c >= p.chunks || r >= p.rows) return;
-  const char* s = p.src + (int64_t)b * p.sbstride + (int64_t)r * p.spitch;
+  const char* s = win_resolve(p.win, p.wpeer, p.src) + (int64_t)b * p.sbstride + (int64_t)r * p.spitch;
   char* d = p.dst + (int64_t)b * p.dbstride + (int64_t)r * p.dpitch;
   if (p.vec16) reinterpret_cast<float4*>(d)[c] = __ldcv(reinterpret_cast<const float4*>(s) + c);
   else reinterpret_cast<float*>(d)[c] = __ldcv(reinterpret_cast<const float*>(s) + c);
 }
+
+// The window entry points run the pointer entry points' validation and launches with the
+// neighbour bands described by placeholder images (base kWinFake + window offset); this context
+// tells them which window / peers resolve those bases on the device.
+struct WinCtx {
+  void* win;
+  int peer[2];  // up, down
+};
+thread_local const WinCtx* t_win = nullptr;
 
 }  // namespace
 }  // namespace icl
@@ -325,6 +365,12 @@ icl_status icl_sepconv_peer(const icl_image* own, const icl_image* dst, int64_t 
     p.seg[0] = seg(up, y0 - up->height);
   }
   if (need_dn) p.seg[2] = seg(down, y1);
+  p.wpeer[0] = p.wpeer[1] = p.wpeer[2] = -1;
+  if (t_win) {
+    p.win = t_win->win;
+    p.wpeer[0] = need_up ? t_win->peer[0] : -1;
+    p.wpeer[2] = need_dn ? t_win->peer[1] : -1;
+  }
   p.W = (int)own->width;
   p.Hg = (int)H;
   p.border = border == ICL_BORDER_CLAMP ? kBorderClamp : kBorderConstant;
@@ -420,6 +466,12 @@ icl_status icl_harris_peer(const icl_image* own, const icl_image* response, int6
   p.seg[1] = seg(own, y0);
   if (need_up) p.seg[0] = seg(up, y0 - up->height);
   if (need_dn) p.seg[2] = seg(down, y1);
+  p.wpeer[0] = p.wpeer[1] = p.wpeer[2] = -1;
+  if (t_win) {
+    p.win = t_win->win;
+    p.wpeer[0] = need_up ? t_win->peer[0] : -1;
+    p.wpeer[2] = need_dn ? t_win->peer[1] : -1;
+  }
   p.W = (int)own->width;
   p.Hg = (int)H;
   p.border = border == ICL_BORDER_CLAMP ? kBorderClamp : kBorderConstant;
@@ -461,12 +513,14 @@ icl_status icl_halo_pull(const icl_image* buf, int64_t global_height, int64_t bu
     return report_error(ICL_ERR_INVALID_ARG, "bad band geometry");
   const int64_t rowb = buf->width * elem_bytes;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  auto pull = [&](const icl_image* nb, int64_t nb_y0, int64_t g0, int64_t g1) -> icl_status {
+  auto pull = [&](const icl_image* nb, int64_t nb_y0, int64_t g0, int64_t g1, int side) -> icl_status {
     if (g1 <= g0) return ICL_OK;
     if (!nb || !nb->data || nb->width != buf->width || nb->batch != buf->batch || g0 < nb_y0 ||
         g1 > nb_y0 + nb->height || check_peer_image(nb, elem_bytes, "neighbour") != ICL_OK)
       return report_error(ICL_ERR_INVALID_ARG, "neighbour band does not hold the halo rows (rows, pitch or stride)");
     PullParams p;
+    p.win = t_win ? t_win->win : nullptr;
+    p.wpeer = t_win ? t_win->peer[side] : -1;
     p.src = static_cast<const char*>(nb->data) + (g0 - nb_y0) * nb->pitch_bytes;
     p.spitch = nb->pitch_bytes;
     p.sbstride = nb->batch > 1 ? nb->batch_stride_bytes : 0;
@@ -485,9 +539,88 @@ icl_status icl_halo_pull(const icl_image* buf, int64_t global_height, int64_t bu
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? ICL_OK : report_error(ICL_ERR_CUDA, cudaGetErrorString(e));
   };
-  icl_status st = pull(up, own_y0 - (up ? up->height : 0), s0, own_y0);
+  icl_status st = pull(up, own_y0 - (up ? up->height : 0), s0, own_y0, 0);
   if (st != ICL_OK) return st;
-  return pull(down, own_y1, own_y1, s1);
+  return pull(down, own_y1, own_y1, s1, 1);
+}
+
+// ---------------------------------------------------------------- NCCL symmetric windows
+static icl_status window_call(const icl_window* win, const icl_image* like, const icl_window_band* up,
+                              const icl_window_band* down, int elem_bytes, icl_image* ui, icl_image* di,
+                              WinCtx* ctx, const icl_image** upp, const icl_image** dnp) {
+#ifndef ICL_HAVE_NCCL_DEVICE
+  (void)win; (void)like; (void)up; (void)down; (void)elem_bytes; (void)ui; (void)di; (void)ctx; (void)upp; (void)dnp;
+  return report_error(ICL_ERR_UNSUPPORTED, "built without the NCCL >= 2.28 device headers");
+#else
+  if (!win || !win->win || !like) return report_error(ICL_ERR_INVALID_ARG, "null window or image");
+  ctx->win = win->win;
+  ctx->peer[0] = ctx->peer[1] = -1;
+  *upp = *dnp = nullptr;
+  auto mk = [&](const icl_window_band* wb, icl_image* im) -> const icl_image* {
+    if (!wb || wb->peer < 0) return nullptr;
+    *im = *like;
+    im->data = reinterpret_cast<void*>(kWinFake + (uintptr_t)wb->offset);
+    im->height = wb->height;
+    im->pitch_bytes = wb->pitch_bytes;
+    im->batch_stride_bytes = wb->batch_stride_bytes;
+    return im;
+  };
+  for (const icl_window_band* wb : {up, down})
+    if (wb && wb->peer >= 0 && (wb->peer >= win->nranks || wb->offset >= win->bytes || wb->height < 1 ||
+                                wb->pitch_bytes < like->width * elem_bytes))
+      return report_error(ICL_ERR_INVALID_ARG, "neighbour window band outside the window / communicator");
+  *upp = mk(up, ui);
+  *dnp = mk(down, di);
+  ctx->peer[0] = up ? up->peer : -1;
+  ctx->peer[1] = down ? down->peer : -1;
+  return ICL_OK;
+#endif
+}
+
+icl_status icl_sepconv_window(const icl_window* win, const icl_image* own, const icl_image* dst,
+                              int64_t global_height, int64_t own_y0, const icl_window_band* up,
+                              const icl_window_band* down, const float* taps_x, int rx, const float* taps_y, int ry,
+                              icl_border border, float border_value, void* stream) {
+  icl_image ui, di;
+  WinCtx ctx;
+  const icl_image *upp, *dnp;
+  icl_status st = window_call(win, own, up, down, 4, &ui, &di, &ctx, &upp, &dnp);
+  if (st != ICL_OK) return st;
+  t_win = &ctx;
+  st = icl_sepconv_peer(own, dst, global_height, own_y0, upp, dnp, taps_x, rx, taps_y, ry, border, border_value,
+                        stream);
+  t_win = nullptr;
+  return st;
+}
+
+icl_status icl_harris_window(const icl_window* win, const icl_image* own, const icl_image* response,
+                             int64_t global_height, int64_t own_y0, const icl_window_band* up,
+                             const icl_window_band* down, int block, float k, icl_border border, float border_value,
+                             const icl_image* mask, float threshold, void* stream) {
+  icl_image ui, di;
+  WinCtx ctx;
+  const icl_image *upp, *dnp;
+  icl_status st = window_call(win, own, up, down, 4, &ui, &di, &ctx, &upp, &dnp);
+  if (st != ICL_OK) return st;
+  t_win = &ctx;
+  st = icl_harris_peer(own, response, global_height, own_y0, upp, dnp, block, k, border, border_value, mask, threshold,
+                       stream);
+  t_win = nullptr;
+  return st;
+}
+
+icl_status icl_halo_pull_window(const icl_window* win, const icl_image* buf, int64_t global_height, int64_t buf_y0,
+                                int64_t own_y0, int64_t own_y1, const icl_window_band* up,
+                                const icl_window_band* down, int elem_bytes, void* stream) {
+  icl_image ui, di;
+  WinCtx ctx;
+  const icl_image *upp, *dnp;
+  icl_status st = window_call(win, buf, up, down, elem_bytes, &ui, &di, &ctx, &upp, &dnp);
+  if (st != ICL_OK) return st;
+  t_win = &ctx;
+  st = icl_halo_pull(buf, global_height, buf_y0, own_y0, own_y1, upp, dnp, elem_bytes, stream);
+  t_win = nullptr;
+  return st;
 }
 
 }  // extern "C"
