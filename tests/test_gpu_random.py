@@ -3,6 +3,8 @@
 patch+search sizes, random border modes and constants, padded and unpadded
 pitches -- every eligible variant against the oracle, and the variants of
 sepconv / Harris / conv2d against each other bit for bit."""
+import os
+
 import numpy as np
 import pytest
 
@@ -17,7 +19,7 @@ if not torch.cuda.is_available():
 import paper_1605_06399_b200 as icl  # noqa: E402
 
 DEV = torch.device("cuda:0")
-CASES = 64
+CASES = int(os.environ.get("ICL_RANDOM_CASES", "64"))  # (more seeds: ICL_RANDOM_CASES=512)
 
 
 def dev_img(a, pad):
