@@ -170,6 +170,7 @@ static const Variant kSepVariants[] = {
     {"bulk_nt64_s64", K_BULK, 64, 4, 64},
     {"tile64_v4", K_TILE2, 256, 4, 64},
     {"tile64p_v4", K_TILE2, 256, 4, 1},
+    {"tile128p_v4", K_TILE2, 512, 4, 2},
     {"tex_c4s16", K_TEX, 128, 4, 16},
 };
 static const Variant kHarVariants[] = {
@@ -307,6 +308,9 @@ static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
                          : (size_t)(v.pm.wx * v.pm.cx + pc.har.block + 1) * (v.pm.wy * v.pm.cy + pc.har.block + 1);
     if (t * sizeof(float) > 227 * 1024) return false;
   }
+  if (pc.f == ICL_FILTER_SEPCONV && v.kind == K_TILE2 && v.S == 2 &&
+      std::max(pc.sep.rx, pc.sep.ry) < 7)
+    return false;  // tile128p: instantiated for R = 7..15
   if (pc.f == ICL_FILTER_SEPCONV && !pc.sep.pad_rows_ok &&
       (v.kind == K_STREAM || v.kind == K_BULK || v.kind == K_TILE2 || v.kind == K_TEX))
     return false;  // padded-radius variant in a band without max(rx, ry) halo rows
@@ -398,7 +402,7 @@ static cudaError_t run_variant_1(const Prepared& pc, const Variant& v, cudaStrea
       if (v.kind == K_NAIVE) return launch_sep_naive_direct(pc.sep, s);
       if (v.kind == K_TWOPASS) return launch_sep_naive_2pass(pc.sep, s);
       if (v.kind == K_BULK) return launch_sep_bulk(pc.sep, v.nt, v.S, s);
-      if (v.kind == K_TILE2) return launch_sep_tile(pc.sep, v.S == 1, s);
+      if (v.kind == K_TILE2) return v.S == 2 ? launch_sep_tile128(pc.sep, s) : launch_sep_tile(pc.sep, v.S == 1, s);
       if (v.kind == K_TEX) return launch_sep_tex(pc.sep, s);
       if (v.kind == K_PMAP) return launch_sep_pmap(pc.sep, v.pm, s);
       return launch_sep_stream(pc.sep, v.nt, v.vec, v.S, s);

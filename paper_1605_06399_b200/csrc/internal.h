@@ -77,6 +77,7 @@ size_t sep_2pass_workspace(int64_t W, int64_t H, int64_t batch, int ry);
 cudaError_t launch_sep_stream(const SepCall& c, int nt, int vec, int S, cudaStream_t s);
 size_t sep_stream_smem_bytes(int nt, int R);
 cudaError_t launch_sep_bulk(const SepCall& c, int nt, int S, cudaStream_t s);
+cudaError_t launch_sep_tile128(const SepCall& c, cudaStream_t s);
 cudaError_t launch_sep_tile(const SepCall& c, bool persistent, cudaStream_t s);
 
 // harris

@@ -22,9 +22,9 @@
 
 namespace icl {
 
-template <int R>
+template <int R, int TH_ = 64>
 struct TileGeom {
-  static constexpr int TW = 64, TH = 64, NT = 256;
+  static constexpr int TW = 64, TH = TH_, NT = 4 * TH_;  // pass V: 32 column pairs x (NT/32) runs of 8 rows
   static constexpr int HP = ((R + 3) / 4) * 4;
   static constexpr int P = 2 * R + 1;
   static constexpr int IR = TH + 2 * R;          // input / t rows
@@ -129,15 +129,18 @@ __global__ void __launch_bounds__(256) sep_tile(SepParams p) {
 // cp.async into a second input buffer while the current tile runs passes H/V,
 // hiding the global-load latency the one-tile-per-CTA form exposes.  Same
 // arithmetic (bit-identical).
-template <int R>
+// TH_ = 128 (round 2, "tile128p_v4"): 128-row tiles with 512 threads (1 CTA/SM, the same 16
+// warps): the pass-H halo recompute drops from (64+2R)/64 to (128+2R)/128 (1.47 -> 1.23 at R = 15)
+// and each barrier covers twice the work.
+template <int R, int TH_ = 64>
 struct TilePGeom {
-  using G = TileGeom<R>;
+  using G = TileGeom<R, TH_>;
   static constexpr size_t smem_bytes = (size_t)(2 * G::IR * G::IW + G::IR * G::TWS) * sizeof(float);
 };
 
-template <int R>
-__global__ void __launch_bounds__(256, 2) sep_tile_p(SepParams p, int ntx, int nty, int ntiles) {
-  using G = TileGeom<R>;
+template <int R, int TH_ = 64>
+__global__ void __launch_bounds__(4 * TH_, TH_ == 64 ? 2 : 1) sep_tile_p(SepParams p, int ntx, int nty, int ntiles) {
+  using G = TileGeom<R, TH_>;
   constexpr int TW = G::TW, TH = G::TH, HP = G::HP, P = G::P, IR = G::IR, IW = G::IW, IW0 = G::IW0;
   constexpr int TWS = G::TWS, NT = G::NT;
   constexpr int NV = IW0 / 4;  // 16-byte vectors per input row (<= 24 for R <= 15: one lane each)
@@ -162,18 +165,19 @@ __global__ void __launch_bounds__(256, 2) sep_tile_p(SepParams p, int ntx, int n
                  g0 - R >= p.src.y0 && g0 + TH + R <= p.src.y0 + p.src.Hl;
     return c;
   };
-  // interior tile: warp w copies rows w, w+8, ... ; lane v copies 16-byte vector v
+  // interior tile: warp w copies rows w, w+NWARP, ... ; lane v copies 16-byte vector v
+  constexpr int NWARP = NT / 32;
   auto load_async = [&](const Tile& c, float* In) {
     if (lane < NV) {
       const char* g = reinterpret_cast<const char*>(src_row(p.src, c.b, p.dst.y0 + c.ly0 - R + warp) +
                                                     (c.x0 - HP + 4 * lane));
-      const int64_t step = 8 * p.src.pitch;
+      const int64_t step = NWARP * p.src.pitch;
       uint32_t sa = smem_u32(In + warp * IW + 4 * lane);
 #pragma unroll 4
-      for (int r = warp; r < IR; r += 8) {
+      for (int r = warp; r < IR; r += NWARP) {
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g) : "memory");
         g += step;
-        sa += 8 * IW * sizeof(float);
+        sa += NWARP * IW * sizeof(float);
       }
     }
   };
@@ -301,12 +305,12 @@ __global__ void __launch_bounds__(256, 2) sep_tile_p(SepParams p, int ntx, int n
   cp_async_wait<0>();
 }
 
-template <int R>
+template <int R, int TH_ = 64>
 static cudaError_t launch_tilep_R(const SepParams& p, int batch, cudaStream_t s) {
-  using G = TileGeom<R>;
-  constexpr size_t smem = TilePGeom<R>::smem_bytes;
+  using G = TileGeom<R, TH_>;
+  constexpr size_t smem = TilePGeom<R, TH_>::smem_bytes;
   static_assert(smem <= 227 * 1024, "shared memory");
-  auto kern = sep_tile_p<R>;
+  auto kern = sep_tile_p<R, TH_>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -314,7 +318,8 @@ static cudaError_t launch_tilep_R(const SepParams& p, int batch, cudaStream_t s)
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int ntx = (p.src.W + G::TW - 1) / G::TW, nty = (p.dst.H + G::TH - 1) / G::TH;
   const int ntiles = ntx * nty * batch;
-  const int grid = ntiles < 2 * sms ? ntiles : 2 * sms;
+  const int per_sm = TH_ == 64 ? 2 : 1;
+  const int grid = ntiles < per_sm * sms ? ntiles : per_sm * sms;
   kern<<<grid, G::NT, smem, s>>>(p, ntx, nty, ntiles);
   count_launch();
   return cudaGetLastError();
@@ -331,6 +336,23 @@ static cudaError_t launch_tile_R(const SepParams& p, int batch, cudaStream_t s) 
   kern<<<grd, G::NT, G::smem_bytes, s>>>(p);
   count_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_sep_tile128(const SepCall& c, cudaStream_t s) {
+  SepParams p = make_sep_params(c, true);
+  const int R = c.rx > c.ry ? c.rx : c.ry;
+  switch (R) {  // (the radii where the FP32 work, not HBM, bounds the tile kernels)
+    case 7: return launch_tilep_R<7, 128>(p, c.batch, s);
+    case 8: return launch_tilep_R<8, 128>(p, c.batch, s);
+    case 9: return launch_tilep_R<9, 128>(p, c.batch, s);
+    case 10: return launch_tilep_R<10, 128>(p, c.batch, s);
+    case 11: return launch_tilep_R<11, 128>(p, c.batch, s);
+    case 12: return launch_tilep_R<12, 128>(p, c.batch, s);
+    case 13: return launch_tilep_R<13, 128>(p, c.batch, s);
+    case 14: return launch_tilep_R<14, 128>(p, c.batch, s);
+    case 15: return launch_tilep_R<15, 128>(p, c.batch, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_sep_tile(const SepCall& c, bool persistent, cudaStream_t s) {
