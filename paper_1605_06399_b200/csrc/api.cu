@@ -188,6 +188,9 @@ static const Variant kHarVariants[] = {
     {"slide_nw2_s64", K_SLIDE, 2, 4, 64},         {"slide_nw2_s8", K_SLIDE, 2, 4, 8},
     {"slide_nw4_s32", K_SLIDE, 4, 4, 32},         {"slide_nw4_s16", K_SLIDE, 4, 4, 16},
     {"slide_nw2_s32_u2", K_SLIDE, 2, 8, 32},      {"slide_nw2_s16_u2", K_SLIDE, 2, 8, 16},
+    // products' horizontal pair sums first, then vertical chains (vec 6 selects HFIRST)
+    {"slide2_nw2_s32", K_SLIDE, 2, 6, 32},        {"slide2_nw2_s16", K_SLIDE, 2, 6, 16},
+    {"slide2_nw2_s64", K_SLIDE, 2, 6, 64},        {"slide2_nw4_s32", K_SLIDE, 4, 6, 32},
 };
 static const Variant kNlmVariants[] = {
     {"naive_direct", K_NAIVE, 0, 0, 0},
@@ -409,7 +412,7 @@ static cudaError_t run_variant_1(const Prepared& pc, const Variant& v, cudaStrea
     case ICL_FILTER_HARRIS:
       if (v.kind == K_NAIVE) return launch_harris_naive(pc.har, s);
       if (v.kind == K_SHFL) return launch_harris_shfl(pc.har, v.nt, v.S, s);
-      if (v.kind == K_SLIDE) return launch_harris_slide(pc.har, v.nt, v.vec == 8 ? 2 : 1, v.S, s);
+      if (v.kind == K_SLIDE) return launch_harris_slide(pc.har, v.nt, v.vec == 8 ? 2 : v.vec == 6 ? 3 : 1, v.S, s);
       if (v.kind == K_PMAP) return launch_harris_pmap(pc.har, v.pm, s);
       return launch_harris_stream(pc.har, v.nt, v.vec, v.S, s);
     case ICL_FILTER_NLM:

@@ -106,8 +106,10 @@ cudaError_t launch_harris_shfl(const HarrisCall& c, int nw, int S, cudaStream_t 
   return cudaErrorInvalidValue;
 }
 
-template <int NW, int UNR>
+template <int NW, int UNR, bool HF = false>
 cudaError_t dispatch_hslide(const HarrisParams& p, int batch, int S, cudaStream_t s);
+extern template cudaError_t dispatch_hslide<2, 1, true>(const HarrisParams&, int, int, cudaStream_t);
+extern template cudaError_t dispatch_hslide<4, 1, true>(const HarrisParams&, int, int, cudaStream_t);
 extern template cudaError_t dispatch_hslide<2, 1>(const HarrisParams&, int, int, cudaStream_t);
 extern template cudaError_t dispatch_hslide<4, 1>(const HarrisParams&, int, int, cudaStream_t);
 extern template cudaError_t dispatch_hslide<2, 2>(const HarrisParams&, int, int, cudaStream_t);
@@ -116,6 +118,11 @@ extern template cudaError_t dispatch_hslide<4, 2>(const HarrisParams&, int, int,
 // unr: the step loop of interior CTAs unrolled by 1 or 2 (two independent Sobel rows in flight)
 cudaError_t launch_harris_slide(const HarrisCall& c, int nw, int unr, int S, cudaStream_t s) {
   HarrisParams p = make_params(c);
+  if (unr == 3) {  // "slide2": products' horizontal pair sums first (harris_slide.cuh HFIRST)
+    if (nw == 2) return dispatch_hslide<2, 1, true>(p, c.batch, S, s);
+    if (nw == 4) return dispatch_hslide<4, 1, true>(p, c.batch, S, s);
+    return cudaErrorInvalidValue;
+  }
   if (nw == 2) return unr == 2 ? dispatch_hslide<2, 2>(p, c.batch, S, s) : dispatch_hslide<2, 1>(p, c.batch, S, s);
   if (nw == 4) return unr == 2 ? dispatch_hslide<4, 2>(p, c.batch, S, s) : dispatch_hslide<4, 1>(p, c.batch, S, s);
   return cudaErrorInvalidValue;

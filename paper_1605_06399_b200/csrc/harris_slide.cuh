@@ -25,7 +25,12 @@
 
 namespace icl {
 
-template <int B, int NW, bool GEN, bool EDGE, int UNR>
+// HFIRST (round 2, "slide2"): the products' window sums run horizontally first -- per input row
+// the products of the lane's 4 columns and of 2 neighbour columns each side (shuffled), with the
+// per-stage column boundary applied to those products, summed over the B columns by shared pair
+// sums (B = 5: (P0+P1) + (P2+P3) + P4, ...), then the B-1 vertical chains of those row sums (the
+// shfl<> structure with each product computed once per column instead of once per output and tap).
+template <int B, int NW, bool GEN, bool EDGE, int UNR, bool HFIRST = false>
 __device__ __forceinline__ void harris_slide_body(const HarrisParams& p, int S, float* smem) {
   constexpr int A = B / 2;
   constexpr int BB = B - 1 - A;
@@ -201,6 +206,78 @@ __device__ __forceinline__ void harris_slide_body(const HarrisParams& p, int S, 
         for (int q = 0; q < 4; ++q) pp[q] = make_float2(0.0f, 0.0f);
         px[0] = px[1] = make_float2(0.0f, 0.0f);
       }
+      if (HFIRST) {  // horizontal window sums of the products first (pp / px become the row sums)
+        float2 P2[8];
+        float Px[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) P2[2 + q] = pp[q];
+        Px[2] = px[0].x; Px[3] = px[0].y; Px[4] = px[1].x; Px[5] = px[1].y;
+        P2[0].x = __shfl_up_sync(0xffffffffu, pp[2].x, 1);
+        P2[0].y = __shfl_up_sync(0xffffffffu, pp[2].y, 1);
+        P2[1].x = __shfl_up_sync(0xffffffffu, pp[3].x, 1);
+        P2[1].y = __shfl_up_sync(0xffffffffu, pp[3].y, 1);
+        Px[0] = __shfl_up_sync(0xffffffffu, px[1].x, 1);
+        Px[1] = __shfl_up_sync(0xffffffffu, px[1].y, 1);
+        P2[6].x = __shfl_down_sync(0xffffffffu, pp[0].x, 1);
+        P2[6].y = __shfl_down_sync(0xffffffffu, pp[0].y, 1);
+        P2[7].x = __shfl_down_sync(0xffffffffu, pp[1].x, 1);
+        P2[7].y = __shfl_down_sync(0xffffffffu, pp[1].y, 1);
+        Px[6] = __shfl_down_sync(0xffffffffu, px[0].x, 1);
+        Px[7] = __shfl_down_sync(0xffffffffu, px[0].y, 1);
+        if (EDGE) {  // per-stage column boundary of dx/dy, hence of their products: P(clamp(x)) or 0
+          const float2 e0 = el == 0 ? pp[0] : el == 1 ? pp[1] : el == 2 ? pp[2] : pp[3];
+          const float2 e1 = er == 0 ? pp[0] : er == 1 ? pp[1] : er == 2 ? pp[2] : pp[3];
+          const float f0 = el == 0 ? px[0].x : el == 1 ? px[0].y : el == 2 ? px[1].x : px[1].y;
+          const float f1 = er == 0 ? px[0].x : er == 1 ? px[0].y : er == 2 ? px[1].x : px[1].y;
+          float2 gl, gr;
+          gl.x = __shfl_sync(0xffffffffu, e0.x, ll & 31);
+          gl.y = __shfl_sync(0xffffffffu, e0.y, ll & 31);
+          gr.x = __shfl_sync(0xffffffffu, e1.x, lr & 31);
+          gr.y = __shfl_sync(0xffffffffu, e1.y, lr & 31);
+          float hl = __shfl_sync(0xffffffffu, f0, ll & 31);
+          float hr = __shfl_sync(0xffffffffu, f1, lr & 31);
+          if (!clampb) {
+            gl = gr = make_float2(0.0f, 0.0f);
+            hl = hr = 0.0f;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int xe = xl - 2 + j;
+            if (xe < 0) { P2[j] = gl; Px[j] = hl; }
+            else if (xe >= W) { P2[j] = gr; Px[j] = hr; }
+          }
+        }
+        float hx[4];
+        if (B == 5) {  // shared pair sums (A = BB = 2)
+          const float2 a01 = __fadd2_rn(P2[0], P2[1]), a23 = __fadd2_rn(P2[2], P2[3]);
+          const float2 a45 = __fadd2_rn(P2[4], P2[5]), a67 = __fadd2_rn(P2[6], P2[7]);
+          pp[0] = __fadd2_rn(__fadd2_rn(a01, a23), P2[4]);
+          pp[1] = __fadd2_rn(__fadd2_rn(P2[1], a23), a45);
+          pp[2] = __fadd2_rn(__fadd2_rn(a23, a45), P2[6]);
+          pp[3] = __fadd2_rn(__fadd2_rn(P2[3], a45), a67);
+          const float b01 = __fadd_rn(Px[0], Px[1]), b23 = __fadd_rn(Px[2], Px[3]);
+          const float b45 = __fadd_rn(Px[4], Px[5]), b67 = __fadd_rn(Px[6], Px[7]);
+          hx[0] = __fadd_rn(__fadd_rn(b01, b23), Px[4]);
+          hx[1] = __fadd_rn(__fadd_rn(Px[1], b23), b45);
+          hx[2] = __fadd_rn(__fadd_rn(b23, b45), Px[6]);
+          hx[3] = __fadd_rn(__fadd_rn(Px[3], b45), b67);
+        } else {  // direct left-to-right sums
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float2 a = P2[2 + q - A];
+            float bx = Px[2 + q - A];
+#pragma unroll
+            for (int t = 1 - A; t <= BB; ++t) {
+              a = __fadd2_rn(a, P2[2 + q + t]);
+              bx = __fadd_rn(bx, Px[2 + q + t]);
+            }
+            pp[q] = a;
+            hx[q] = bx;
+          }
+        }
+        px[0] = make_float2(hx[0], hx[1]);
+        px[1] = make_float2(hx[2], hx[3]);
+      }
       float2 v2[4], vx[2];
       if (B > 1) {
 #pragma unroll
@@ -224,6 +301,13 @@ __device__ __forceinline__ void harris_slide_body(const HarrisParams& p, int S, 
         vx[1] = px[1];
       }
       if (step < B - 1) continue;
+      float2 s2[4];
+      float sx[4];
+      if (HFIRST) {  // the chains summed the row sums: the window sums are complete
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s2[q] = v2[q];
+        sx[0] = vx[0].x; sx[1] = vx[0].y; sx[2] = vx[1].x; sx[3] = vx[1].y;
+      } else {
       // ---- column sums of columns xl-2 .. xl+5: own 2..5, neighbours' 0,1 and 6,7
       float2 V2[8];
       float Vx[8];
@@ -268,8 +352,6 @@ __device__ __forceinline__ void harris_slide_body(const HarrisParams& p, int S, 
       // ---- horizontal window sums (sliding; the form depends only on the column mod 4)
       // direct horizontal sums, left to right (a sliding sum would cancel across step edges:
       // measured 1e-3 x D on the rectangles scene, beyond the 1e-4 tolerance)
-      float2 s2[4];
-      float sx[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         s2[q] = V2[2 + q - A];
@@ -279,6 +361,7 @@ __device__ __forceinline__ void harris_slide_body(const HarrisParams& p, int S, 
           s2[q] = __fadd2_rn(s2[q], V2[2 + q + t]);
           sx[q] = __fadd_rn(sx[q], Vx[2 + q + t]);
         }
+      }
       }
       float R[4];
 #pragma unroll
@@ -305,7 +388,7 @@ __device__ __forceinline__ void harris_slide_body(const HarrisParams& p, int S, 
   cp_async_wait<0>();
 }
 
-template <int B, int NW, int UNR>
+template <int B, int NW, int UNR, bool HF = false>
 __global__ void __launch_bounds__(32 * NW, 16 / NW) harris_slide(HarrisParams p, int S) {
   extern __shared__ __align__(16) float smem[];
   constexpr int TW = 120 * NW, HP = 8, A = B / 2, BB = B - 1 - A;
@@ -314,17 +397,17 @@ __global__ void __launch_bounds__(32 * NW, 16 / NW) harris_slide(HarrisParams p,
   const int g0 = p.dst.y0 + ly0;
   const bool rows_in = g0 - A - 1 >= 0 && p.dst.y0 + ly1 + BB + 1 <= p.src.Hg;
   const bool cols_in = x0 - HP >= 0 && x0 + TW + HP <= p.src.W;
-  if (rows_in && cols_in) harris_slide_body<B, NW, false, false, UNR>(p, S, smem);
-  else if (rows_in) harris_slide_body<B, NW, false, true, 1>(p, S, smem);
-  else harris_slide_body<B, NW, true, true, 1>(p, S, smem);
+  if (rows_in && cols_in) harris_slide_body<B, NW, false, false, UNR, HF>(p, S, smem);
+  else if (rows_in) harris_slide_body<B, NW, false, true, 1, HF>(p, S, smem);
+  else harris_slide_body<B, NW, true, true, 1, HF>(p, S, smem);
 }
 
-template <int B, int NW, int UNR>
+template <int B, int NW, int UNR, bool HF = false>
 static inline cudaError_t launch_hslide(const HarrisParams& p, int batch, int S, cudaStream_t s) {
   constexpr int TW = 120 * NW;
   constexpr int ROWLEN = TW + 16;
   const size_t smem = (size_t)(HarFastGeom<B>::NSR + 2) * ROWLEN * sizeof(float);  // + 2 mirror rows
-  auto kern = harris_slide<B, NW, UNR>;
+  auto kern = harris_slide<B, NW, UNR, HF>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -335,14 +418,14 @@ static inline cudaError_t launch_hslide(const HarrisParams& p, int batch, int S,
   return cudaGetLastError();
 }
 
-template <int NW, int UNR>
+template <int NW, int UNR, bool HF = false>
 cudaError_t dispatch_hslide(const HarrisParams& p, int batch, int S, cudaStream_t s) {
   switch (p.block) {
-    case 1: return launch_hslide<1, NW, UNR>(p, batch, S, s);
-    case 2: return launch_hslide<2, NW, UNR>(p, batch, S, s);
-    case 3: return launch_hslide<3, NW, UNR>(p, batch, S, s);
-    case 4: return launch_hslide<4, NW, UNR>(p, batch, S, s);
-    case 5: return launch_hslide<5, NW, UNR>(p, batch, S, s);
+    case 1: return launch_hslide<1, NW, UNR, HF>(p, batch, S, s);
+    case 2: return launch_hslide<2, NW, UNR, HF>(p, batch, S, s);
+    case 3: return launch_hslide<3, NW, UNR, HF>(p, batch, S, s);
+    case 4: return launch_hslide<4, NW, UNR, HF>(p, batch, S, s);
+    case 5: return launch_hslide<5, NW, UNR, HF>(p, batch, S, s);
     default: return cudaErrorInvalidValue;  // B = 6, 7 need a wider shuffle halo
   }
 }

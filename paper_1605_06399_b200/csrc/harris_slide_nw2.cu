@@ -5,4 +5,5 @@
 namespace icl {
 template cudaError_t dispatch_hslide<2, 1>(const HarrisParams& p, int batch, int S, cudaStream_t s);
 template cudaError_t dispatch_hslide<2, 2>(const HarrisParams& p, int batch, int S, cudaStream_t s);
+template cudaError_t dispatch_hslide<2, 1, true>(const HarrisParams& p, int batch, int S, cudaStream_t s);
 }  // namespace icl

@@ -62,20 +62,23 @@ def check_conv2d(got, img, filt, border, c, points=None, tol=SEP_TOL):
 
 
 def check_harris_families(outs, img, block, k, border, c, thr, points=None):
-    """The naive-order variants are bit-identical to naive_direct; the slide<> family (separable
-    window sums on the products, re-associated -- SURVEY.md §8(c) R16) is bit-identical within
-    itself and matches the oracle within the Harris tolerance."""
+    """The naive-order variants are bit-identical to naive_direct; each re-associated family
+    (slide_*: vertical sums of the products first; slide2_*: horizontal pair sums first --
+    SURVEY.md §8(c) R16, R27) is bit-identical within itself and matches the oracle
+    within the Harris tolerance."""
     R0, M0 = outs["naive_direct"]
-    slide = {n: v for n, v in outs.items() if n.startswith("slide")}
-    for name, (R, M) in outs.items():
-        if name in slide:
-            continue
-        np.testing.assert_array_equal(R, R0, err_msg=name)
-        np.testing.assert_array_equal(M, M0, err_msg=name)
-    if slide:
-        Rs, Ms = next(iter(slide.values()))
+    fams = {}
+    for name, v in outs.items():
+        fam = name.split("_")[0] if name.startswith("slide") else None
+        if fam is None:
+            np.testing.assert_array_equal(v[0], R0, err_msg=name)
+            np.testing.assert_array_equal(v[1], M0, err_msg=name)
+        else:
+            fams.setdefault(fam, {})[name] = v
+    for fam in fams.values():
+        Rs, Ms = next(iter(fam.values()))
         check_harris(Rs, Ms, img, block, k, border, c, thr, points=points)
-        for name, (R, M) in slide.items():
+        for name, (R, M) in fam.items():
             np.testing.assert_array_equal(R, Rs, err_msg=name)
             np.testing.assert_array_equal(M, Ms, err_msg=name)
 

@@ -504,7 +504,7 @@ def test_model_guided_tuner(tmp_path):
     icl.force_variant("harris", "naive_direct")
     icl.harris(src, ref, 5, 0.04, "clamp")
     icl.force_variant("harris", None)
-    if h["name"].startswith("slide"):  # the re-associated family: the oracle tolerance
+    if h["name"].startswith("slide"):  # the re-associated families: the oracle tolerance
         check_harris(host(dst), None, img, 5, 0.04, "clamp", 0.0, 0.0)
     else:  # every other Harris variant shares the naive fp32 order
         assert torch.equal(dst, ref)
