@@ -1,1 +1,2 @@
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/j25.log 2>&1; echo "pytest rc=$? $(tail -1 gpurun_out/j25.log)"; grep -E "^FAILED" gpurun_out/j25.log | head
+mkdir -p gpurun_out/j26
+ncu --set full --clock-control none --import-source on -k regex:harris_slide -s 3 -c 1 -o gpurun_out/j26/s2 python tools/time_variants.py harris --batch 8 --reps 2 slide2_nw2_s32 > gpurun_out/j26/s2.log 2>&1; echo rc=$?
