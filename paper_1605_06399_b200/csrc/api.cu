@@ -166,6 +166,11 @@ static const Variant kSepVariants[] = {
     {"stream_nt256_s16_v4", K_STREAM, 256, 4, 16},
     {"stream_nt64_s64_v1", K_STREAM, 64, 1, 64},
     {"stream_nt64_s16_v1", K_STREAM, 64, 1, 16},
+    // interior row blocks staged by one cp.async.bulk.tensor (TMA) each (vec 7)
+    {"tma_nt32_s16_v4", K_STREAM, 32, 7, 16},
+    {"tma_nt32_s32_v4", K_STREAM, 32, 7, 32},
+    {"tma_nt32_s64_v4", K_STREAM, 32, 7, 64},
+    {"tma_nt32_s128_v4", K_STREAM, 32, 7, 128},
     {"bulk_nt128_s64", K_BULK, 128, 4, 64},
     {"bulk_nt64_s64", K_BULK, 64, 4, 64},
     {"tile64_v4", K_TILE2, 256, 4, 64},
@@ -456,12 +461,15 @@ static int default_variant(const Prepared& pc) {
         // shared-memory tile kernel wins (16384^2 sweep)
         // (round 2: FFMA2 in both passes of stream<> moved its crossover with tile64p to R = 9;
         // 16384^2: R = 5 / 6 / 7 / 8 in 0.426 / 0.468 / 0.579 / 0.673 ms)
+        // (round 2b: the TMA-fed one-warp stream CTAs beat the cp.async ones at every R <= 10:
+        // 16384^2 R = 1 / 2 / 3 / 5 / 8 / 10 in 0.361 / 0.364 / 0.385 / 0.410 / 0.591 / 0.781 ms
+        // vs 0.378 / 0.383 / 0.403 / 0.453 / 0.664 / 0.841; 8 x 4096^2 R = 2 0.205 vs 0.218 ms)
         const int R = pc.sep.rx > pc.sep.ry ? pc.sep.rx : pc.sep.ry;
-        if (R <= 2) return variant_id(pc.f, "stream_nt64_s16_v4");
-        if (R <= 4) return variant_id(pc.f, "stream_nt64_s32_v4");
-        if (R <= 5) return variant_id(pc.f, "stream_nt64_s64_v4");
-        if (R <= 6) return variant_id(pc.f, "stream_nt128_s64_v4");
-        if (R <= 8) return variant_id(pc.f, "stream_nt64_s128_v4");
+        if (R <= 2) return variant_id(pc.f, "tma_nt32_s16_v4");
+        if (R <= 5) return variant_id(pc.f, "tma_nt32_s32_v4");
+        if (R <= 8) return variant_id(pc.f, "tma_nt32_s64_v4");
+        if (R == 9) return variant_id(pc.f, "tma_nt32_s128_v4");
+        if (R == 10) return variant_id(pc.f, "tma_nt32_s64_v4");
         return variant_id(pc.f, "tile64p_v4");
       }
     case ICL_FILTER_HARRIS:

@@ -122,12 +122,41 @@ size_t sep_stream_smem_bytes(int nt, int R) {
   const int RB = P * ((4 + P - 1) / P);
   const int NSR = RB * (RB <= 8 ? 3 : 2);
   const int HP = ((R + 3) / 4) * 4;
-  return (size_t)NSR * (size_t)(4 * nt + 2 * HP) * sizeof(float);
+  const size_t blk = ((size_t)RB * (4 * nt + 2 * HP) * 4 + 127) / 128 * 128;  // 128-byte block slots
+  return (size_t)(NSR / RB) * blk + 64;
 }
+
+// The source of a sepconv call as a 3-D tensor map for the TMA variants (sepconv_stream.cuh).
+bool make_src_tmap(const SepParams& p, int batch, int box_w, int box_h, CUtensorMap* map) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn enc = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess) fn = nullptr;
+    return reinterpret_cast<EncodeFn>(fn);
+  }();
+  if (!enc) return false;
+  const cuuint64_t rows = (cuuint64_t)p.src.Hl;
+  const cuuint64_t dims[3] = {(cuuint64_t)p.src.W, rows, (cuuint64_t)batch};
+  const cuuint64_t bstride = batch > 1 ? (cuuint64_t)p.src.bstride : (cuuint64_t)p.src.pitch * rows;
+  const cuuint64_t strides[2] = {(cuuint64_t)p.src.pitch, bstride};
+  const cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<char*>(p.src.base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int NT>
+cudaError_t dispatch_stream_tma(const SepParams& p, int R, int batch, int S, cudaStream_t s);
+extern template cudaError_t dispatch_stream_tma<32>(const SepParams&, int, int, int, cudaStream_t);
 
 cudaError_t launch_sep_stream(const SepCall& c, int nt, int vec, int S, cudaStream_t s) {
   SepParams p = make_sep_params(c, true);
   const int R = c.rx > c.ry ? c.rx : c.ry;
+  if (vec == 7) return nt == 32 ? dispatch_stream_tma<32>(p, R, c.batch, S, s) : cudaErrorInvalidValue;  // TMA
   if (vec == 4) {
     if (nt == 32) return dispatch_stream<32, 4>(p, R, c.batch, S, s);
     if (nt == 64) return dispatch_stream<64, 4>(p, R, c.batch, S, s);

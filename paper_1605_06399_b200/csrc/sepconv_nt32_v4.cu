@@ -4,4 +4,5 @@
 
 namespace icl {
 template cudaError_t dispatch_stream<32, 4>(const SepParams& p, int R, int batch, int S, cudaStream_t s);
+template cudaError_t dispatch_stream_tma<32>(const SepParams& p, int R, int batch, int S, cudaStream_t s);
 }  // namespace icl

@@ -1,6 +1,8 @@
 // sepconv_stream.cuh -- the fused streaming sepconv kernel template and its
 // launch helpers; instantiated per CTA width in sepconv_nt*.cu (parallel build).
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -42,17 +44,37 @@ struct StreamGeom {
   static constexpr int RB = P * ((4 + P - 1) / P);
   static constexpr int NBLK = RB <= 8 ? 3 : 2;
   static constexpr int NSR = RB * NBLK;  // rows of shared memory
+  // floats per block slot for a row length L, padded to 128 bytes (a TMA tile destination)
+  static constexpr int blk(int L) { return ((RB * L * 4 + 127) / 128) * 128 / 4; }
 };
 
-template <int R, int NT, int VEC>
-__global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
+// 3-D TMA tile load (cp.async.bulk.tensor: x = column, y = local row, z = image) into shared
+// memory, completion counted on `bar` (expect_tx armed by the issuing thread).
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// TMA (round 2, the "tma_*" variants, NT = 32: a 144-column row fits one tensor box): interior
+// CTAs stage each block of RB input rows with ONE cp.async.bulk.tensor issued by thread 0 (a
+// 144 x RB x 1 box of the source's tensor map -- rows past the band buffer are zero-filled by the
+// TMA unit, never read from memory) and wait on that block's mbarrier instead of per-thread
+// cp.async groups; border CTAs keep the per-thread loader.  Same arithmetic (bit-identical).
+template <int R, int NT, int VEC, bool TMA = false>
+__device__ __forceinline__ void sep_stream_body(const SepParams& p, int S, const CUtensorMap* tmap) {
   constexpr int HP = SepGeom<R>::HP;
   constexpr int P = SepGeom<R>::P;
   constexpr int RB = StreamGeom<R>::RB, NBLK = StreamGeom<R>::NBLK, NSR = StreamGeom<R>::NSR;
   constexpr int TW = 4 * NT;
   constexpr int ROWLEN = TW + 2 * HP;
   constexpr int NSLOT = ROWLEN / 4;
-  extern __shared__ __align__(16) float smem[];
+  extern __shared__ __align__(128) float smem[];
+  constexpr int BLKF = StreamGeom<R>::blk(ROWLEN);  // floats per block slot (128-byte multiple)
+  // smem row of input row k: block slot (k / RB) % NBLK, row k % RB inside it
+  auto srow = [&](int k) { return smem + ((k / RB) % NBLK) * BLKF + (k % RB) * ROWLEN; };
 
   const int tid = threadIdx.x;
   const int b = blockIdx.z;
@@ -68,6 +90,15 @@ __global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
   const bool edge = (x0 - HP < 0) || (x0 + TW + HP > W);
   const bool vint = (g0 - R >= 0) && (g0 - R + NI <= Hg);
   const bool fast = !edge && vint && VEC == 4;  // no boundary work anywhere in this CTA
+  const bool tma = TMA && fast;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NBLK * BLKF);  // NBLK mbarriers (TMA)
+  if (TMA) {
+    if (tid == 0) {
+      for (int i = 0; i < NBLK; ++i) mbar_init(&bars[i], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
 
   // fast-path copy descriptors (columns never change across rows)
   const float* row0 = src_row(p.src, b, fast ? g0 - R : 0);  // row of input k = 0
@@ -76,12 +107,20 @@ __global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
 
   // Issue the loads of rows [kb, kb + RB) into their smem rows (k % NSR).
   auto load_block = [&](int kb) {
+    if (tma) {
+      if (tid == 0) {
+        uint64_t* bar = &bars[(kb / RB) % NBLK];
+        mbar_arrive_expect_tx(bar, (uint32_t)(RB * ROWLEN * sizeof(float)));
+        tma_load_3d(srow(kb), tmap, x0 - HP, g0 - R + kb - p.src.y0, b, bar);
+      }
+      return;
+    }
     if (fast) {
 #pragma unroll
       for (int u = 0; u < RB; ++u) {
         const int k = kb + u;
         if (k < NI) {
-          float* st = smem + (k % NSR) * ROWLEN;
+          float* st = srow(k);
           const float* row = row0 + (int64_t)k * (p.src.pitch >> 2);
           cp_async16(st + 4 * tid, row + c0, 16);
           if (s1 < NSLOT) cp_async16(st + 4 * s1, row + c1, 16);
@@ -92,7 +131,7 @@ __global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
     for (int u = 0; u < RB; ++u) {
       const int k = kb + u;
       if (k >= NI) break;
-      float* st = smem + (k % NSR) * ROWLEN;
+      float* st = srow(k);
       int gi = g0 - R + k;
       if (gi < 0 || gi >= Hg) {
         if (!clampb) {  // constant border: a full row of c
@@ -126,7 +165,7 @@ __global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
     for (int u = 0; u < RB; ++u) {
       const int k = kb + u;
       if (k >= NI) break;
-      float* st = smem + (k % NSR) * ROWLEN;
+      float* st = srow(k);
       const float vl = (il >= 0 && il < ROWLEN) ? st[il] : 0.0f;  // column 0, if in this row
       const float vr = (ir >= 0 && ir < ROWLEN) ? st[ir] : 0.0f;  // column W-1, if in this row
       for (int s = tid; s < NSLOT; s += NT) {
@@ -153,7 +192,8 @@ __global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
 
 #pragma unroll 1
   for (int i = 0; i < NB; ++i) {
-    cp_async_wait<NBLK - 2>();  // block i complete
+    if (tma) mbar_wait(&bars[i % NBLK], (uint32_t)((i / NBLK) & 1));  // block i's TMA landed
+    else cp_async_wait<NBLK - 2>();  // block i complete
     __syncthreads();            // ... for every thread; block i-1's rows are free
     if (edge) {
       fix_block(i * RB);
@@ -165,7 +205,7 @@ __global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
     for (int u = 0; u < RB; ++u) {
       const int k = i * RB + u;
       if (k < NI) {
-        const float* st = smem + (k % NSR) * ROWLEN;
+        const float* st = srow(k);
         float v[4 + 2 * HP];
 #pragma unroll
         for (int q = 0; q < (4 + 2 * HP) / 4; ++q) {
@@ -223,6 +263,16 @@ __global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
   }
   cp_async_wait<0>();
 }
+
+template <int R, int NT, int VEC>
+__global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
+  sep_stream_body<R, NT, VEC, false>(p, S, nullptr);
+}
+
+template <int R, int NT>
+__global__ void __launch_bounds__(NT) sep_stream_tma(SepParams p, int S, const __grid_constant__ CUtensorMap tmap) {
+  sep_stream_body<R, NT, 4, true>(p, S, &tmap);
+}
 // Pipeline invariant: before block i, NBLK-1+i cp.async groups are committed
 // (one per block, empty past the end), so wait_group(NBLK-2) completes block
 // i while block i+1 .. stays in flight; block i+NBLK-1 is issued into the
@@ -232,7 +282,7 @@ __global__ void __launch_bounds__(NT) sep_stream(SepParams p, int S) {
 template <int R, int NT, int VEC>
 static inline cudaError_t launch_stream_R(const SepParams& p, int batch, int S, cudaStream_t s) {
   constexpr int ROWLEN = 4 * NT + 2 * SepGeom<R>::HP;
-  const size_t smem = (size_t)StreamGeom<R>::NSR * ROWLEN * sizeof(float);
+  const size_t smem = (size_t)StreamGeom<R>::NBLK * StreamGeom<R>::blk(ROWLEN) * sizeof(float);
   auto kern = sep_stream<R, NT, VEC>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -242,6 +292,45 @@ static inline cudaError_t launch_stream_R(const SepParams& p, int batch, int S, 
   kern<<<grd, NT, smem, s>>>(p, S);
   count_launch();
   return cudaGetLastError();
+}
+
+// The source as a 3-D tensor map (x = W columns, y = the rows held locally, z = images), box
+// ROWLEN x RB x 1, zero fill out of bounds (cuTensorMapEncodeTiled through the runtime's driver
+// entry point: no link-time libcuda dependency).
+bool make_src_tmap(const SepParams& p, int batch, int box_w, int box_h, CUtensorMap* map);
+
+template <int R, int NT>
+static inline cudaError_t launch_stream_tma_R(const SepParams& p, int batch, int S, cudaStream_t s) {
+  constexpr int ROWLEN = 4 * NT + 2 * SepGeom<R>::HP;
+  static_assert(ROWLEN <= 256, "one tensor box per row block");
+  const size_t smem = (size_t)StreamGeom<R>::NBLK * StreamGeom<R>::blk(ROWLEN) * sizeof(float) +
+                      8 * StreamGeom<R>::NBLK;
+  CUtensorMap map;
+  if (!make_src_tmap(p, batch, ROWLEN, StreamGeom<R>::RB, &map)) return cudaErrorNotSupported;
+  auto kern = sep_stream_tma<R, NT>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grd((p.src.W + 4 * NT - 1) / (4 * NT), (p.dst.H + S - 1) / S, batch);
+  kern<<<grd, NT, smem, s>>>(p, S, map);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int NT>
+cudaError_t dispatch_stream_tma(const SepParams& p, int R, int batch, int S, cudaStream_t s) {
+  switch (R) {
+#define ICL_SEPT_CASE(r) \
+  case r:                \
+    return launch_stream_tma_R<r, NT>(p, batch, S, s);
+    ICL_SEPT_CASE(0) ICL_SEPT_CASE(1) ICL_SEPT_CASE(2) ICL_SEPT_CASE(3) ICL_SEPT_CASE(4) ICL_SEPT_CASE(5)
+    ICL_SEPT_CASE(6) ICL_SEPT_CASE(7) ICL_SEPT_CASE(8) ICL_SEPT_CASE(9) ICL_SEPT_CASE(10) ICL_SEPT_CASE(11)
+    ICL_SEPT_CASE(12) ICL_SEPT_CASE(13) ICL_SEPT_CASE(14) ICL_SEPT_CASE(15)
+#undef ICL_SEPT_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
 }
 
 template <int NT, int VEC>
