@@ -60,6 +60,7 @@ def measured_peaks():
 # (the S = segment-rows variants of one family launch the same kernel function)
 KERNEL_OF = {"boxsum_x2": ("nlm_box_x2",), "boxsum_r8": ("nlm_box_r8",),
              **{f"stream_nt64_s{s}_v4": ("sep_stream<2, 64",) for s in (16, 32, 64, 128)},
+             **{f"tma_nt32_s{s}_v4": ("sep_stream_tma<2, 32",) for s in (16, 32, 64, 128)},
              **{f"shfl_nw2_s{s}": ("harris_shfl<5, 2>",) for s in (8, 16, 32, 64, 128)}}
 
 
