@@ -35,6 +35,7 @@ bool nlm_r8_supported(int P, int S);
 bool nlm_r16_supported(int P, int S);
 bool nlm_x2_supported(int P, int S);
 bool nlm_w_supported(int P, int S);
+bool nlm_sym_supported(int P, int S);
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -141,7 +142,7 @@ static icl_status make_views(const icl_image* src, const icl_image* dst, const i
 }
 
 // ------------------------------------------------------------------ variants
-enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL, K_TILE2, K_BOXX2, K_C2TILE, K_TEX, K_SLIDE, K_BOXW, K_PMAP, K_COUNT };
+enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL, K_TILE2, K_BOXX2, K_C2TILE, K_TEX, K_SLIDE, K_BOXW, K_PMAP, K_BOXSYM, K_COUNT };
 struct Variant {
   const char* name;
   Kind kind;
@@ -205,6 +206,7 @@ static const Variant kNlmVariants[] = {
     {"boxsum_r16", K_BOXR16, 0, 0, 0},
     {"boxsum_x2", K_BOXX2, 0, 0, 0},
     {"boxsum_w", K_BOXW, 0, 0, 1},
+    {"sym_tmem", K_BOXSYM, 0, 0, 0},
 };
 
 static const Variant kConvVariants[] = {
@@ -338,6 +340,7 @@ static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXR16 && !nlm_r16_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXX2 && !nlm_x2_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXW && !nlm_w_supported(pc.nlm.P, pc.nlm.S)) return false;
+  if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXSYM && !nlm_sym_supported(pc.nlm.P, pc.nlm.S)) return false;
   return true;
 }
 
@@ -427,6 +430,7 @@ static cudaError_t run_variant_1(const Prepared& pc, const Variant& v, cudaStrea
       if (v.kind == K_BOXR16) return launch_nlm_r16(pc.nlm, s);
       if (v.kind == K_BOXX2) return launch_nlm_x2(pc.nlm, s);
       if (v.kind == K_BOXW) return launch_nlm_w(pc.nlm, v.S, s);
+      if (v.kind == K_BOXSYM) return launch_nlm_sym(pc.nlm, s);
       return launch_nlm_boxsum(pc.nlm, 0, s);
     case ICL_FILTER_CONV2D:
       if (v.kind == K_NAIVE) return launch_conv2d_naive(pc.c2d, s);
@@ -482,6 +486,8 @@ static int default_variant(const Prepared& pc) {
       // (1024^2 24.5 vs 34.8 us, 2048^2 30.7 vs 66 us, 4096^2 76 vs 90 us; 8 x 4096^2 prefers s64)
       return variant_id(pc.f, pc.pixels <= (1 << 21) ? "shfl_nw2_s8" : pc.pixels <= (1 << 25) ? "shfl_nw2_s16" : "shfl_nw2_s32");
     case ICL_FILTER_NLM:
+      // the offset-symmetric TMEM kernel once the launch fills the GPU (118 x 128 tiles, 2 CTAs/SM)
+      if (nlm_sym_supported(pc.nlm.P, pc.nlm.S) && pc.pixels >= (1 << 23)) return variant_id(pc.f, "sym_tmem");
       if (nlm_x2_supported(pc.nlm.P, pc.nlm.S)) return variant_id(pc.f, "boxsum_x2");
       if (nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return variant_id(pc.f, "boxsum_r8");
       return nlm_tiled_supported(pc.nlm.P, pc.nlm.S) ? variant_id(pc.f, "tiled_direct_32x8") : 0;

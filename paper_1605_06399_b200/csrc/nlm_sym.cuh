@@ -1,0 +1,408 @@
+// nlm_sym.cuh -- NLM variant "sym_tmem": the offset-symmetric formulation.  (NLM is not in
+// PAPER.md; definition DESIGN.md R11-R14, this formulation R30.)
+//
+// With the boundary-extended image u_B, the patch distance is symmetric under a shift:
+//   d_{-o}(p) = sum_t (u_B(p+t) - u_B(p+t-o))^2 = d_o(p-o)          (substitute t' = t - o)
+// so one weight w_o(q) = 2^(-coef * d_o(q)) serves two (pixel, offset) pairs:
+//   own      (q, o):   num(q)   += w * u_B(q+o),  den(q)   += w
+//   partner  (q+o,-o): num(q+o) += w * u_B(q),    den(q+o) += w
+// Walking the half set  O+ = {oy > 0, |ox| <= S} u {oy = 0, 0 < ox <= S}  (plus the centre,
+// w = 1) covers every pair of the (2S+1)^2 window exactly once, with half the patch distances
+// and half the ex2 of the direct enumeration.
+//
+// Layout (one warp = one 4-column-per-lane strip of 128 d-columns, walking 32 rows):
+//   * the CTA's image tile (plus the 2(S+P)+1 halo rows and 2S+2P halo columns, boundary
+//     applied at load time) sits in shared memory; 4 warps stack vertically (128 output rows);
+//   * a warp's d-columns are [X-S, X-S+128): the 128-2S output columns plus S on each side,
+//     the partner sources tile - o of the shifts that cross the strip edge;
+//   * per search row oy (outer loop) the warp walks d-rows y from -oy to 31 (the rows above
+//     the strip are partner sources), the vertical patch sum sliding
+//        d(y) = d(y-1) + H(y+P) - H(y-P-1),  H(r) = horizontal patch sum of (u(q)-u(q+o))^2,
+//     in registers for all 2S+1 ox at once, as float2 pairs of adjacent ox (FADD2/FFMA2);
+//     H_old is recomputed from the image rows, not stored (no ring);
+//   * own contributions accumulate in registers per row; partner contributions accumulate in a
+//     (4+2S)-column register window which the lanes exchange by warp shuffles (columns that
+//     belong to the neighbouring lanes);
+//   * num/den of the warp's 32 x 128 pixels live in TENSOR MEMORY (one TMEM lane per thread,
+//     8 columns per row: num[4], den[4]), read-modify-written once per (row, oy) for the own
+//     row and once for the partner row, with tcgen05.ld / tcgen05.st -- the on-chip space that
+//     lets the walk be long (32 rows) without giving up registers or shared memory.
+// Results agree with the direct definition to rounding (tolerance-checked, R16).
+#pragma once
+
+#include "nlm_common.cuh"
+
+namespace icl {
+
+__device__ __forceinline__ float2 s2_add(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 s2_sub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 s2_mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 s2_fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+
+// ---- tensor memory (tcgen05) helpers: 32 lanes x 32 bit, 8 consecutive columns per thread
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r0, r1, r2, r3, r4, r5, r6, r7;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3), "=r"(r4), "=r"(r5), "=r"(r6), "=r"(r7)
+               : "r"(taddr));
+  v[0] = __uint_as_float(r0); v[1] = __uint_as_float(r1); v[2] = __uint_as_float(r2); v[3] = __uint_as_float(r3);
+  v[4] = __uint_as_float(r4); v[5] = __uint_as_float(r5); v[6] = __uint_as_float(r6); v[7] = __uint_as_float(r7);
+}
+// wait for the outstanding tcgen05.ld; the values are threaded through the asm so no use of
+// them can be scheduled above the wait
+__device__ __forceinline__ void tm_wait_ld(float (&a)[8], float (&b)[8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+f"(a[0]), "+f"(a[1]), "+f"(a[2]), "+f"(a[3]), "+f"(a[4]), "+f"(a[5]), "+f"(a[6]), "+f"(a[7]),
+                 "+f"(b[0]), "+f"(b[1]), "+f"(b[2]), "+f"(b[3]), "+f"(b[4]), "+f"(b[5]), "+f"(b[6]), "+f"(b[7])
+               :
+               : "memory");
+}
+__device__ __forceinline__ void tm_st8(uint32_t taddr, const float (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+template <int P, int S>
+struct SymGeom {
+  static constexpr int C = 4;                 // columns per lane
+  static constexpr int NW = 4;                // warps per CTA (stacked vertically)
+  static constexpr int T = 32;                // output rows per warp
+  static constexpr int NT = 32 * NW;
+  static constexpr int TWO = 128 - 2 * S;     // output columns per strip
+  static constexpr int TH = NW * T;           // output rows per CTA
+  static constexpr int SW = (128 + 2 * S + 2 * P + 3) / 4 * 4;  // smem row (floats), col j <-> X - 2S - P + j
+  static constexpr int SH0 = TH + 2 * (S + P) + 1;               // smem rows used, row i <-> Y - S - P - 1 + i
+  static constexpr int SH = SH0;
+  static constexpr int NCW = C + 2 * P;       // centre window of a lane (H)
+  static constexpr int NSW = C + 2 * P + 2 * S;  // shifted window (H, every ox)
+  static constexpr int NIW = C + 2 * S;       // accumulation window u(q + o), and the partner window
+  static constexpr int TMEM_COLS = 8 * T;     // num[4] den[4] per row
+  static constexpr size_t smem_bytes = (size_t)SW * SH * sizeof(float);
+  static_assert(S >= 1 && S <= 8, "partner exchange reaches two lanes");
+  static_assert(TMEM_COLS == 256, "two CTAs per SM share the 512 TMEM columns");
+};
+
+// N consecutive floats starting OFF floats after a 16-byte aligned lane base, via LDS.128
+template <int OFF, int N>
+__device__ __forceinline__ void sym_ld_win(const float* base, float (&v)[N]) {
+  constexpr int A = OFF & ~3;
+  constexpr int NQ = (OFF + N - A + 3) / 4;
+  float tmp[4 * NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const float4 f = reinterpret_cast<const float4*>(base + A)[q];
+    tmp[4 * q] = f.x; tmp[4 * q + 1] = f.y; tmp[4 * q + 2] = f.z; tmp[4 * q + 3] = f.w;
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = tmp[OFF - A + i];
+}
+
+template <int P, int S, int OXMIN>
+struct SymPass {
+  static constexpr int NOX = S - OXMIN + 1;
+  static constexpr int NPAIR = (NOX + 1) / 2;
+  __host__ __device__ static constexpr int oxa(int g) { return OXMIN + 2 * g; }
+  __host__ __device__ static constexpr bool single(int g) { return OXMIN + 2 * g + 1 > S; }
+  __host__ __device__ static constexpr int oxb(int g) { return single(g) ? OXMIN + 2 * g : OXMIN + 2 * g + 1; }
+};
+
+// D[g][k] += H_{(oxa,oxb)}(column k, image row of crow), one pair of ox per float2 (the walk's
+// initial window)
+template <int P, int S, int OXMIN>
+__device__ __forceinline__ void sym_acc_H(float2 (&D)[SymPass<P, S, OXMIN>::NPAIR][4], const float* crow,
+                                          const float* srow) {
+  using G = SymGeom<P, S>;
+  using Q = SymPass<P, S, OXMIN>;
+  constexpr int C = G::C, NCW = G::NCW, NSW = G::NSW;
+  float cen[NCW], sh[NSW];
+  sym_ld_win<S, NCW>(crow, cen);
+  sym_ld_win<0, NSW>(srow, sh);
+#pragma unroll
+  for (int g = 0; g < Q::NPAIR; ++g) {
+    float2 df[NCW];
+#pragma unroll
+    for (int t = 0; t < NCW; ++t)
+      df[t] = s2_sub(make_float2(cen[t], cen[t]), make_float2(sh[t + Q::oxa(g) + S], sh[t + Q::oxb(g) + S]));
+    float2 a = s2_mul(df[0], df[0]);
+#pragma unroll
+    for (int t = 1; t <= 2 * P; ++t) a = s2_fma(df[t], df[t], a);
+    D[g][0] = s2_add(D[g][0], a);
+#pragma unroll
+    for (int k = 1; k < C; ++k) {
+      a = s2_fma(df[k + 2 * P], df[k + 2 * P], a);
+      a = s2_fma(make_float2(-df[k - 1].x, -df[k - 1].y), df[k - 1], a);
+      D[g][k] = s2_add(D[g][k], a);
+    }
+  }
+}
+
+// One step of the vertical slide: D[g][k] += H(new row) - H(old row), the difference formed in
+// one FFMA2 chain per pair (sum of the new squares minus the old ones, then slid along k)
+template <int P, int S, int OXMIN>
+__device__ __forceinline__ void sym_slide_H(float2 (&D)[SymPass<P, S, OXMIN>::NPAIR][4], const float* crow_n,
+                                            const float* srow_n, const float* crow_o, const float* srow_o) {
+  using G = SymGeom<P, S>;
+  using Q = SymPass<P, S, OXMIN>;
+  constexpr int C = G::C, NCW = G::NCW, NSW = G::NSW;
+  float cn[NCW], sn[NSW], co[NCW], so[NSW];
+  sym_ld_win<S, NCW>(crow_n, cn);
+  sym_ld_win<0, NSW>(srow_n, sn);
+  sym_ld_win<S, NCW>(crow_o, co);
+  sym_ld_win<0, NSW>(srow_o, so);
+#pragma unroll
+  for (int g = 0; g < Q::NPAIR; ++g) {
+    float2 dn[NCW], dd[NCW];
+#pragma unroll
+    for (int t = 0; t < NCW; ++t) {
+      dn[t] = s2_sub(make_float2(cn[t], cn[t]), make_float2(sn[t + Q::oxa(g) + S], sn[t + Q::oxb(g) + S]));
+      dd[t] = s2_sub(make_float2(co[t], co[t]), make_float2(so[t + Q::oxa(g) + S], so[t + Q::oxb(g) + S]));
+    }
+    float2 a = s2_mul(dn[0], dn[0]);
+#pragma unroll
+    for (int t = 1; t <= 2 * P; ++t) a = s2_fma(dn[t], dn[t], a);
+#pragma unroll
+    for (int t = 0; t <= 2 * P; ++t) a = s2_fma(make_float2(-dd[t].x, -dd[t].y), dd[t], a);
+    D[g][0] = s2_add(D[g][0], a);
+#pragma unroll
+    for (int k = 1; k < C; ++k) {
+      a = s2_fma(dn[k + 2 * P], dn[k + 2 * P], a);
+      a = s2_fma(make_float2(-dn[k - 1].x, -dn[k - 1].y), dn[k - 1], a);
+      a = s2_fma(make_float2(-dd[k + 2 * P].x, -dd[k + 2 * P].y), dd[k + 2 * P], a);
+      a = s2_fma(dd[k - 1], dd[k - 1], a);
+      D[g][k] = s2_add(D[g][k], a);
+    }
+  }
+}
+
+// One search row oy of the warp's walk.  U: smem tile; wrow0: smem row of the warp's d-row 0;
+// lanebase: lane's column offset (4 * lane); tm: the thread's TMEM address (column 0).
+template <int P, int S, int OXMIN>
+__device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, int oy, uint32_t tm, float2 nc) {
+  using G = SymGeom<P, S>;
+  using Q = SymPass<P, S, OXMIN>;
+  constexpr int C = G::C, SW = G::SW, T = G::T, NIW = G::NIW, NP = Q::NPAIR;
+  const float* Ul = U + 4 * lane;
+  auto row = [&](int y) { return Ul + (wrow0 + y) * SW; };
+
+  float2 D[NP][C];
+#pragma unroll
+  for (int g = 0; g < NP; ++g)
+#pragma unroll
+    for (int k = 0; k < C; ++k) D[g][k] = make_float2(0.0f, 0.0f);
+  const int y0 = -oy;
+  // d(y0) + H(y0-P-1): the first step subtracts that row again
+#pragma unroll 1
+  for (int r = y0 - P - 1; r <= y0 + P - 1; ++r) sym_acc_H<P, S, OXMIN>(D, row(r), row(r + oy));
+
+#pragma unroll 1
+  for (int y = y0; y < T; ++y) {
+    sym_slide_H<P, S, OXMIN>(D, row(y + P), row(y + P + oy), row(y - P - 1), row(y - P - 1 + oy));
+
+    float ia[NIW], io[C];
+    sym_ld_win<P, NIW>(row(y + oy), ia);   // u(q + o), q + o - (X - S + 4 lane) in [-S, C + S)
+    sym_ld_win<S + P, C>(row(y), io);      // u(q)
+    float2 A[C], B[C], Pn[NIW], Pd[NIW];
+#pragma unroll
+    for (int k = 0; k < C; ++k) A[k] = B[k] = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int j = 0; j < NIW; ++j) Pn[j] = Pd[j] = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int g = 0; g < NP; ++g)
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        // sliding sums can round below 0; a negative d with a tiny h would give w = inf (R29)
+        const float2 t = s2_mul(make_float2(fmaxf(D[g][k].x, 0.0f), fmaxf(D[g][k].y, 0.0f)), nc);
+        float2 w = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+        if (Q::single(g)) w.y = 0.0f;
+        const int ja = k + Q::oxa(g) + S;  // window index of column k + oxa
+        A[k] = s2_fma(w, make_float2(ia[ja], ia[Q::single(g) ? ja : ja + 1]), A[k]);
+        B[k] = s2_add(B[k], w);
+        Pn[ja] = s2_fma(w, make_float2(io[k], io[k]), Pn[ja]);  // .x -> column ja, .y -> ja + 1
+        Pd[ja] = s2_add(Pd[ja], w);
+      }
+    // partner window: column J collects Pn[J].x and Pn[J-1].y; columns outside [S, S+C) belong
+    // to the lanes 1..2 to the left / right
+    float on[NIW], od[NIW];
+#pragma unroll
+    for (int j = 0; j < NIW; ++j) {
+      on[j] = j > 0 ? Pn[j].x + Pn[j - 1].y : Pn[j].x;
+      od[j] = j > 0 ? Pd[j].x + Pd[j - 1].y : Pd[j].x;
+    }
+    float rn[C], rd[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      rn[k] = on[k + S];
+      rd[k] = od[k + S];
+    }
+#pragma unroll
+    for (int dl = 1; dl <= 2; ++dl)
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        // from lane - dl: its window index k + 4 dl + S
+        if (k + 4 * dl + S < NIW) {
+          rn[k] += __shfl_up_sync(0xffffffffu, on[k + 4 * dl + S], dl);
+          rd[k] += __shfl_up_sync(0xffffffffu, od[k + 4 * dl + S], dl);
+        }
+        // from lane + dl: its window index k - 4 dl + S
+        if (k - 4 * dl + S >= 0) {
+          rn[k] += __shfl_down_sync(0xffffffffu, on[k - 4 * dl + S], dl);
+          rd[k] += __shfl_down_sync(0xffffffffu, od[k - 4 * dl + S], dl);
+        }
+      }
+    // TMEM read-modify-write: own row y (with the partner row when oy = 0), partner row y + oy
+    const bool own_ok = y >= 0;
+    const bool par_ok = oy > 0 && y + oy < T;
+    float vo[8], vp[8];
+    tm_wait_st();
+    if (own_ok) tm_ld8(tm + 8 * y, vo);
+    if (par_ok) tm_ld8(tm + 8 * (y + oy), vp);
+    tm_wait_ld(vo, vp);
+    if (own_ok) {
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        float n = A[k].x + A[k].y, d = B[k].x + B[k].y;
+        if (oy == 0) {
+          n += rn[k];
+          d += rd[k];
+        }
+        vo[k] += n;
+        vo[4 + k] += d;
+      }
+      tm_st8(tm + 8 * y, vo);
+    }
+    if (par_ok) {
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        vp[k] += rn[k];
+        vp[4 + k] += rd[k];
+      }
+      tm_st8(tm + 8 * (y + oy), vp);
+    }
+  }
+}
+
+template <int P, int S>
+__global__ void __launch_bounds__(128, 2) nlm_sym(NlmParams p, int ntx, int nty, int use_async) {
+  using G = SymGeom<P, S>;
+  constexpr int C = G::C, SW = G::SW, SH = G::SH, T = G::T, TWO = G::TWO, TH = G::TH;
+  extern __shared__ __align__(128) float U[];
+  __shared__ uint32_t tm_base_sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  const int per_img = ntx * nty;
+  const int b = blockIdx.x / per_img;
+  const int rr = blockIdx.x - b * per_img;
+  const int X = (rr % ntx) * TWO;  // first output column
+  const int Y = (rr / ntx) * TH;   // first output row (local)
+  const int gY = p.dst.y0 + Y;
+  const int c0 = X - 2 * S - P, r0 = gY - S - P - 1;  // image column / global row of smem (0, 0)
+  // interior tiles (no boundary inside the tile) take the asynchronous copy
+  const bool async_tile = use_async && (c0 & 1) == 0 && c0 >= 0 && c0 + SW <= p.src.W && r0 >= 0 && r0 + G::SH0 <= p.src.Hg;
+
+  if (warp == 0) {
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&tm_base_sh);
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst), "n"(G::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (async_tile) {
+    // interior tile: 8-byte cp.async (LDGSTS.64) of every row, all in flight at once; rows past
+    // the band buffer are zero (read_B returns 0 there)
+    constexpr int HW = SW / 2;  // float2 per row
+#pragma unroll 4
+    for (int i = tid; i < HW * SH; i += G::NT) {
+      const int r = i / HW, c = i - r * HW;
+      const int lr = r0 + r - p.src.y0;
+      float2* dst = reinterpret_cast<float2*>(U + r * SW) + c;
+      if ((unsigned)lr < (unsigned)p.src.Hl) {
+        const float* src = reinterpret_cast<const float*>(p.src.base + (int64_t)b * p.src.bstride + (int64_t)lr * p.src.pitch) + c0 + 2 * c;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+      } else {
+        *dst = make_float2(0.0f, 0.0f);
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else {
+    // image tile, boundary applied at load time (8 loads in flight per thread)
+    constexpr int N = SW * SH, STEP = G::NT * 8;
+#pragma unroll 1
+    for (int i0 = 0; i0 < N; i0 += STEP) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * G::NT + tid;
+        const int r = i / SW, c = i - r * SW;
+        v[u] = i < N ? read_B(p.src, b, c0 + c, r0 + r) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * G::NT + tid;
+        if (i < N) U[i] = v[u];
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tm_base_sh + ((uint32_t)(32 * warp) << 16);
+  const int wrow0 = warp * T + S + P + 1;  // smem row of the warp's output row 0
+  const float* Ul = U + 4 * lane;
+
+  // centre pair: num = u(p), den = 1
+#pragma unroll 1
+  for (int y = 0; y < T; ++y) {
+    float io[C];
+    sym_ld_win<S + P, C>(Ul + (wrow0 + y) * SW, io);
+    float v[8] = {io[0], io[1], io[2], io[3], 1.0f, 1.0f, 1.0f, 1.0f};
+    tm_st8(tm + 8 * y, v);
+  }
+  const float2 nc = make_float2(-p.coef, -p.coef);
+  sym_pass<P, S, 1>(U, wrow0, lane, 0, tm, nc);
+#pragma unroll 1
+  for (int oy = 1; oy <= S; ++oy) sym_pass<P, S, -S>(U, wrow0, lane, oy, tm, nc);
+
+  tm_wait_st();
+  const int x0 = X - S + 4 * lane;
+#pragma unroll 1
+  for (int y = 0; y < T; ++y) {
+    float v[8], dummy[8];
+    tm_ld8(tm + 8 * y, v);
+    tm_wait_ld(v, dummy);
+    const int ly = Y + warp * T + y;
+    if (ly < p.dst.H) {
+      float* drow = dst_row(p.dst, b, ly);
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        const int x = x0 + k;
+        if (x >= X && x < X + TWO && x < p.src.W) drow[x] = __fdiv_rn(v[k], v[4 + k]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base_sh), "n"(G::TMEM_COLS));
+  }
+}
+
+template <int P, int S>
+inline cudaError_t launch_sym(const NlmParams& p, int batch, cudaStream_t s) {
+  using G = SymGeom<P, S>;
+  static_assert(G::smem_bytes <= 113 * 1024, "two CTAs per SM");
+  auto kern = nlm_sym<P, S>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::smem_bytes);
+  if (e != cudaSuccess) return e;
+  const int ntx = (p.src.W + G::TWO - 1) / G::TWO, nty = (p.dst.H + G::TH - 1) / G::TH;
+  const long long nblk = (long long)ntx * nty * batch;
+  if (nblk <= 0) return cudaSuccess;
+  if (nblk > 0x7fffffffLL) return cudaErrorInvalidValue;
+  // the asynchronous tile copy moves 8-byte pairs: base, pitch and image stride 8-byte aligned
+  const int use_async = ((uintptr_t)p.src.base % 8 == 0) && (p.src.pitch % 8 == 0) && (batch == 1 || p.src.bstride % 8 == 0);
+  kern<<<(unsigned)nblk, G::NT, G::smem_bytes, s>>>(p, ntx, nty, use_async);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace icl

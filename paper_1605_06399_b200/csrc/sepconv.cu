@@ -126,8 +126,16 @@ size_t sep_stream_smem_bytes(int nt, int R) {
   return (size_t)(NSR / RB) * blk + 64;
 }
 
+bool make_view_tmap(const SrcView& src, int batch, int box_w, int box_h, CUtensorMap* map);
+
 // The source of a sepconv call as a 3-D tensor map for the TMA variants (sepconv_stream.cuh).
 bool make_src_tmap(const SepParams& p, int batch, int box_w, int box_h, CUtensorMap* map) {
+  return make_view_tmap(p.src, batch, box_w, box_h, map);
+}
+
+// Any source view as a 3-D tensor map (x = W columns, y = the rows held locally, z = images),
+// box box_w x box_h x 1, zero fill out of bounds (also the NLM sym_tmem tiles, nlm_sym.cuh).
+bool make_view_tmap(const SrcView& src, int batch, int box_w, int box_h, CUtensorMap* map) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -138,13 +146,13 @@ bool make_src_tmap(const SepParams& p, int batch, int box_w, int box_h, CUtensor
     return reinterpret_cast<EncodeFn>(fn);
   }();
   if (!enc) return false;
-  const cuuint64_t rows = (cuuint64_t)p.src.Hl;
-  const cuuint64_t dims[3] = {(cuuint64_t)p.src.W, rows, (cuuint64_t)batch};
-  const cuuint64_t bstride = batch > 1 ? (cuuint64_t)p.src.bstride : (cuuint64_t)p.src.pitch * rows;
-  const cuuint64_t strides[2] = {(cuuint64_t)p.src.pitch, bstride};
+  const cuuint64_t rows = (cuuint64_t)src.Hl;
+  const cuuint64_t dims[3] = {(cuuint64_t)src.W, rows, (cuuint64_t)batch};
+  const cuuint64_t bstride = batch > 1 ? (cuuint64_t)src.bstride : (cuuint64_t)src.pitch * rows;
+  const cuuint64_t strides[2] = {(cuuint64_t)src.pitch, bstride};
   const cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<char*>(p.src.base), dims, strides, box, estr,
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<char*>(src.base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
