@@ -99,90 +99,81 @@ __device__ __forceinline__ void sym_ld_win(const float* base, float (&v)[N]) {
   for (int i = 0; i < N; ++i) v[i] = tmp[OFF - A + i];
 }
 
-template <int P, int S, int OXMIN>
+// The pairs of search row OY (1..S): S pairs (ox, ox+1) of row OY covering ox = -S..S-1, and one
+// mixed pair: (S, OY) with (OY, 0) -- the S offsets of search row 0 (0 < ox <= S) ride in the
+// last pair of the S passes, so no lane is idle and row 0 needs no walk of its own.
+template <int P, int S, int OY>
 struct SymPass {
-  static constexpr int NOX = S - OXMIN + 1;
-  static constexpr int NPAIR = (NOX + 1) / 2;
-  __host__ __device__ static constexpr int oxa(int g) { return OXMIN + 2 * g; }
-  __host__ __device__ static constexpr bool single(int g) { return OXMIN + 2 * g + 1 > S; }
-  __host__ __device__ static constexpr int oxb(int g) { return single(g) ? OXMIN + 2 * g : OXMIN + 2 * g + 1; }
+  static constexpr int NPAIR = S + 1;
+  __host__ __device__ static constexpr bool mixed(int g) { return g == S; }
+  __host__ __device__ static constexpr int oxa(int g) { return mixed(g) ? S : -S + 2 * g; }
 };
 
-// D[g][k] += H_{(oxa,oxb)}(column k, image row of crow), one pair of ox per float2 (the walk's
-// initial window)
-template <int P, int S, int OXMIN>
-__device__ __forceinline__ void sym_acc_H(float2 (&D)[SymPass<P, S, OXMIN>::NPAIR][4], const float* crow,
-                                          const float* srow) {
-  using G = SymGeom<P, S>;
-  using Q = SymPass<P, S, OXMIN>;
-  constexpr int C = G::C, NCW = G::NCW, NSW = G::NSW;
-  float cen[NCW], sh[NSW];
-  sym_ld_win<S, NCW>(crow, cen);
-  sym_ld_win<0, NSW>(srow, sh);
-#pragma unroll
-  for (int g = 0; g < Q::NPAIR; ++g) {
-    float2 df[NCW];
-#pragma unroll
-    for (int t = 0; t < NCW; ++t)
-      df[t] = s2_sub(make_float2(cen[t], cen[t]), make_float2(sh[t + Q::oxa(g) + S], sh[t + Q::oxb(g) + S]));
-    float2 a = s2_mul(df[0], df[0]);
-#pragma unroll
-    for (int t = 1; t <= 2 * P; ++t) a = s2_fma(df[t], df[t], a);
-    D[g][0] = s2_add(D[g][0], a);
-#pragma unroll
-    for (int k = 1; k < C; ++k) {
-      a = s2_fma(df[k + 2 * P], df[k + 2 * P], a);
-      a = s2_fma(make_float2(-df[k - 1].x, -df[k - 1].y), df[k - 1], a);
-      D[g][k] = s2_add(D[g][k], a);
-    }
-  }
+// the two lanes' differences u(q) - u(q+o) at window index t of the pair g
+template <int P, int S, int OY, int G_>
+__device__ __forceinline__ float2 sym_df(const float* c18, const float* s18, int t) {
+  using Q = SymPass<P, S, OY>;
+  if (Q::mixed(G_)) return s2_sub(make_float2(c18[t + S], c18[t + S]), make_float2(s18[t + 2 * S], c18[t + OY + S]));
+  return s2_sub(make_float2(c18[t + S], c18[t + S]), make_float2(s18[t + Q::oxa(G_) + S], s18[t + Q::oxa(G_) + S + 1]));
 }
 
-// One step of the vertical slide: D[g][k] += H(new row) - H(old row), the difference formed in
-// one FFMA2 chain per pair (sum of the new squares minus the old ones, then slid along k)
-template <int P, int S, int OXMIN>
-__device__ __forceinline__ void sym_slide_H(float2 (&D)[SymPass<P, S, OXMIN>::NPAIR][4], const float* crow_n,
-                                            const float* srow_n, const float* crow_o, const float* srow_o) {
-  using G = SymGeom<P, S>;
-  using Q = SymPass<P, S, OXMIN>;
-  constexpr int C = G::C, NCW = G::NCW, NSW = G::NSW;
-  float cn[NCW], sn[NSW], co[NCW], so[NSW];
-  sym_ld_win<S, NCW>(crow_n, cn);
-  sym_ld_win<0, NSW>(srow_n, sn);
-  sym_ld_win<S, NCW>(crow_o, co);
-  sym_ld_win<0, NSW>(srow_o, so);
+template <int P, int S, int OY, int G_>
+__device__ __forceinline__ void sym_df_all(const float* c18, const float* s18, float2 (&df)[4 + 2 * P]) {
 #pragma unroll
-  for (int g = 0; g < Q::NPAIR; ++g) {
-    float2 dn[NCW], dd[NCW];
-#pragma unroll
-    for (int t = 0; t < NCW; ++t) {
-      dn[t] = s2_sub(make_float2(cn[t], cn[t]), make_float2(sn[t + Q::oxa(g) + S], sn[t + Q::oxb(g) + S]));
-      dd[t] = s2_sub(make_float2(co[t], co[t]), make_float2(so[t + Q::oxa(g) + S], so[t + Q::oxb(g) + S]));
-    }
-    float2 a = s2_mul(dn[0], dn[0]);
-#pragma unroll
-    for (int t = 1; t <= 2 * P; ++t) a = s2_fma(dn[t], dn[t], a);
-#pragma unroll
-    for (int t = 0; t <= 2 * P; ++t) a = s2_fma(make_float2(-dd[t].x, -dd[t].y), dd[t], a);
-    D[g][0] = s2_add(D[g][0], a);
-#pragma unroll
-    for (int k = 1; k < C; ++k) {
-      a = s2_fma(dn[k + 2 * P], dn[k + 2 * P], a);
-      a = s2_fma(make_float2(-dn[k - 1].x, -dn[k - 1].y), dn[k - 1], a);
-      a = s2_fma(make_float2(-dd[k + 2 * P].x, -dd[k + 2 * P].y), dd[k + 2 * P], a);
-      a = s2_fma(dd[k - 1], dd[k - 1], a);
-      D[g][k] = s2_add(D[g][k], a);
-    }
-  }
+  for (int t = 0; t < 4 + 2 * P; ++t) df[t] = sym_df<P, S, OY, G_>(c18, s18, t);
 }
 
-// One search row oy of the warp's walk.  U: smem tile; wrow0: smem row of the warp's d-row 0;
-// lanebase: lane's column offset (4 * lane); tm: the thread's TMEM address (column 0).
-template <int P, int S, int OXMIN>
-__device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, int oy, uint32_t tm, float2 nc) {
+// D[g][k] += H_g(column k, image row r): the walk's initial window
+template <int P, int S, int OY, int G_ = 0>
+__device__ __forceinline__ void sym_acc_H_g(float2 (&D)[S + 1][4], const float* c18, const float* s18) {
+  constexpr int C = 4, NCW = C + 2 * P;
+  float2 df[NCW];
+  sym_df_all<P, S, OY, G_>(c18, s18, df);
+  float2 a = s2_mul(df[0], df[0]);
+#pragma unroll
+  for (int t = 1; t <= 2 * P; ++t) a = s2_fma(df[t], df[t], a);
+  D[G_][0] = s2_add(D[G_][0], a);
+#pragma unroll
+  for (int k = 1; k < C; ++k) {
+    a = s2_fma(df[k + 2 * P], df[k + 2 * P], a);
+    a = s2_fma(make_float2(-df[k - 1].x, -df[k - 1].y), df[k - 1], a);
+    D[G_][k] = s2_add(D[G_][k], a);
+  }
+  if constexpr (G_ < S) sym_acc_H_g<P, S, OY, G_ + 1>(D, c18, s18);
+}
+
+// D[g][k] += H_g(new row) - H_g(old row), the difference formed in one FFMA2 chain per pair
+template <int P, int S, int OY, int G_ = 0>
+__device__ __forceinline__ void sym_slide_H_g(float2 (&D)[S + 1][4], const float* cn, const float* sn,
+                                              const float* co, const float* so) {
+  constexpr int C = 4, NCW = C + 2 * P;
+  float2 dn[NCW], dd[NCW];
+  sym_df_all<P, S, OY, G_>(cn, sn, dn);
+  sym_df_all<P, S, OY, G_>(co, so, dd);
+  float2 a = s2_mul(dn[0], dn[0]);
+#pragma unroll
+  for (int t = 1; t <= 2 * P; ++t) a = s2_fma(dn[t], dn[t], a);
+#pragma unroll
+  for (int t = 0; t <= 2 * P; ++t) a = s2_fma(make_float2(-dd[t].x, -dd[t].y), dd[t], a);
+  D[G_][0] = s2_add(D[G_][0], a);
+#pragma unroll
+  for (int k = 1; k < C; ++k) {
+    a = s2_fma(dn[k + 2 * P], dn[k + 2 * P], a);
+    a = s2_fma(make_float2(-dn[k - 1].x, -dn[k - 1].y), dn[k - 1], a);
+    a = s2_fma(make_float2(-dd[k + 2 * P].x, -dd[k + 2 * P].y), dd[k + 2 * P], a);
+    a = s2_fma(dd[k - 1], dd[k - 1], a);
+    D[G_][k] = s2_add(D[G_][k], a);
+  }
+  if constexpr (G_ < S) sym_slide_H_g<P, S, OY, G_ + 1>(D, cn, sn, co, so);
+}
+
+// One search row OY of the warp's walk (with the mixed pair's row-0 offset).  U: smem tile;
+// wrow0: smem row of the warp's d-row 0; tm: the thread's TMEM address (column 0).
+template <int P, int S, int OY>
+__device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, uint32_t tm, float2 nc) {
   using G = SymGeom<P, S>;
-  using Q = SymPass<P, S, OXMIN>;
-  constexpr int C = G::C, SW = G::SW, T = G::T, NIW = G::NIW, NP = Q::NPAIR;
+  using Q = SymPass<P, S, OY>;
+  constexpr int C = G::C, SW = G::SW, T = G::T, NIW = G::NIW, NSW = G::NSW, NP = Q::NPAIR;
   const float* Ul = U + 4 * lane;
   auto row = [&](int y) { return Ul + (wrow0 + y) * SW; };
 
@@ -191,21 +182,36 @@ __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, in
   for (int g = 0; g < NP; ++g)
 #pragma unroll
     for (int k = 0; k < C; ++k) D[g][k] = make_float2(0.0f, 0.0f);
-  const int y0 = -oy;
+  constexpr int y0 = -OY;
   // d(y0) + H(y0-P-1): the first step subtracts that row again
 #pragma unroll 1
-  for (int r = y0 - P - 1; r <= y0 + P - 1; ++r) sym_acc_H<P, S, OXMIN>(D, row(r), row(r + oy));
+  for (int r = y0 - P - 1; r <= y0 + P - 1; ++r) {
+    float c18[NSW], s18[NSW];
+    sym_ld_win<0, NSW>(row(r), c18);
+    sym_ld_win<0, NSW>(row(r + OY), s18);
+    sym_acc_H_g<P, S, OY>(D, c18, s18);
+  }
 
 #pragma unroll 1
   for (int y = y0; y < T; ++y) {
-    sym_slide_H<P, S, OXMIN>(D, row(y + P), row(y + P + oy), row(y - P - 1), row(y - P - 1 + oy));
-
-    float ia[NIW], io[C];
-    sym_ld_win<P, NIW>(row(y + oy), ia);   // u(q + o), q + o - (X - S + 4 lane) in [-S, C + S)
-    sym_ld_win<S + P, C>(row(y), io);      // u(q)
+    {
+      float cn[NSW], sn[NSW], co[NSW], so[NSW];
+      sym_ld_win<0, NSW>(row(y + P), cn);
+      sym_ld_win<0, NSW>(row(y + P + OY), sn);
+      sym_ld_win<0, NSW>(row(y - P - 1), co);
+      sym_ld_win<0, NSW>(row(y - P - 1 + OY), so);
+      sym_slide_H_g<P, S, OY>(D, cn, sn, co, so);
+    }
+    float ia[NIW], iy[NIW];
+    sym_ld_win<P, NIW>(row(y + OY), ia);  // u(q + o): window index m + S, m = column - (X - S + 4 lane)
+    sym_ld_win<P, NIW>(row(y), iy);       // row y: u(q) = iy[k + S], and u(q + (OY, 0))
     float2 A[C], B[C], Pn[NIW], Pd[NIW];
+    float Zn[C], Zd[C];  // the mixed pair's row-0 partner contributions, by source column
 #pragma unroll
-    for (int k = 0; k < C; ++k) A[k] = B[k] = make_float2(0.0f, 0.0f);
+    for (int k = 0; k < C; ++k) {
+      A[k] = B[k] = make_float2(0.0f, 0.0f);
+      Zn[k] = Zd[k] = 0.0f;
+    }
 #pragma unroll
     for (int j = 0; j < NIW; ++j) Pn[j] = Pd[j] = make_float2(0.0f, 0.0f);
 #pragma unroll
@@ -214,27 +220,37 @@ __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, in
       for (int k = 0; k < C; ++k) {
         // sliding sums can round below 0; a negative d with a tiny h would give w = inf (R29)
         const float2 t = s2_mul(make_float2(fmaxf(D[g][k].x, 0.0f), fmaxf(D[g][k].y, 0.0f)), nc);
-        float2 w = make_float2(ex2_approx(t.x), ex2_approx(t.y));
-        if (Q::single(g)) w.y = 0.0f;
-        const int ja = k + Q::oxa(g) + S;  // window index of column k + oxa
-        A[k] = s2_fma(w, make_float2(ia[ja], ia[Q::single(g) ? ja : ja + 1]), A[k]);
+        const float2 w = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+        const float uq = iy[k + S];
         B[k] = s2_add(B[k], w);
-        Pn[ja] = s2_fma(w, make_float2(io[k], io[k]), Pn[ja]);  // .x -> column ja, .y -> ja + 1
-        Pd[ja] = s2_add(Pd[ja], w);
+        if (Q::mixed(g)) {
+          A[k] = s2_fma(w, make_float2(ia[k + 2 * S], iy[k + OY + S]), A[k]);
+          Pn[k + 2 * S].x = fmaf(w.x, uq, Pn[k + 2 * S].x);  // partner (q + (S, OY)): row y + OY
+          Pd[k + 2 * S].x += w.x;
+          Zn[k] = fmaf(w.y, uq, Zn[k]);  // partner (q + (OY, 0)): row y
+          Zd[k] += w.y;
+        } else {
+          const int ja = k + Q::oxa(g) + S;  // window index of column k + oxa
+          A[k] = s2_fma(w, make_float2(ia[ja], ia[ja + 1]), A[k]);
+          Pn[ja] = s2_fma(w, make_float2(uq, uq), Pn[ja]);  // .x -> column ja, .y -> ja + 1
+          Pd[ja] = s2_add(Pd[ja], w);
+        }
       }
-    // partner window: column J collects Pn[J].x and Pn[J-1].y; columns outside [S, S+C) belong
-    // to the lanes 1..2 to the left / right
+    // partner window of row y + OY: column J collects Pn[J].x and Pn[J-1].y; columns outside
+    // [S, S+C) belong to the lanes 1..2 to the left / right
     float on[NIW], od[NIW];
 #pragma unroll
     for (int j = 0; j < NIW; ++j) {
       on[j] = j > 0 ? Pn[j].x + Pn[j - 1].y : Pn[j].x;
       od[j] = j > 0 ? Pd[j].x + Pd[j - 1].y : Pd[j].x;
     }
-    float rn[C], rd[C];
+    float rn[C], rd[C], zn[C], zd[C];
 #pragma unroll
     for (int k = 0; k < C; ++k) {
       rn[k] = on[k + S];
       rd[k] = od[k + S];
+      zn[k] = k >= OY ? Zn[k - OY] : 0.0f;
+      zd[k] = k >= OY ? Zd[k - OY] : 0.0f;
     }
 #pragma unroll
     for (int dl = 1; dl <= 2; ++dl)
@@ -250,25 +266,25 @@ __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, in
           rn[k] += __shfl_down_sync(0xffffffffu, on[k - 4 * dl + S], dl);
           rd[k] += __shfl_down_sync(0xffffffffu, od[k - 4 * dl + S], dl);
         }
+        // row-0 partner: source column k + 4 dl - OY of lane - dl
+        if (k + 4 * dl - OY >= 0 && k + 4 * dl - OY < C) {
+          zn[k] += __shfl_up_sync(0xffffffffu, Zn[k + 4 * dl - OY], dl);
+          zd[k] += __shfl_up_sync(0xffffffffu, Zd[k + 4 * dl - OY], dl);
+        }
       }
-    // TMEM read-modify-write: own row y (with the partner row when oy = 0), partner row y + oy
+    // TMEM read-modify-write: own row y (own pairs + the row-0 partners), partner row y + OY
     const bool own_ok = y >= 0;
-    const bool par_ok = oy > 0 && y + oy < T;
+    const bool par_ok = y + OY < T;
     float vo[8], vp[8];
     tm_wait_st();
     if (own_ok) tm_ld8(tm + 8 * y, vo);
-    if (par_ok) tm_ld8(tm + 8 * (y + oy), vp);
+    if (par_ok) tm_ld8(tm + 8 * (y + OY), vp);
     tm_wait_ld(vo, vp);
     if (own_ok) {
 #pragma unroll
       for (int k = 0; k < C; ++k) {
-        float n = A[k].x + A[k].y, d = B[k].x + B[k].y;
-        if (oy == 0) {
-          n += rn[k];
-          d += rd[k];
-        }
-        vo[k] += n;
-        vo[4 + k] += d;
+        vo[k] += (A[k].x + A[k].y) + zn[k];
+        vo[4 + k] += (B[k].x + B[k].y) + zd[k];
       }
       tm_st8(tm + 8 * y, vo);
     }
@@ -278,9 +294,15 @@ __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, in
         vp[k] += rn[k];
         vp[4 + k] += rd[k];
       }
-      tm_st8(tm + 8 * (y + oy), vp);
+      tm_st8(tm + 8 * (y + OY), vp);
     }
   }
+}
+
+template <int P, int S, int OY = 1>
+__device__ __forceinline__ void sym_passes(const float* U, int wrow0, int lane, uint32_t tm, float2 nc) {
+  sym_pass<P, S, OY>(U, wrow0, lane, tm, nc);
+  if constexpr (OY < S) sym_passes<P, S, OY + 1>(U, wrow0, lane, tm, nc);
 }
 
 template <int P, int S>
@@ -358,9 +380,7 @@ __global__ void __launch_bounds__(128, 2) nlm_sym(NlmParams p, int ntx, int nty,
     tm_st8(tm + 8 * y, v);
   }
   const float2 nc = make_float2(-p.coef, -p.coef);
-  sym_pass<P, S, 1>(U, wrow0, lane, 0, tm, nc);
-#pragma unroll 1
-  for (int oy = 1; oy <= S; ++oy) sym_pass<P, S, -S>(U, wrow0, lane, oy, tm, nc);
+  sym_passes<P, S>(U, wrow0, lane, tm, nc);
 
   tm_wait_st();
   const int x0 = X - S + 4 * lane;
