@@ -109,6 +109,14 @@ struct SymPass {
   __host__ __device__ static constexpr int oxa(int g) { return mixed(g) ? S : -S + 2 * g; }
 };
 
+// true when the normal pair g, column k is the first (in the unrolled g-major order) to write the
+// partner window entry k + 2g: that write assigns instead of accumulating into 0
+__host__ __device__ constexpr bool sym_first_pn(int g, int k) {
+  for (int gg = 0; gg < g; ++gg)
+    if (k + 2 * g - 2 * gg >= 0 && k + 2 * g - 2 * gg < 4) return false;
+  return true;
+}
+
 // the two lanes' differences u(q) - u(q+o) at window index t of the pair g
 template <int P, int S, int OY, int G_>
 __device__ __forceinline__ float2 sym_df(const float* c18, const float* s18, int t) {
@@ -222,18 +230,30 @@ __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, ui
         const float2 t = s2_mul(make_float2(fmaxf(D[g][k].x, 0.0f), fmaxf(D[g][k].y, 0.0f)), nc);
         const float2 w = make_float2(ex2_approx(t.x), ex2_approx(t.y));
         const float uq = iy[k + S];
-        B[k] = s2_add(B[k], w);
+        const bool first = g == 0;  // first write of A[k], B[k] (resolved at compile time)
+        B[k] = first ? w : s2_add(B[k], w);
         if (Q::mixed(g)) {
           A[k] = s2_fma(w, make_float2(ia[k + 2 * S], iy[k + OY + S]), A[k]);
-          Pn[k + 2 * S].x = fmaf(w.x, uq, Pn[k + 2 * S].x);  // partner (q + (S, OY)): row y + OY
-          Pd[k + 2 * S].x += w.x;
-          Zn[k] = fmaf(w.y, uq, Zn[k]);  // partner (q + (OY, 0)): row y
-          Zd[k] += w.y;
+          if (k < 2) {  // entries 2S, 2S + 1 were written by the last normal pair
+            Pn[k + 2 * S].x = fmaf(w.x, uq, Pn[k + 2 * S].x);  // partner (q + (S, OY)): row y + OY
+            Pd[k + 2 * S].x += w.x;
+          } else {
+            Pn[k + 2 * S].x = w.x * uq;
+            Pd[k + 2 * S].x = w.x;
+          }
+          Zn[k] = w.y * uq;  // partner (q + (OY, 0)): row y
+          Zd[k] = w.y;
         } else {
           const int ja = k + Q::oxa(g) + S;  // window index of column k + oxa
-          A[k] = s2_fma(w, make_float2(ia[ja], ia[ja + 1]), A[k]);
-          Pn[ja] = s2_fma(w, make_float2(uq, uq), Pn[ja]);  // .x -> column ja, .y -> ja + 1
-          Pd[ja] = s2_add(Pd[ja], w);
+          const float2 qa = make_float2(ia[ja], ia[ja + 1]);
+          A[k] = first ? s2_mul(w, qa) : s2_fma(w, qa, A[k]);
+          if (sym_first_pn(g, k)) {
+            Pn[ja] = s2_mul(w, make_float2(uq, uq));  // .x -> column ja, .y -> ja + 1
+            Pd[ja] = w;
+          } else {
+            Pn[ja] = s2_fma(w, make_float2(uq, uq), Pn[ja]);
+            Pd[ja] = s2_add(Pd[ja], w);
+          }
         }
       }
     // partner window of row y + OY: column J collects Pn[J].x and Pn[J-1].y; columns outside
