@@ -150,29 +150,57 @@ __device__ __forceinline__ void sym_acc_H_g(float2 (&D)[S + 1][4], const float* 
   if constexpr (G_ < S) sym_acc_H_g<P, S, OY, G_ + 1>(D, c18, s18);
 }
 
-// D[g][k] += H_g(new row) - H_g(old row), the difference formed in one FFMA2 chain per pair
+// D[g][k] += H_g(new row) - H_g(old row).  Per window index t the two squares enter as one
+// product: dn^2 - dd^2 = (dn - dd)(dn + dd), and with dn = cn - sn, dd = co - so
+//   dn - dd = (cn - co) - (sn - so),   dn + dd = (cn + co) - (sn + so),
+// whose four row sums / differences are shared by every pair of the row (formed once per step):
+// per pair and t two FADD2 and one FFMA2 link of the sliding chain instead of two FADD2 and two
+// FFMA2 links.
 template <int P, int S, int OY, int G_ = 0>
-__device__ __forceinline__ void sym_slide_H_g(float2 (&D)[S + 1][4], const float* cn, const float* sn,
-                                              const float* co, const float* so) {
+__device__ __forceinline__ void sym_slide_pq(float2 (&D)[S + 1][4], const float* Cd, const float* Cs,
+                                             const float* Sd, const float* Ss) {
+  using Q = SymPass<P, S, OY>;
   constexpr int C = 4, NCW = C + 2 * P;
-  float2 dn[NCW], dd[NCW];
-  sym_df_all<P, S, OY, G_>(cn, sn, dn);
-  sym_df_all<P, S, OY, G_>(co, so, dd);
-  float2 a = s2_mul(dn[0], dn[0]);
+  float2 pp[NCW], qq[NCW];
 #pragma unroll
-  for (int t = 1; t <= 2 * P; ++t) a = s2_fma(dn[t], dn[t], a);
+  for (int t = 0; t < NCW; ++t) {
+    if (Q::mixed(G_)) {
+      pp[t] = s2_sub(make_float2(Cd[t + S], Cd[t + S]), make_float2(Sd[t + 2 * S], Cd[t + OY + S]));
+      qq[t] = s2_sub(make_float2(Cs[t + S], Cs[t + S]), make_float2(Ss[t + 2 * S], Cs[t + OY + S]));
+    } else {
+      const int j = t + Q::oxa(G_) + S;
+      pp[t] = s2_sub(make_float2(Cd[t + S], Cd[t + S]), make_float2(Sd[j], Sd[j + 1]));
+      qq[t] = s2_sub(make_float2(Cs[t + S], Cs[t + S]), make_float2(Ss[j], Ss[j + 1]));
+    }
+  }
+  float2 a = s2_mul(pp[0], qq[0]);
 #pragma unroll
-  for (int t = 0; t <= 2 * P; ++t) a = s2_fma(make_float2(-dd[t].x, -dd[t].y), dd[t], a);
+  for (int t = 1; t <= 2 * P; ++t) a = s2_fma(pp[t], qq[t], a);
   D[G_][0] = s2_add(D[G_][0], a);
 #pragma unroll
   for (int k = 1; k < C; ++k) {
-    a = s2_fma(dn[k + 2 * P], dn[k + 2 * P], a);
-    a = s2_fma(make_float2(-dn[k - 1].x, -dn[k - 1].y), dn[k - 1], a);
-    a = s2_fma(make_float2(-dd[k + 2 * P].x, -dd[k + 2 * P].y), dd[k + 2 * P], a);
-    a = s2_fma(dd[k - 1], dd[k - 1], a);
+    a = s2_fma(pp[k + 2 * P], qq[k + 2 * P], a);
+    a = s2_fma(make_float2(-pp[k - 1].x, -pp[k - 1].y), qq[k - 1], a);
     D[G_][k] = s2_add(D[G_][k], a);
   }
-  if constexpr (G_ < S) sym_slide_H_g<P, S, OY, G_ + 1>(D, cn, sn, co, so);
+  if constexpr (G_ < S) sym_slide_pq<P, S, OY, G_ + 1>(D, Cd, Cs, Sd, Ss);
+}
+
+template <int P, int S, int OY>
+__device__ __forceinline__ void sym_slide_H(float2 (&D)[S + 1][4], const float* cn, const float* sn,
+                                            const float* co, const float* so) {
+  constexpr int NSW = 4 + 2 * P + 2 * S;
+  static_assert(NSW % 2 == 0, "window in float2 pairs");
+  float Cd[NSW], Cs[NSW], Sd[NSW], Ss[NSW];
+#pragma unroll
+  for (int j = 0; j < NSW; j += 2) {
+    const float2 a = make_float2(cn[j], cn[j + 1]), b = make_float2(co[j], co[j + 1]);
+    const float2 c = make_float2(sn[j], sn[j + 1]), d = make_float2(so[j], so[j + 1]);
+    const float2 cd = s2_sub(a, b), cs = s2_add(a, b), sd = s2_sub(c, d), ss = s2_add(c, d);
+    Cd[j] = cd.x; Cd[j + 1] = cd.y; Cs[j] = cs.x; Cs[j + 1] = cs.y;
+    Sd[j] = sd.x; Sd[j + 1] = sd.y; Ss[j] = ss.x; Ss[j + 1] = ss.y;
+  }
+  sym_slide_pq<P, S, OY>(D, Cd, Cs, Sd, Ss);
 }
 
 // One search row OY of the warp's walk (with the mixed pair's row-0 offset).  U: smem tile;
@@ -208,7 +236,7 @@ __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, ui
       sym_ld_win<0, NSW>(row(y + P + OY), sn);
       sym_ld_win<0, NSW>(row(y - P - 1), co);
       sym_ld_win<0, NSW>(row(y - P - 1 + OY), so);
-      sym_slide_H_g<P, S, OY>(D, cn, sn, co, so);
+      sym_slide_H<P, S, OY>(D, cn, sn, co, so);
     }
     float ia[NIW], iy[NIW];
     sym_ld_win<P, NIW>(row(y + OY), ia);  // u(q + o): window index m + S, m = column - (X - S + 4 lane)
