@@ -455,8 +455,12 @@ static int default_variant(const Prepared& pc) {
   switch (pc.f) {
     case ICL_FILTER_SEPCONV:
       if (!pc.a16) return variant_id(pc.f, pc.pixels < (1 << 20) ? "stream_nt64_s16_v1" : "stream_nt64_s64_v1");
-      // latency-bound small images (BASELINE configs[0], 512^2): the persistent tile kernel's single
-      // pass wins (6.8 vs 9.2 us per call, graph-replayed; tools/small_sweep.py)
+      // latency-bound small images (BASELINE configs[0], 512^2, r <= 3): one of the paper's Table-1
+      // configurations -- 32x8 work-groups, one pixel per thread, the block + halo in local memory --
+      // has the shortest critical path (5.8 vs 8.7 us per call for tile64p, graph-replayed;
+      // tools/small_sweep.py, round 2c); up to 2^19 pixels the persistent tile kernel's single pass
+      if (pc.pixels <= (1 << 18) && (pc.sep.rx > pc.sep.ry ? pc.sep.rx : pc.sep.ry) <= 3)
+        return variant_id(pc.f, "pm_w32x8_c1x1_blk_l1_u4");
       if (pc.pixels <= (1 << 19)) return variant_id(pc.f, "tile64p_v4");
       if (pc.pixels < (1 << 20)) return variant_id(pc.f, "stream_nt32_s8_v4");
       {
