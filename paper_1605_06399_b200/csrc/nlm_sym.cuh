@@ -79,7 +79,10 @@ struct SymGeom {
   static constexpr int NSW = C + 2 * P + 2 * S;  // shifted window (H, every ox)
   static constexpr int NIW = C + 2 * S;       // accumulation window u(q + o), and the partner window
   static constexpr int TMEM_COLS = 8 * T;     // num[4] den[4] per row
-  static constexpr size_t smem_bytes = (size_t)SW * SH * sizeof(float);
+  // at least 77 KB: never three CTAs on an SM (two CTAs x 256 columns fill the 512 TMEM columns; a
+  // third would spin in tcgen05.alloc until one of them finishes)
+  static constexpr size_t tile_bytes = (size_t)SW * SH * sizeof(float);
+  static constexpr size_t smem_bytes = tile_bytes > 77 * 1024 ? tile_bytes : 77 * 1024;
   static_assert(S >= 1 && S <= 8, "partner exchange reaches two lanes");
   static_assert(TMEM_COLS == 256, "two CTAs per SM share the 512 TMEM columns");
 };
