@@ -189,6 +189,9 @@ static const Variant kHarVariants[] = {
     {"shfl_nw2_s128", K_SHFL, 2, 4, 128},         {"shfl_nw2_s16", K_SHFL, 2, 4, 16},
     {"shfl_nw2_s8", K_SHFL, 2, 4, 8},             {"shfl_nw4_s16", K_SHFL, 4, 4, 16},
     {"shfl_nw4_s8", K_SHFL, 4, 4, 8},
+    // one-warp CTAs (120-column strips): more CTAs for images that do not fill the GPU
+    {"shfl_nw1_s16", K_SHFL, 1, 4, 16},           {"shfl_nw1_s32", K_SHFL, 1, 4, 32},
+    {"shfl_nw1_s8", K_SHFL, 1, 4, 8},
     // separable window sums on the products (re-associated: tolerance vs naive, R16)
     {"slide_nw2_s32", K_SLIDE, 2, 4, 32},         {"slide_nw2_s16", K_SLIDE, 2, 4, 16},
     {"slide_nw2_s64", K_SLIDE, 2, 4, 64},         {"slide_nw2_s8", K_SLIDE, 2, 4, 8},

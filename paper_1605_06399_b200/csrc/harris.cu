@@ -96,11 +96,13 @@ extern template cudaError_t dispatch_hs<128, 4>(const HarrisParams&, int, int, c
 extern template cudaError_t dispatch_hs<64, 1>(const HarrisParams&, int, int, cudaStream_t);
 template <int NW>
 cudaError_t dispatch_hshfl(const HarrisParams& p, int batch, int S, cudaStream_t s);
+extern template cudaError_t dispatch_hshfl<1>(const HarrisParams&, int, int, cudaStream_t);
 extern template cudaError_t dispatch_hshfl<2>(const HarrisParams&, int, int, cudaStream_t);
 extern template cudaError_t dispatch_hshfl<4>(const HarrisParams&, int, int, cudaStream_t);
 
 cudaError_t launch_harris_shfl(const HarrisCall& c, int nw, int S, cudaStream_t s) {
   HarrisParams p = make_params(c);
+  if (nw == 1) return dispatch_hshfl<1>(p, c.batch, S, s);
   if (nw == 2) return dispatch_hshfl<2>(p, c.batch, S, s);
   if (nw == 4) return dispatch_hshfl<4>(p, c.batch, S, s);
   return cudaErrorInvalidValue;

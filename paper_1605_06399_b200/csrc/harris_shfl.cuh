@@ -290,17 +290,34 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
   const float* gsrc = src_row(p.src, b, g0 - A - 1) + (EDGE && nb == 0 ? 0 : xs);
   float* sdst = smem + 4 * tid;
 
+  // a one-warp CTA (NW = 1) has more 16-byte slots per row than threads: lanes 0..NSLOT-NT-1 also
+  // load a second slot
+  constexpr bool TWO_SLOTS = NSLOT > NT;
+  static_assert(NSLOT <= 2 * NT, "at most two loader slots per thread");
+  const int tid2 = tid + NT;
+  const bool loader2 = TWO_SLOTS && tid2 < NSLOT;
+  const int xs2 = x0 - HP + 4 * tid2;
+  const int nb2 = !EDGE ? 16 : (xs2 < 0 ? 0 : min(max(W - xs2, 0), 4) * 4);
+  const float* gsrc2 = src_row(p.src, b, g0 - A - 1) + (EDGE && nb2 == 0 ? 0 : xs2);
+  float* sdst2 = smem + 4 * tid2;
+
   auto load_block = [&](int m) {
     if (!loader) return;
     const float* g = gsrc + (int64_t)(m * RB) * spitch;
+    const float* g2 = gsrc2 + (int64_t)(m * RB) * spitch;
     const int r0 = (m % NBLKS) * RB;
 #pragma unroll
     for (int u = 0; u < RB; ++u) {
       if (m * RB + u < NL) {
         cp_async16(sdst + (r0 + u) * ROWLEN, g, nb);
         if (u < 2 && r0 == 0) cp_async16(sdst + (NSR + u) * ROWLEN, g, nb);  // mirror
+        if (TWO_SLOTS && loader2) {
+          cp_async16(sdst2 + (r0 + u) * ROWLEN, g2, nb2);
+          if (u < 2 && r0 == 0) cp_async16(sdst2 + (NSR + u) * ROWLEN, g2, nb2);
+        }
       }
       g += spitch;
+      g2 += spitch;
     }
   };
   // EDGE: input boundary of the halo columns outside [0, W) of load block m (and of its mirror rows)
