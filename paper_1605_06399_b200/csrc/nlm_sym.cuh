@@ -63,6 +63,10 @@ __device__ __forceinline__ void tm_st8(uint32_t taddr, const float (&v)[8]) {
                : "memory");
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// keep values of an earlier tcgen05.ld behind the (preceding, volatile) wait::ld
+__device__ __forceinline__ void tm_pin8(float (&v)[8]) {
+  asm volatile("" : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]));
+}
 
 template <int P, int S>
 struct SymGeom {
@@ -153,6 +157,28 @@ __device__ __forceinline__ void sym_acc_H_g(float2 (&D)[S + 1][4], const float* 
   if constexpr (G_ < S) sym_acc_H_g<P, S, OY, G_ + 1>(D, c18, s18);
 }
 
+// H_g(column k) of every pair at one image row (squares chains, two distinct register pairs per
+// FFMA2), into Hr[g][2k], Hr[g][2k+1] -- the layout of the TMEM ring (8 words per pair)
+template <int P, int S, int OY, int G_ = 0>
+__device__ __forceinline__ void sym_H_all(float (&Hr)[S + 1][8], const float* c18, const float* s18) {
+  constexpr int C = 4, NCW = C + 2 * P;
+  float2 df[NCW];
+  sym_df_all<P, S, OY, G_>(c18, s18, df);
+  float2 a = s2_mul(df[0], df[0]);
+#pragma unroll
+  for (int t = 1; t <= 2 * P; ++t) a = s2_fma(df[t], df[t], a);
+  Hr[G_][0] = a.x;
+  Hr[G_][1] = a.y;
+#pragma unroll
+  for (int k = 1; k < C; ++k) {
+    a = s2_fma(df[k + 2 * P], df[k + 2 * P], a);
+    a = s2_fma(make_float2(-df[k - 1].x, -df[k - 1].y), df[k - 1], a);
+    Hr[G_][2 * k] = a.x;
+    Hr[G_][2 * k + 1] = a.y;
+  }
+  if constexpr (G_ < S) sym_H_all<P, S, OY, G_ + 1>(Hr, c18, s18);
+}
+
 // D[g][k] += H_g(new row) - H_g(old row).  Per window index t the two squares enter as one
 // product: dn^2 - dd^2 = (dn - dd)(dn + dd), and with dn = cn - sn, dd = co - so
 //   dn - dd = (cn - co) - (sn - so),   dn + dd = (cn + co) - (sn + so),
@@ -208,7 +234,7 @@ __device__ __forceinline__ void sym_slide_H(float2 (&D)[S + 1][4], const float* 
 
 // One search row OY of the warp's walk (with the mixed pair's row-0 offset).  U: smem tile;
 // wrow0: smem row of the warp's d-row 0; tm: the thread's TMEM address (column 0).
-template <int P, int S, int OY>
+template <int P, int S, int OY, bool RING>
 __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, uint32_t tm, float2 nc) {
   using G = SymGeom<P, S>;
   using Q = SymPass<P, S, OY>;
@@ -223,17 +249,59 @@ __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, ui
     for (int k = 0; k < C; ++k) D[g][k] = make_float2(0.0f, 0.0f);
   constexpr int y0 = -OY;
   // d(y0) + H(y0-P-1): the first step subtracts that row again
+  // RING: H of the last 2P+1 rows kept in tensor memory (columns 8T.., slot r mod (2P+1), 8 words
+  // per pair), so a step computes only the row entering the window
+  constexpr int NSLOT = 2 * P + 1;
+  const uint32_t ring = tm + 8 * T;
 #pragma unroll 1
   for (int r = y0 - P - 1; r <= y0 + P - 1; ++r) {
     float c18[NSW], s18[NSW];
     sym_ld_win<0, NSW>(row(r), c18);
     sym_ld_win<0, NSW>(row(r + OY), s18);
-    sym_acc_H_g<P, S, OY>(D, c18, s18);
+    if constexpr (RING) {
+      float Hr[NP][8];
+      sym_H_all<P, S, OY>(Hr, c18, s18);
+      const int slot = (r + 64 * NSLOT) % NSLOT;
+#pragma unroll
+      for (int g = 0; g < NP; ++g) {
+#pragma unroll
+        for (int k = 0; k < C; ++k) D[g][k] = s2_add(D[g][k], make_float2(Hr[g][2 * k], Hr[g][2 * k + 1]));
+        tm_st8(ring + 8 * (slot * NP + g), Hr[g]);
+      }
+    } else {
+      sym_acc_H_g<P, S, OY>(D, c18, s18);
+    }
   }
+  int slot = (y0 + P + 64 * NSLOT) % NSLOT;  // slot of row y + P == slot of row y - P - 1
 
 #pragma unroll 1
   for (int y = y0; y < T; ++y) {
-    {
+    if constexpr (RING) {
+      float Ho[NP][8], Hn[NP][8];
+      const uint32_t sa = ring + 8 * (slot * NP);
+      tm_wait_st();  // the previous step's stores (this slot was written 2P+1 steps ago)
+#pragma unroll
+      for (int g = 0; g < NP; ++g) tm_ld8(sa + 8 * g, Ho[g]);
+      float cn[NSW], sn[NSW];
+      sym_ld_win<0, NSW>(row(y + P), cn);
+      sym_ld_win<0, NSW>(row(y + P + OY), sn);
+      sym_H_all<P, S, OY>(Hn, cn, sn);
+      {
+        float dummy[8];
+        tm_wait_ld(Ho[0], dummy);
+      }
+#pragma unroll
+      for (int g = 1; g < NP; ++g) tm_pin8(Ho[g]);
+#pragma unroll
+      for (int g = 0; g < NP; ++g) {
+#pragma unroll
+        for (int k = 0; k < C; ++k)
+          D[g][k] = s2_add(D[g][k], s2_sub(make_float2(Hn[g][2 * k], Hn[g][2 * k + 1]),
+                                           make_float2(Ho[g][2 * k], Ho[g][2 * k + 1])));
+        tm_st8(sa + 8 * g, Hn[g]);
+      }
+      slot = slot + 1 == NSLOT ? 0 : slot + 1;
+    } else {
       float cn[NSW], sn[NSW], co[NSW], so[NSW];
       sym_ld_win<0, NSW>(row(y + P), cn);
       sym_ld_win<0, NSW>(row(y + P + OY), sn);
@@ -350,15 +418,19 @@ __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, ui
   }
 }
 
-template <int P, int S, int OY = 1>
+template <int P, int S, bool RING, int OY = 1>
 __device__ __forceinline__ void sym_passes(const float* U, int wrow0, int lane, uint32_t tm, float2 nc) {
-  sym_pass<P, S, OY>(U, wrow0, lane, tm, nc);
-  if constexpr (OY < S) sym_passes<P, S, OY + 1>(U, wrow0, lane, tm, nc);
+  sym_pass<P, S, OY, RING>(U, wrow0, lane, tm, nc);
+  if constexpr (OY < S) sym_passes<P, S, RING, OY + 1>(U, wrow0, lane, tm, nc);
 }
 
-template <int P, int S>
-__global__ void __launch_bounds__(128, 2) nlm_sym(NlmParams p, int ntx, int nty, int use_async) {
+// RING = false: 2 CTAs/SM, 256 TMEM columns each (num/den), the slide recomputes the leaving row.
+// RING = true ("sym_ring"): 1 CTA/SM with all 512 columns: num/den + the H ring of the last 2P+1 rows.
+template <int P, int S, bool RING>
+__global__ void __launch_bounds__(128, RING ? 1 : 2) nlm_sym(NlmParams p, int ntx, int nty, int use_async) {
   using G = SymGeom<P, S>;
+  constexpr int TMEM_COLS = RING ? 512 : G::TMEM_COLS;
+  static_assert(!RING || G::TMEM_COLS + 8 * (2 * P + 1) * (S + 1) <= 512, "ring fits the tensor memory");
   constexpr int C = G::C, SW = G::SW, SH = G::SH, T = G::T, TWO = G::TWO, TH = G::TH;
   extern __shared__ __align__(128) float U[];
   __shared__ uint32_t tm_base_sh;
@@ -376,7 +448,7 @@ __global__ void __launch_bounds__(128, 2) nlm_sym(NlmParams p, int ntx, int nty,
 
   if (warp == 0) {
     const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&tm_base_sh);
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst), "n"(G::TMEM_COLS));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst), "n"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (async_tile) {
@@ -431,7 +503,7 @@ __global__ void __launch_bounds__(128, 2) nlm_sym(NlmParams p, int ntx, int nty,
     tm_st8(tm + 8 * y, v);
   }
   const float2 nc = make_float2(-p.coef, -p.coef);
-  sym_passes<P, S>(U, wrow0, lane, tm, nc);
+  sym_passes<P, S, RING>(U, wrow0, lane, tm, nc);
 
   tm_wait_st();
   const int x0 = X - S + 4 * lane;
@@ -454,16 +526,19 @@ __global__ void __launch_bounds__(128, 2) nlm_sym(NlmParams p, int ntx, int nty,
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base_sh), "n"(G::TMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base_sh), "n"(TMEM_COLS));
   }
 }
 
-template <int P, int S>
+template <int P, int S, bool RING = false>
 inline cudaError_t launch_sym(const NlmParams& p, int batch, cudaStream_t s) {
   using G = SymGeom<P, S>;
   static_assert(G::smem_bytes <= 113 * 1024, "two CTAs per SM");
-  auto kern = nlm_sym<P, S>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::smem_bytes);
+  auto kern = nlm_sym<P, S, RING>;
+  // RING holds all 512 TMEM columns: shared memory above half the SM's so a second CTA never waits
+  // in tcgen05.alloc
+  const size_t smem = RING ? (G::smem_bytes > 115 * 1024 ? G::smem_bytes : 115 * 1024) : G::smem_bytes;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int ntx = (p.src.W + G::TWO - 1) / G::TWO, nty = (p.dst.H + G::TH - 1) / G::TH;
   const long long nblk = (long long)ntx * nty * batch;
@@ -471,7 +546,7 @@ inline cudaError_t launch_sym(const NlmParams& p, int batch, cudaStream_t s) {
   if (nblk > 0x7fffffffLL) return cudaErrorInvalidValue;
   // the asynchronous tile copy moves 8-byte pairs: base, pitch and image stride 8-byte aligned
   const int use_async = ((uintptr_t)p.src.base % 8 == 0) && (p.src.pitch % 8 == 0) && (batch == 1 || p.src.bstride % 8 == 0);
-  kern<<<(unsigned)nblk, G::NT, G::smem_bytes, s>>>(p, ntx, nty, use_async);
+  kern<<<(unsigned)nblk, G::NT, smem, s>>>(p, ntx, nty, use_async);
   count_launch();
   return cudaGetLastError();
 }
