@@ -58,7 +58,7 @@ def measured_peaks():
 
 # variant -> kernel-name fragments (to attach ncu counters only to the kernel they were measured on)
 # (the S = segment-rows variants of one family launch the same kernel function)
-KERNEL_OF = {"sym_tmem": ("nlm_sym<2, 5",), "boxsum_x2": ("nlm_box_x2",), "boxsum_r8": ("nlm_box_r8",),
+KERNEL_OF = {"sym_tmem": ("nlm_sym<2, 5>", "nlm_sym<2, 5, false"), "sym_ring": ("nlm_sym<2, 5, true",), "boxsum_x2": ("nlm_box_x2",), "boxsum_r8": ("nlm_box_r8",),
              **{f"stream_nt64_s{s}_v4": ("sep_stream<2, 64",) for s in (16, 32, 64, 128)},
              **{f"tma_nt32_s{s}_v4": ("sep_stream_tma<2, 32",) for s in (16, 32, 64, 128)},
              **{f"shfl_nw2_s{s}": ("harris_shfl<5, 2>",) for s in (8, 16, 32, 64, 128)}}
@@ -456,7 +456,7 @@ def run_suite(args):
     med = {f: statistics.median(v) for f, v in per.items()}
     # the symmetric kernel (sym_tmem) evaluates half the box sums; the roofline keeps the §8(d)
     # box-sum count of the full window (the algorithmic work)
-    nlm_kind = "boxsum" if variants["nlm"].startswith("boxsum") or variants["nlm"] == "sym_tmem" else "direct"
+    nlm_kind = "boxsum" if variants["nlm"].startswith(("boxsum", "sym_")) else "direct"
     P, Sr = c["nlm_P"], c["nlm_S"]
     pairs = (2 * Sr + 1) ** 2
     nlm_flop_px = pairs * (NLM_FLOP_PER_PAIR[nlm_kind] if nlm_kind == "boxsum" else
@@ -465,7 +465,7 @@ def run_suite(args):
         "nlm": {"bound": "alu", "achieved": nlm_flop_px * px_rank / (med["nlm"] * 1e-3) / 1e12,
                 "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "flop_per_px": nlm_flop_px,
                 "formulation": nlm_kind + (" (offset-symmetric: d_-o(p) = d_o(p-o), half the distances "
-                                           "evaluated)" if variants["nlm"] == "sym_tmem" else ""),
+                                           "evaluated)" if variants["nlm"].startswith("sym_") else ""),
                 "kernel": variants["nlm"],
                 "traffic": _traffic(traffic, "nlm", px_rank)},
         "sepconv": {"bound": "hbm", "achieved": SEP_BYTES_PER_PX * px_rank / (med["sepconv"] * 1e-3) / 1e9,
@@ -488,10 +488,13 @@ def run_suite(args):
         if e and any(k in kname for k in KERNEL_OF.get(roof[f]["kernel"], ())):
             roof[f]["ncu"] = {k: e.get(k) for k in ("fma_pipe_cycles_pct", "issue_active_pct", "smem_wavefronts_pct",
                                                     "mufu_pct")}
-    roof["nlm"]["limiter"] = (
-        "FP32 pipe: the H slide recomputes the row leaving the window (no register/TMEM room for a ring); "
-        "8 warps/SM (TMEM: 256 columns x 2 CTAs; 196 registers), DESIGN.md §5" if variants["nlm"] == "sym_tmem" else
-        "shared-memory wavefronts (two-phase separable box sums: H round trip + accumulation loads, DESIGN.md §5)")
+    roof["nlm"]["limiter"] = {
+        "sym_tmem": "FP32 pipe: the H slide recomputes the row leaving the window (no register/TMEM room for a "
+                    "ring); FFMA2s with three distinct register pairs issue at 2/3 rate; 8 warps/SM (TMEM: 256 "
+                    "columns x 2 CTAs; 222 registers), DESIGN.md §5",
+        "sym_ring": "FFMA2 chain latency at 4 warps/SM (the TMEM ring takes all 512 columns), DESIGN.md §5",
+    }.get(variants["nlm"], "shared-memory wavefronts (two-phase separable box sums: H round trip + accumulation "
+                           "loads, DESIGN.md §5)")
     dominant = max(med, key=med.get)
 
     cpu = None
