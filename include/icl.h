@@ -153,6 +153,10 @@ icl_status icl_harris(const icl_image* src, const icl_image* response, int block
  *   w = exp(-d2/h^2), out(p) = sum_{q in p+[-S,S]^2} w src_B(q) / sum w.
  * patch_radius P in [0,3], search_radius S in [0,10]; h > 0 or +INF
  * (box mean); h <= 0 or NaN -> ICL_ERR_INVALID_ARG.
+ * The box-sum variants re-associate d2 (sliding sums); "sym_tmem" /
+ * "sym_ring" also use d_{-o}(p) = d_o(p-o) (R30: one weight per
+ * pair of offsets) and hold num/den in tensor memory -- results agree with
+ * the direct definition to the NLM tolerance, not bit for bit.
  * ---------------------------------------------------------------------- */
 icl_status icl_nlm(const icl_image* src, const icl_image* dst, int patch_radius, int search_radius,
                    float h, icl_border border, float border_value, const icl_band* band,
