@@ -48,21 +48,15 @@ __device__ __forceinline__ void tm_ld8(uint32_t taddr, float (&v)[8]) {
   v[0] = __uint_as_float(r0); v[1] = __uint_as_float(r1); v[2] = __uint_as_float(r2); v[3] = __uint_as_float(r3);
   v[4] = __uint_as_float(r4); v[5] = __uint_as_float(r5); v[6] = __uint_as_float(r6); v[7] = __uint_as_float(r7);
 }
-// wait for the outstanding tcgen05.ld; the values are threaded through the asm so no use of
-// them can be scheduled above the wait
-__device__ __forceinline__ void tm_wait_ld(float (&a)[8], float (&b)[8]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+f"(a[0]), "+f"(a[1]), "+f"(a[2]), "+f"(a[3]), "+f"(a[4]), "+f"(a[5]), "+f"(a[6]), "+f"(a[7]),
-                 "+f"(b[0]), "+f"(b[1]), "+f"(b[2]), "+f"(b[3]), "+f"(b[4]), "+f"(b[5]), "+f"(b[6]), "+f"(b[7])
-               :
-               : "memory");
-}
+// wait for the outstanding tcgen05.ld (tm_wait_ld), then pin the loaded values behind it (tm_pin8):
+// no use of them can be scheduled above the wait
 __device__ __forceinline__ void tm_st8(uint32_t taddr, const float (&v)[8]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
                "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
                : "memory");
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 // keep values of an earlier tcgen05.ld behind the (preceding, volatile) wait::ld
 __device__ __forceinline__ void tm_pin8(float (&v)[8]) {
   asm volatile("" : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]));
@@ -286,12 +280,9 @@ __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, ui
       sym_ld_win<0, NSW>(row(y + P), cn);
       sym_ld_win<0, NSW>(row(y + P + OY), sn);
       sym_H_all<P, S, OY>(Hn, cn, sn);
-      {
-        float dummy[8];
-        tm_wait_ld(Ho[0], dummy);
-      }
+      tm_wait_ld();
 #pragma unroll
-      for (int g = 1; g < NP; ++g) tm_pin8(Ho[g]);
+      for (int g = 0; g < NP; ++g) tm_pin8(Ho[g]);
 #pragma unroll
       for (int g = 0; g < NP; ++g) {
 #pragma unroll
@@ -398,7 +389,9 @@ __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, ui
     tm_wait_st();
     if (own_ok) tm_ld8(tm + 8 * y, vo);
     if (par_ok) tm_ld8(tm + 8 * (y + OY), vp);
-    tm_wait_ld(vo, vp);
+    tm_wait_ld();
+    if (own_ok) tm_pin8(vo);
+    if (par_ok) tm_pin8(vp);
     if (own_ok) {
 #pragma unroll
       for (int k = 0; k < C; ++k) {
@@ -509,9 +502,10 @@ __global__ void __launch_bounds__(128, RING ? 1 : 2) nlm_sym(NlmParams p, int nt
   const int x0 = X - S + 4 * lane;
 #pragma unroll 1
   for (int y = 0; y < T; ++y) {
-    float v[8], dummy[8];
+    float v[8];
     tm_ld8(tm + 8 * y, v);
-    tm_wait_ld(v, dummy);
+    tm_wait_ld();
+    tm_pin8(v);
     const int ly = Y + warp * T + y;
     if (ly < p.dst.H) {
       float* drow = dst_row(p.dst, b, ly);
