@@ -414,6 +414,9 @@ __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, ui
 template <int P, int S, bool RING, int OY = 1>
 __device__ __forceinline__ void sym_passes(const float* U, int wrow0, int lane, uint32_t tm, float2 nc) {
   sym_pass<P, S, OY, RING>(U, wrow0, lane, tm, nc);
+  // keep the CTA's warps in the same pass: they then share the instruction fetch of one pass body
+  // (~0.4% faster; a barrier every step or every 4 steps costs 3%)
+  __syncthreads();
   if constexpr (OY < S) sym_passes<P, S, RING, OY + 1>(U, wrow0, lane, tm, nc);
 }
 
