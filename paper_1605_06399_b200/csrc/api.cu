@@ -37,6 +37,7 @@ bool nlm_x2_supported(int P, int S);
 bool nlm_w_supported(int P, int S);
 bool nlm_sym_supported(int P, int S);
 bool nlm_sym_ring_supported(int P, int S);
+bool nlm_sym8_supported(int P, int S);
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -143,7 +144,7 @@ static icl_status make_views(const icl_image* src, const icl_image* dst, const i
 }
 
 // ------------------------------------------------------------------ variants
-enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL, K_TILE2, K_BOXX2, K_C2TILE, K_TEX, K_SLIDE, K_BOXW, K_PMAP, K_BOXSYM, K_BOXRING, K_COUNT };
+enum Kind { K_NAIVE, K_TWOPASS, K_STREAM, K_TILED, K_BOXSUM, K_BOXR8, K_BULK, K_BOXR16, K_SHFL, K_TILE2, K_BOXX2, K_C2TILE, K_TEX, K_SLIDE, K_BOXW, K_PMAP, K_BOXSYM, K_BOXRING, K_BOXSYM8, K_COUNT };
 struct Variant {
   const char* name;
   Kind kind;
@@ -212,6 +213,7 @@ static const Variant kNlmVariants[] = {
     {"boxsum_w", K_BOXW, 0, 0, 1},
     {"sym_tmem", K_BOXSYM, 0, 0, 0},
     {"sym_ring", K_BOXRING, 0, 0, 0},
+    {"sym_tmem8", K_BOXSYM8, 0, 0, 0},
 };
 
 static const Variant kConvVariants[] = {
@@ -347,6 +349,7 @@ static bool eligible(const Prepared& pc, const Variant& v, icl_status* why) {
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXW && !nlm_w_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXSYM && !nlm_sym_supported(pc.nlm.P, pc.nlm.S)) return false;
   if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXRING && !nlm_sym_ring_supported(pc.nlm.P, pc.nlm.S)) return false;
+  if (pc.f == ICL_FILTER_NLM && v.kind == K_BOXSYM8 && !nlm_sym8_supported(pc.nlm.P, pc.nlm.S)) return false;
   return true;
 }
 
@@ -438,6 +441,7 @@ static cudaError_t run_variant_1(const Prepared& pc, const Variant& v, cudaStrea
       if (v.kind == K_BOXW) return launch_nlm_w(pc.nlm, v.S, s);
       if (v.kind == K_BOXSYM) return launch_nlm_sym(pc.nlm, s);
       if (v.kind == K_BOXRING) return launch_nlm_sym_ring(pc.nlm, s);
+      if (v.kind == K_BOXSYM8) return launch_nlm_sym8(pc.nlm, s);
       return launch_nlm_boxsum(pc.nlm, 0, s);
     case ICL_FILTER_CONV2D:
       if (v.kind == K_NAIVE) return launch_conv2d_naive(pc.c2d, s);

@@ -100,6 +100,7 @@ cudaError_t launch_nlm_x2(const NlmCall& c, cudaStream_t s);
 cudaError_t launch_nlm_w(const NlmCall& c, int unroll, cudaStream_t s);
 cudaError_t launch_nlm_sym(const NlmCall& c, cudaStream_t s);
 cudaError_t launch_nlm_sym_ring(const NlmCall& c, cudaStream_t s);
+cudaError_t launch_nlm_sym8(const NlmCall& c, cudaStream_t s);
 // conv2d (u8)
 cudaError_t launch_conv2d_naive(const Conv2dCall& c, cudaStream_t s);
 cudaError_t launch_conv2d_tile(const Conv2dCall& c, int rows_per_thread, bool persistent, cudaStream_t s);

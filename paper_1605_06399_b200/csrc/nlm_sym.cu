@@ -22,6 +22,16 @@ cudaError_t launch_nlm_sym_ring(const NlmCall& c, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
+// "sym_tmem8": one 8-warp CTA per SM (the warps of an SM run each pass together)
+bool nlm_sym8_supported(int P, int S) { return (P == 2 && S == 5) || (P == 1 && S == 3); }
+
+cudaError_t launch_nlm_sym8(const NlmCall& c, cudaStream_t s) {
+  NlmParams p = make_nlm_params(c);
+  if (c.P == 2 && c.S == 5) return launch_sym<2, 5, false, 8>(p, c.batch, s);
+  if (c.P == 1 && c.S == 3) return launch_sym<1, 3, false, 8>(p, c.batch, s);
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_nlm_sym(const NlmCall& c, cudaStream_t s) {
   NlmParams p = make_nlm_params(c);
 #define ICL_SYM_RUN(PP, SS) if (c.P == PP && c.S == SS) return launch_sym<PP, SS>(p, c.batch, s);

@@ -62,10 +62,10 @@ __device__ __forceinline__ void tm_pin8(float (&v)[8]) {
   asm volatile("" : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]));
 }
 
-template <int P, int S>
+template <int P, int S, int NW_ = 4>
 struct SymGeom {
   static constexpr int C = 4;                 // columns per lane
-  static constexpr int NW = 4;                // warps per CTA (stacked vertically)
+  static constexpr int NW = NW_;              // warps per CTA (stacked vertically): 4, or 8 (one CTA/SM)
   static constexpr int T = 32;                // output rows per warp
   static constexpr int NT = 32 * NW;
   static constexpr int TWO = 128 - 2 * S;     // output columns per strip
@@ -76,13 +76,14 @@ struct SymGeom {
   static constexpr int NCW = C + 2 * P;       // centre window of a lane (H)
   static constexpr int NSW = C + 2 * P + 2 * S;  // shifted window (H, every ox)
   static constexpr int NIW = C + 2 * S;       // accumulation window u(q + o), and the partner window
-  static constexpr int TMEM_COLS = 8 * T;     // num[4] den[4] per row
+  static constexpr int WARP_COLS = 8 * T;     // num[4] den[4] per row
+  static constexpr int TMEM_COLS = WARP_COLS * (NW / 4);  // warps w and w+4 share a lane quadrant
   // at least 77 KB: never three CTAs on an SM (two CTAs x 256 columns fill the 512 TMEM columns; a
   // third would spin in tcgen05.alloc until one of them finishes)
   static constexpr size_t tile_bytes = (size_t)SW * SH * sizeof(float);
   static constexpr size_t smem_bytes = tile_bytes > 77 * 1024 ? tile_bytes : 77 * 1024;
   static_assert(S >= 1 && S <= 8, "partner exchange reaches two lanes");
-  static_assert(TMEM_COLS == 256, "two CTAs per SM share the 512 TMEM columns");
+  static_assert(WARP_COLS == 256 && (NW == 4 || NW == 8), "two 4-warp CTAs or one 8-warp CTA fill the 512 TMEM columns");
 };
 
 // N consecutive floats starting OFF floats after a 16-byte aligned lane base, via LDS.128
@@ -422,11 +423,13 @@ __device__ __forceinline__ void sym_passes(const float* U, int wrow0, int lane, 
 
 // RING = false: 2 CTAs/SM, 256 TMEM columns each (num/den), the slide recomputes the leaving row.
 // RING = true ("sym_ring"): 1 CTA/SM with all 512 columns: num/den + the H ring of the last 2P+1 rows.
-template <int P, int S, bool RING>
-__global__ void __launch_bounds__(128, RING ? 1 : 2) nlm_sym(NlmParams p, int ntx, int nty, int use_async) {
-  using G = SymGeom<P, S>;
+// NW = 8 ("sym_tmem8"): one 8-warp CTA per SM (256 x 118 tiles); its warps run each pass together.
+template <int P, int S, bool RING, int NW = 4>
+__global__ void __launch_bounds__(32 * NW, (RING || NW == 8) ? 1 : 2) nlm_sym(NlmParams p, int ntx, int nty,
+                                                                              int use_async) {
+  using G = SymGeom<P, S, NW>;
   constexpr int TMEM_COLS = RING ? 512 : G::TMEM_COLS;
-  static_assert(!RING || G::TMEM_COLS + 8 * (2 * P + 1) * (S + 1) <= 512, "ring fits the tensor memory");
+  static_assert(!RING || (NW == 4 && G::WARP_COLS + 8 * (2 * P + 1) * (S + 1) <= 512), "ring fits the tensor memory");
   constexpr int C = G::C, SW = G::SW, SH = G::SH, T = G::T, TWO = G::TWO, TH = G::TH;
   extern __shared__ __align__(128) float U[];
   __shared__ uint32_t tm_base_sh;
@@ -486,7 +489,7 @@ __global__ void __launch_bounds__(128, RING ? 1 : 2) nlm_sym(NlmParams p, int nt
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tm = tm_base_sh + ((uint32_t)(32 * warp) << 16);
+  const uint32_t tm = tm_base_sh + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(G::WARP_COLS * (warp >> 2));
   const int wrow0 = warp * T + S + P + 1;  // smem row of the warp's output row 0
   const float* Ul = U + 4 * lane;
 
@@ -527,14 +530,16 @@ __global__ void __launch_bounds__(128, RING ? 1 : 2) nlm_sym(NlmParams p, int nt
   }
 }
 
-template <int P, int S, bool RING = false>
+template <int P, int S, bool RING = false, int NW = 4>
 inline cudaError_t launch_sym(const NlmParams& p, int batch, cudaStream_t s) {
-  using G = SymGeom<P, S>;
-  static_assert(G::smem_bytes <= 113 * 1024, "two CTAs per SM");
-  auto kern = nlm_sym<P, S, RING>;
-  // RING holds all 512 TMEM columns: shared memory above half the SM's so a second CTA never waits
-  // in tcgen05.alloc
-  const size_t smem = RING ? (G::smem_bytes > 115 * 1024 ? G::smem_bytes : 115 * 1024) : G::smem_bytes;
+  using G = SymGeom<P, S, NW>;
+  static_assert(NW == 8 || G::smem_bytes <= 113 * 1024, "two CTAs per SM");
+  static_assert(G::smem_bytes <= 227 * 1024, "shared memory");
+  auto kern = nlm_sym<P, S, RING, NW>;
+  // RING / NW = 8 hold all 512 TMEM columns: shared memory above half the SM's so a second CTA never
+  // waits in tcgen05.alloc
+  const bool one = RING || NW == 8;
+  const size_t smem = one ? (G::smem_bytes > 115 * 1024 ? G::smem_bytes : 115 * 1024) : G::smem_bytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int ntx = (p.src.W + G::TWO - 1) / G::TWO, nty = (p.dst.H + G::TH - 1) / G::TH;
