@@ -33,6 +33,19 @@ def _force_sym():
     icl.force_variant("nlm", None)
 
 
+@pytest.mark.parametrize("variant", ["sym_ring", "sym_tmem8"])
+@pytest.mark.parametrize("P,S,h", [(2, 5, 0.1), (1, 3, 0.05)])
+def test_sym_variants_multi_tile_vs_oracle(variant, P, S, h):
+    """the TMEM-ring and the 8-warp forms on 2 images of 300 x 389 (several strips and CTA rows,
+    interior and border tiles), clamp and constant borders, every pixel vs the oracle."""
+    icl.force_variant("nlm", variant)
+    img = np.stack([synth.rect_scene(900 + 10 * P + S + i, 300, 389, n_rect=20, noise=0.0866) for i in range(2)])
+    for border, c in (("clamp", 0.0), ("constant", 0.3)):
+        out = _run(img, P, S, h, border, c)
+        for i in range(2):
+            check_nlm(out[i], img[i], P, S, h, border, c)
+
+
 def _dev(img, pitch=None):
     b, h, w = img.shape
     pitch = pitch or w
