@@ -27,6 +27,11 @@
 //     8 columns per row: num[4], den[4]), read-modify-written once per (row, oy) for the own
 //     row and once for the partner row, with tcgen05.ld / tcgen05.st -- the on-chip space that
 //     lets the walk be long (32 rows) without giving up registers or shared memory.
+//   * interior tiles are staged by 8-byte cp.async (all in flight), border tiles through read_B;
+//     a barrier after each pass keeps the CTA's warps on one pass body (instruction fetch).
+// Variants: "sym_tmem" (2 CTAs x 4 warps per SM, the default for large calls), "sym_ring" (RING:
+// one CTA/SM whose TMEM also holds the last 2P+1 H rows, so a step computes only the entering
+// row), "sym_tmem8" (NW = 8: one 8-warp CTA per SM).  DESIGN.md §5 has the measurements.
 // Results agree with the direct definition to rounding (tolerance-checked, R16).
 #pragma once
 
