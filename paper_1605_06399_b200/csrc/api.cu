@@ -501,8 +501,10 @@ static int default_variant(const Prepared& pc) {
       // (1024^2 24.5 vs 34.8 us, 2048^2 30.7 vs 66 us, 4096^2 76 vs 90 us; 8 x 4096^2 prefers s64)
       return variant_id(pc.f, pc.pixels <= (1 << 21) ? "shfl_nw2_s8" : pc.pixels <= (1 << 25) ? "shfl_nw2_s16" : "shfl_nw2_s32");
     case ICL_FILTER_NLM:
-      // the offset-symmetric TMEM kernel once the launch fills the GPU (118 x 128 tiles, 2 CTAs/SM)
-      if (nlm_sym_supported(pc.nlm.P, pc.nlm.S) && pc.pixels >= (1 << 23)) return variant_id(pc.f, "sym_tmem");
+      // the offset-symmetric TMEM kernel once the launch fills most of one wave of 118 x 128 tiles
+      // (2 CTAs/SM; 2048^2: 0.265 vs 0.319 ms for boxsum_x2, 1792^2 a tie, 1536^2 0.266 vs 0.191 ms --
+      // profiles/r02e_nlm_sizes.txt)
+      if (nlm_sym_supported(pc.nlm.P, pc.nlm.S) && pc.pixels >= (1 << 22)) return variant_id(pc.f, "sym_tmem");
       if (nlm_x2_supported(pc.nlm.P, pc.nlm.S)) return variant_id(pc.f, "boxsum_x2");
       if (nlm_r8_supported(pc.nlm.P, pc.nlm.S)) return variant_id(pc.f, "boxsum_r8");
       return nlm_tiled_supported(pc.nlm.P, pc.nlm.S) ? variant_id(pc.f, "tiled_direct_32x8") : 0;
