@@ -12,6 +12,7 @@ import math
 import numpy as np
 import pytest
 
+import oracle
 import synth
 from tests._tol import check_nlm
 
@@ -108,3 +109,18 @@ def test_sym_agrees_with_boxsum_x2_large():
     ys = np.concatenate([rng.integers(0, 1024, 1500), np.repeat([0, 127, 128, 255, 1023], 40)])
     xs = np.concatenate([rng.integers(0, 1536, 1500), np.tile(np.arange(0, 1536, 39)[:40], 5)])
     check_nlm(out[0][ys, xs], img[0], 2, 5, 0.1, "clamp", 0.0, points=(xs, ys))
+
+
+@pytest.mark.parametrize("variant", ["sym_tmem", "sym_ring"])
+def test_sym_equivariant_under_flips_and_transpose(variant):
+    """NLM commutes with transposition and flips (symmetric patch and window, per-coordinate
+    boundary): the symmetric kernels' partner bookkeeping is direction-specific (the half set
+    {oy > 0} u {oy = 0, ox > 0}), so a flipped or transposed image sends every pair through the
+    other half -- the outputs must still agree with the flipped output to the NLM tolerance."""
+    icl.force_variant("nlm", variant)
+    img = synth.rect_scene(977, 260, 300, n_rect=16, noise=0.0866)
+    out = _run(img[None], 2, 5, 0.1, "clamp", 0.0)[0]
+    _, scale = oracle.nlm(img, 2, 5, 0.1, "clamp", 0.0, with_scale=True)
+    for f in (lambda a: a.T, lambda a: a[:, ::-1], lambda a: a[::-1, :]):
+        got = _run(np.ascontiguousarray(f(img))[None], 2, 5, 0.1, "clamp", 0.0)[0]
+        np.testing.assert_array_less(np.abs(got - f(out)), 2e-4 * f(scale) + 1e-30)

@@ -227,6 +227,18 @@ def test_nlm_invariants():
     np.testing.assert_allclose(out_s, out + 0.5, rtol=0, atol=1e-6)
 
 
+@pytest.mark.parametrize("border,c", [("clamp", 0.0), ("constant", 0.3)])
+def test_nlm_equivariant_under_flips_and_transpose(border, c):
+    """The patch (2P+1)^2 and the search window (2S+1)^2 are symmetric squares and the boundary
+    is per coordinate, so NLM commutes with transposition and with either flip -- a swapped row /
+    column index or an asymmetric window in the oracle breaks one of these."""
+    img = synth.rect_scene(15, 13, 11, n_rect=5, noise=0.0866)
+    out = oracle.nlm(img, 2, 3, 0.15, border, c)
+    for f in (lambda a: a.T, lambda a: a[:, ::-1], lambda a: a[::-1, :]):
+        got = oracle.nlm(np.ascontiguousarray(f(img)), 2, 3, 0.15, border, c)
+        np.testing.assert_allclose(got, f(out), rtol=0, atol=1e-14)
+
+
 def test_nlm_rejects_bad_h():
     img = np.zeros((3, 3), np.float32)
     for h in (0.0, -1.0, float("nan")):
