@@ -24,6 +24,13 @@
 
 namespace icl {
 
+// Row segment of this CTA.  The last segment (bottom border, general path) is launched first: in a
+// grid of about one wave (e.g. BASELINE configs[1], 2048^2) the slower border CTAs then run beside
+// the interior ones instead of forming the tail.
+__device__ __forceinline__ int hshfl_segment() {
+  return blockIdx.y == 0 ? (int)gridDim.y - 1 : (int)blockIdx.y - 1;
+}
+
 template <int B, int NW>
 __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, float* smem) {
   constexpr int A = B / 2;
@@ -38,7 +45,7 @@ __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, f
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.z;
   const int x0 = blockIdx.x * TW;
-  const int ly0 = blockIdx.y * S;
+  const int ly0 = hshfl_segment() * S;
   const int ly1 = min(ly0 + S, p.dst.H);
   const int g0 = p.dst.y0 + ly0;
   const int NY = (ly1 - ly0) + B - 1;
@@ -274,7 +281,7 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.z;
   const int x0 = blockIdx.x * TW;
-  const int ly0 = blockIdx.y * S;
+  const int ly0 = hshfl_segment() * S;
   const int ly1 = min(ly0 + S, p.dst.H);
   const int g0 = p.dst.y0 + ly0;
   const int NY = (ly1 - ly0) + B - 1;
@@ -515,7 +522,7 @@ template <int B, int NW>
 __global__ void __launch_bounds__(32 * NW, ICL_HSHFL_MINB) harris_shfl(HarrisParams p, int S) {
   extern __shared__ __align__(16) float smem[];
   constexpr int TW = 120 * NW, HP = 8, A = B / 2, BB = B - 1 - A;
-  const int x0 = blockIdx.x * TW, ly0 = blockIdx.y * S;
+  const int x0 = blockIdx.x * TW, ly0 = hshfl_segment() * S;
   const int ly1 = min(ly0 + S, p.dst.H);
   const int g0 = p.dst.y0 + ly0;
   // every input row (g0-A-1 .. last output row + BB + 1) and column inside the image
