@@ -484,7 +484,8 @@ static int default_variant(const Prepared& pc) {
         // 16384^2 R = 1 / 2 / 3 / 5 / 8 / 10 in 0.361 / 0.364 / 0.385 / 0.410 / 0.591 / 0.781 ms
         // vs 0.378 / 0.383 / 0.403 / 0.453 / 0.664 / 0.841; 8 x 4096^2 R = 2 0.205 vs 0.218 ms)
         const int R = pc.sep.rx > pc.sep.ry ? pc.sep.rx : pc.sep.ry;
-        if (R <= 2 || R == 4) return variant_id(pc.f, "tma_nt32_s16_v4");
+        // (round 2f: branch-free full blocks for R <= 4: 16384^2 R = 3 / 4 in 0.354 / 0.364 ms)
+        if (R <= 4) return variant_id(pc.f, "tma_nt32_s16_v4");
         if (R <= 5) return variant_id(pc.f, "tma_nt32_s32_v4");
         if (R <= 8) return variant_id(pc.f, "tma_nt32_s64_v4");
         if (R == 9) return variant_id(pc.f, "tma_nt32_s128_v4");
