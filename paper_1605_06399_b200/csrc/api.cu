@@ -486,10 +486,11 @@ static int default_variant(const Prepared& pc) {
         const int R = pc.sep.rx > pc.sep.ry ? pc.sep.rx : pc.sep.ry;
         // (round 2f: branch-free full blocks for R <= 4: 16384^2 R = 3 / 4 in 0.354 / 0.364 ms)
         if (R <= 4) return variant_id(pc.f, "tma_nt32_s16_v4");
+        // (round 2f: predicated single-block bodies for R >= 5: 16384^2 R = 5..10 in 0.394 / 0.426 /
+        // 0.476 / 0.508 / 0.618 / 0.720 ms, profiles/r02f_sweep16k.txt)
         if (R <= 5) return variant_id(pc.f, "tma_nt32_s32_v4");
-        if (R <= 8) return variant_id(pc.f, "tma_nt32_s64_v4");
-        if (R == 9) return variant_id(pc.f, "tma_nt32_s128_v4");
-        if (R == 10) return variant_id(pc.f, "tma_nt32_s64_v4");
+        if (R == 6 || R == 8 || R == 10) return variant_id(pc.f, "tma_nt32_s64_v4");
+        if (R == 7 || R == 9) return variant_id(pc.f, "tma_nt32_s128_v4");
         return variant_id(pc.f, "tile64p_v4");
       }
     case ICL_FILTER_HARRIS:

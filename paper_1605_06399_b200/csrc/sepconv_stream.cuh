@@ -210,6 +210,7 @@ __device__ __forceinline__ void sep_stream_body(const SepParams& p, int S, const
     // the duplicated block body costs more in instruction fetch than the overlap gains (16384^2:
     // R = 4 0.359 vs 0.387 ms; R = 6 / 8 / 10 0.468 / 0.636 / 0.877 vs 0.433 / 0.574 / 0.771 ms).
     constexpr bool kFastBlocks = R <= 4;
+    constexpr bool kPredBlocks = R >= 5;
     const bool full = kFastBlocks && VEC == 4 && !edge && (i + 1) * RB <= NI && i * RB >= 2 * R;
     auto step = [&](const int u, const int k, auto fast_tag) {
       constexpr bool FAST = decltype(fast_tag)::value;
@@ -247,6 +248,28 @@ __device__ __forceinline__ void sep_stream_body(const SepParams& p, int S, const
           }
         }
         ring[u % P] = make_float4(t01.x, t01.y, t23.x, t23.y);
+        if constexpr (kPredBlocks) {
+          // R >= 5: the column pass for every step (a partly filled ring before step 2R only
+          // feeds discarded outputs) and emission by predicate, so every block is one basic block
+          // without duplicating the body (16384^2 R = 5 / 6 / 7 / 8 / 9 / 10: 0.397 / 0.427 /
+          // 0.476 / 0.509 / 0.625 / 0.730 vs 0.408 / 0.441 / 0.497 / 0.587 / 0.708 / 0.778 ms)
+          const bool em = FAST || (k >= 2 * R && k < NI);
+          float2 o01 = make_float2(0.0f, 0.0f), o23 = make_float2(0.0f, 0.0f);
+#pragma unroll
+          for (int j = 0; j < P; ++j) {
+            const float4 rr = ring[(u + 1 + j) % P];
+            const float2 g = make_float2(p.gy[j], p.gy[j]);
+            o01 = __ffma2_rn(g, make_float2(rr.x, rr.y), o01);
+            o23 = __ffma2_rn(g, make_float2(rr.z, rr.w), o23);
+          }
+          const float o[4] = {o01.x, o01.y, o23.x, o23.y};
+          const bool v4 = FAST || (VEC == 4 && xc + 3 < W);
+          if (em && v4) st_cs4(drow + xc, make_float4(o[0], o[1], o[2], o[3]));
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (!FAST && em && !v4 && xc + c < W) drow[xc + c] = o[c];
+          drow += em ? dpitch : 0;
+        } else {
         if (FAST || k >= 2 * R) {
           // column pass: two columns per FFMA2 (the tap broadcast), each lane its scalar chain
           float2 o01 = make_float2(0.0f, 0.0f), o23 = make_float2(0.0f, 0.0f);
@@ -267,6 +290,7 @@ __device__ __forceinline__ void sep_stream_body(const SepParams& p, int S, const
           }
           drow += dpitch;
         }
+        }
     };
     if constexpr (kFastBlocks) {
       if (full) {
@@ -279,7 +303,7 @@ __device__ __forceinline__ void sep_stream_body(const SepParams& p, int S, const
 #pragma unroll
       for (int u = 0; u < RB; ++u) {
         const int k = i * RB + u;
-        if (k < NI) step(u, k, std::false_type{});
+        if (kPredBlocks || k < NI) step(u, k, std::false_type{});
       }
     }
   }
