@@ -63,7 +63,8 @@ KERNEL_OF = {"sym_tmem": ("nlm_sym<2, 5, 0, 4>", "nlm_sym<2, 5, false, 4>", "nlm
              "sym_tmem8": ("nlm_sym<2, 5, 0, 8>", "nlm_sym<2, 5, false, 8>"), "boxsum_x2": ("nlm_box_x2",), "boxsum_r8": ("nlm_box_r8",),
              **{f"stream_nt64_s{s}_v4": ("sep_stream<2, 64",) for s in (16, 32, 64, 128)},
              **{f"tma_nt32_s{s}_v4": ("sep_stream_tma<2, 32",) for s in (16, 32, 64, 128)},
-             **{f"shfl_nw2_s{s}": ("harris_shfl<5, 2>",) for s in (8, 16, 32, 64, 128)}}
+             **{f"shfl_nw2_s{s}": ("harris_shfl<5, 2>",) for s in (8, 16, 32, 64, 128)},
+             **{f"shfl_tma_nw2_s{s}": ("harris_shfl_tma<5, 2>",) for s in (8, 16, 32)}}
 
 
 def ncu_traffic():

@@ -194,6 +194,9 @@ static const Variant kHarVariants[] = {
     // one-warp CTAs (120-column strips): more CTAs for images that do not fill the GPU
     {"shfl_nw1_s16", K_SHFL, 1, 4, 16},           {"shfl_nw1_s32", K_SHFL, 1, 4, 32},
     {"shfl_nw1_s8", K_SHFL, 1, 4, 8},
+    // interior ring blocks staged by one TMA box each (vec 7; 16-byte aligned images)
+    {"shfl_tma_nw2_s32", K_SHFL, 2, 7, 32},       {"shfl_tma_nw2_s16", K_SHFL, 2, 7, 16},
+    {"shfl_tma_nw2_s8", K_SHFL, 2, 7, 8},
     // separable window sums on the products (re-associated: tolerance vs naive, R16)
     {"slide_nw2_s32", K_SLIDE, 2, 4, 32},         {"slide_nw2_s16", K_SLIDE, 2, 4, 16},
     {"slide_nw2_s64", K_SLIDE, 2, 4, 64},         {"slide_nw2_s8", K_SLIDE, 2, 4, 8},
@@ -428,7 +431,7 @@ static cudaError_t run_variant_1(const Prepared& pc, const Variant& v, cudaStrea
       return launch_sep_stream(pc.sep, v.nt, v.vec, v.S, s);
     case ICL_FILTER_HARRIS:
       if (v.kind == K_NAIVE) return launch_harris_naive(pc.har, s);
-      if (v.kind == K_SHFL) return launch_harris_shfl(pc.har, v.nt, v.S, s);
+      if (v.kind == K_SHFL) return launch_harris_shfl(pc.har, v.nt, v.S, s, v.vec == 7);
       if (v.kind == K_SLIDE) return launch_harris_slide(pc.har, v.nt, v.vec == 8 ? 2 : v.vec == 6 ? 3 : 1, v.S, s);
       if (v.kind == K_PMAP) return launch_harris_pmap(pc.har, v.pm, s);
       return launch_harris_stream(pc.har, v.nt, v.vec, v.S, s);
@@ -501,7 +504,10 @@ static int default_variant(const Prepared& pc) {
       if (pc.pixels < (1 << 16)) return variant_id(pc.f, "stream_nt32_s16_v4");
       // 240-column strips: short row segments keep enough CTAs in flight up to one 4096^2 image
       // (1024^2 24.5 vs 34.8 us, 2048^2 30.7 vs 66 us, 4096^2 76 vs 90 us; 8 x 4096^2 prefers s64)
-      return variant_id(pc.f, pc.pixels <= (1 << 21) ? "shfl_nw2_s8" : pc.pixels <= (1 << 25) ? "shfl_nw2_s16" : "shfl_nw2_s32");
+      // (round 2f: the same kernels with TMA-fed ring blocks, bit-identical: 8 x 4096^2 0.385 vs
+      // 0.396 ms, 2048^2 25.4 vs 26.6 us)
+      return variant_id(pc.f, pc.pixels <= (1 << 21) ? "shfl_tma_nw2_s8"
+                              : pc.pixels <= (1 << 25) ? "shfl_tma_nw2_s16" : "shfl_tma_nw2_s32");
     case ICL_FILTER_NLM:
       // the offset-symmetric TMEM kernel once the launch fills most of one wave of 118 x 128 tiles
       // (2 CTAs/SM; 2048^2: 0.265 vs 0.319 ms for boxsum_x2, 1792^2 a tie, 1536^2 0.266 vs 0.191 ms --

@@ -100,8 +100,13 @@ extern template cudaError_t dispatch_hshfl<1>(const HarrisParams&, int, int, cud
 extern template cudaError_t dispatch_hshfl<2>(const HarrisParams&, int, int, cudaStream_t);
 extern template cudaError_t dispatch_hshfl<4>(const HarrisParams&, int, int, cudaStream_t);
 
-cudaError_t launch_harris_shfl(const HarrisCall& c, int nw, int S, cudaStream_t s) {
+template <int NW>
+cudaError_t dispatch_hshfl_tma(const HarrisParams& p, int batch, int S, cudaStream_t s);
+extern template cudaError_t dispatch_hshfl_tma<2>(const HarrisParams&, int, int, cudaStream_t);
+
+cudaError_t launch_harris_shfl(const HarrisCall& c, int nw, int S, cudaStream_t s, bool tma) {
   HarrisParams p = make_params(c);
+  if (tma) return nw == 2 ? dispatch_hshfl_tma<2>(p, c.batch, S, s) : cudaErrorInvalidValue;
   if (nw == 1) return dispatch_hshfl<1>(p, c.batch, S, s);
   if (nw == 2) return dispatch_hshfl<2>(p, c.batch, S, s);
   if (nw == 4) return dispatch_hshfl<4>(p, c.batch, S, s);

@@ -16,6 +16,8 @@
 // row (== H(clamp(yy)), per-stage semantics).  Same per-output fp32 operation
 // order as every other Harris variant (bit-identical).
 #pragma once
+#include <cuda.h>
+
 #include "harris_stream.cuh"
 
 #ifndef ICL_HSHFL_MINB
@@ -267,8 +269,15 @@ __device__ __forceinline__ void harris_shfl_fast(const HarrisParams& p, int S, f
 // loader zero-fills columns outside [0, W), fix_block applies the input boundary there (mirror rows
 // included), dx/dy outside [0, W) take the per-stage boundary, and stores are guarded -- the
 // general path's column logic without its row logic.
-template <int B, int NW, bool EDGE>
-__device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int S, float* smem) {
+// TMA (the "shfl_tma_*" variants, NW <= 2): each block of RB ring rows arrives as ONE
+// cp.async.bulk.tensor box (tm_blk: ROWLEN x RB) issued by thread 0 -- plus a 2-row box (tm_mir)
+// for the mirror rows when the block lands in ring slot 0 -- completing on that slot's mbarrier;
+// columns outside the image are zero-filled by the TMA unit exactly as by the zero-byte cp.async.
+template <int B, int NW, bool EDGE, bool TMA = false>
+__device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int S, float* smem,
+                                                     const CUtensorMap* tm_blk = nullptr,
+                                                     const CUtensorMap* tm_mir = nullptr,
+                                                     uint64_t* bars = nullptr) {
   constexpr int A = B / 2;
   constexpr int BB = B - 1 - A;
   constexpr int NT = 32 * NW;
@@ -308,7 +317,18 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
   const float* gsrc2 = src_row(p.src, b, g0 - A - 1) + (EDGE && nb2 == 0 ? 0 : xs2);
   float* sdst2 = smem + 4 * tid2;
 
+  const int trow0 = g0 - A - 1 - p.src.y0;  // band-buffer row of load index 0
   auto load_block = [&](int m) {
+    if constexpr (TMA) {
+      if (tid == 0) {
+        const int r0 = (m % NBLKS) * RB;
+        uint64_t* bar = &bars[m % NBLKS];
+        mbar_arrive_expect_tx(bar, (uint32_t)((RB + (r0 == 0 ? 2 : 0)) * ROWLEN * sizeof(float)));
+        tma_load_3d(smem + r0 * ROWLEN, tm_blk, x0 - HP, trow0 + m * RB, b, bar);
+        if (r0 == 0) tma_load_3d(smem + NSR * ROWLEN, tm_mir, x0 - HP, trow0 + m * RB, b, bar);  // mirror
+      }
+      return;
+    }
     if (!loader) return;
     const float* g = gsrc + (int64_t)(m * RB) * spitch;
     const float* g2 = gsrc2 + (int64_t)(m * RB) * spitch;
@@ -347,9 +367,17 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
       }
     }
   };
+  if constexpr (TMA) {
+    if (tid == 0) {
+#pragma unroll
+      for (int m = 0; m < NBLKS; ++m) mbar_init(&bars[m], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+  }
   for (int m = 0; m < NBLKS - 1; ++m) {
     if (m < NBL) load_block(m);
-    cp_async_commit();
+    if constexpr (!TMA) cp_async_commit();
   }
 
   const int xl = x0 + 120 * warp + 4 * (lane - 1);
@@ -380,7 +408,12 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
 
 #pragma unroll 1
   for (int i = 0; i < NBI; ++i) {
-    cp_async_wait<NBLKS - 3>();
+    if constexpr (TMA) {  // blocks i and i+1 (a step reads up to two rows past its block)
+      mbar_wait(&bars[i % NBLKS], (uint32_t)((i / NBLKS) & 1));
+      if (i + 1 < NBL) mbar_wait(&bars[(i + 1) % NBLKS], (uint32_t)(((i + 1) / NBLKS) & 1));
+    } else {
+      cp_async_wait<NBLKS - 3>();
+    }
     __syncthreads();
     if (EDGE) {  // rows of load blocks i (first time only) and i+1 become visible now
       if (i == 0) fix_block(0);
@@ -388,7 +421,7 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
       __syncthreads();
     }
     if (i + NBLKS - 1 < NBL) load_block(i + NBLKS - 1);
-    cp_async_commit();
+    if constexpr (!TMA) cp_async_commit();
     if (!warp_live) continue;
     const float* sb = stb + (i % NBLKS) * RB * ROWLEN;
 #pragma unroll 1
@@ -515,7 +548,11 @@ __device__ __forceinline__ void harris_shfl_interior(const HarrisParams& p, int 
       }
     }
   }
-  cp_async_wait<0>();
+  if constexpr (TMA) {  // boxes issued past the last computed block land before the CTA exits
+    for (int m = NBI + 1; m < NBL; ++m) mbar_wait(&bars[m % NBLKS], (uint32_t)((m / NBLKS) & 1));
+  } else {
+    cp_async_wait<0>();
+  }
 }
 
 template <int B, int NW>
@@ -533,6 +570,61 @@ __global__ void __launch_bounds__(32 * NW, ICL_HSHFL_MINB) harris_shfl(HarrisPar
   if (interior) harris_shfl_interior<B, NW, false>(p, S, smem);
   else if (rows_in) harris_shfl_interior<B, NW, true>(p, S, smem);
   else harris_shfl_fast<B, NW>(p, S, smem);
+}
+
+// the "shfl_tma_*" variants: the interior paths fed by TMA boxes (NW <= 2: a ring row of 120*NW + 16
+// columns fits one box); the general path (top / bottom segments) keeps the per-thread loader
+template <int B, int NW>
+__global__ void __launch_bounds__(32 * NW, ICL_HSHFL_MINB) harris_shfl_tma(HarrisParams p, int S,
+                                                                            const __grid_constant__ CUtensorMap tm_blk,
+                                                                            const __grid_constant__ CUtensorMap tm_mir) {
+  extern __shared__ __align__(128) float hsmem_tma[];  // TMA destinations: 128-byte aligned ring
+  __shared__ __align__(8) uint64_t bars[HarFastGeom<B>::NBLKS];
+  float* smem = hsmem_tma;
+  constexpr int TW = 120 * NW, HP = 8, A = B / 2, BB = B - 1 - A;
+  const int x0 = blockIdx.x * TW, ly0 = hshfl_segment() * S;
+  const int ly1 = min(ly0 + S, p.dst.H);
+  const int g0 = p.dst.y0 + ly0;
+  const bool interior = x0 - HP >= 0 && x0 + TW + HP <= p.src.W && g0 - A - 1 >= 0 &&
+                        p.dst.y0 + ly1 + BB + 1 <= p.src.Hg;
+  const bool rows_in = g0 - A - 1 >= 0 && p.dst.y0 + ly1 + BB + 1 <= p.src.Hg;
+  if (interior) harris_shfl_interior<B, NW, false, true>(p, S, smem, &tm_blk, &tm_mir, bars);
+  else if (rows_in) harris_shfl_interior<B, NW, true, true>(p, S, smem, &tm_blk, &tm_mir, bars);
+  else harris_shfl_fast<B, NW>(p, S, smem);
+}
+
+bool make_view_tmap(const SrcView& src, int batch, int box_w, int box_h, CUtensorMap* map);
+
+template <int B, int NW>
+static inline cudaError_t launch_hshfl_tma(const HarrisParams& p, int batch, int S, cudaStream_t s) {
+  constexpr int TW = 120 * NW;
+  constexpr int ROWLEN = TW + 16;
+  static_assert(ROWLEN <= 256, "one tensor box per ring row");
+  const size_t smem = (size_t)(HarFastGeom<B>::NSR + 2) * ROWLEN * sizeof(float);  // + 2 mirror rows
+  CUtensorMap mb, mm;
+  if (!make_view_tmap(p.src, batch, ROWLEN, HarFastGeom<B>::RB, &mb) || !make_view_tmap(p.src, batch, ROWLEN, 2, &mm))
+    return cudaErrorNotSupported;
+  auto kern = harris_shfl_tma<B, NW>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grd((p.src.W + TW - 1) / TW, (p.dst.H + S - 1) / S, batch);
+  kern<<<grd, 32 * NW, smem, s>>>(p, S, mb, mm);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int NW>
+cudaError_t dispatch_hshfl_tma(const HarrisParams& p, int batch, int S, cudaStream_t s) {
+  switch (p.block) {
+    case 1: return launch_hshfl_tma<1, NW>(p, batch, S, s);
+    case 2: return launch_hshfl_tma<2, NW>(p, batch, S, s);
+    case 3: return launch_hshfl_tma<3, NW>(p, batch, S, s);
+    case 4: return launch_hshfl_tma<4, NW>(p, batch, S, s);
+    case 5: return launch_hshfl_tma<5, NW>(p, batch, S, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 template <int B, int NW>

@@ -4,4 +4,5 @@
 
 namespace icl {
 template cudaError_t dispatch_hshfl<2>(const HarrisParams& p, int batch, int S, cudaStream_t s);
+template cudaError_t dispatch_hshfl_tma<2>(const HarrisParams& p, int batch, int S, cudaStream_t s);
 }  // namespace icl

@@ -83,7 +83,7 @@ cudaError_t launch_sep_tile(const SepCall& c, bool persistent, cudaStream_t s);
 // harris
 cudaError_t launch_harris_naive(const HarrisCall& c, cudaStream_t s);
 cudaError_t launch_harris_stream(const HarrisCall& c, int nt, int vec, int S, cudaStream_t s);
-cudaError_t launch_harris_shfl(const HarrisCall& c, int nw, int S, cudaStream_t s);
+cudaError_t launch_harris_shfl(const HarrisCall& c, int nw, int S, cudaStream_t s, bool tma = false);
 cudaError_t launch_harris_slide(const HarrisCall& c, int nw, int unr, int S, cudaStream_t s);
 cudaError_t launch_harris_dhat(const HarrisCall& c, float* out, cudaStream_t s);
 // two-filter chain (blur_harris.cu): separable blur (radius <= 3) then Harris (block <= 5) in one pass

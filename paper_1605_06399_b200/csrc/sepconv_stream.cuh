@@ -50,15 +50,6 @@ struct StreamGeom {
   static constexpr int blk(int L) { return ((RB * L * 4 + 127) / 128) * 128 / 4; }
 };
 
-// 3-D TMA tile load (cp.async.bulk.tensor: x = column, y = local row, z = image) into shared
-// memory, completion counted on `bar` (expect_tx armed by the issuing thread).
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-      "[%5];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-      : "memory");
-}
 
 // TMA (round 2, the "tma_*" variants, NT = 32: a 144-column row fits one tensor box): interior
 // CTAs stage each block of RB input rows with ONE cp.async.bulk.tensor issued by thread 0 (a
