@@ -12,7 +12,7 @@ BENCH="python bench.py --steps 2 --warmup 3 --batch $BATCH --no-e2e --no-cpu-bas
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $BENCH > $OUT/launches_bench.log 2>&1
 echo "launch list rc=$?"
 REGEXES=("$@")
-if [ ${#REGEXES[@]} -eq 0 ]; then REGEXES=(nlm_sym sep_stream harris_shfl)  # harris_shfl matches harris_shfl_tma too; fi
+if [ ${#REGEXES[@]} -eq 0 ]; then REGEXES=(nlm_sym sep_stream harris_shfl); fi
 for K in "${REGEXES[@]}"; do
   ncu --set full --clock-control none --import-source on -k regex:$K -s 3 -c 1 -o $OUT/full_$K $BENCH > $OUT/full_$K.log 2>&1
   echo "full $K rc=$?"
