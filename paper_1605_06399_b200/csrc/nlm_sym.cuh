@@ -19,6 +19,12 @@
 //     the strip are partner sources), the vertical patch sum sliding
 //        d(y) = d(y-1) + H(y+P) - H(y-P-1),  H(r) = horizontal patch sum of (u(q)-u(q+o))^2,
 //     in registers for all 2S+1 ox at once, as float2 pairs of adjacent ox (FADD2/FFMA2);
+//     the second offset of a pair is evaluated ONE COLUMN TO THE LEFT ("b lags"): for the pair
+//     (ox, ox+1) lane column k holds (d_(ox)(k), d_(ox+1)(k-1)), so both halves read the same
+//     shifted sample u(k + ox + t) (a broadcast operand) and the same u(q + o) = u(k + ox), and
+//     send their partner contributions to the same column k + ox; only the shared centre window
+//     is read as the pair (c(t), c(t-1)).  No per-pair register-pair assembly (MOV) is left;
+//     the own sums of column k then collect half a of k and half b of k+1 (one shuffle for k=3);
 //     H_old is recomputed from the image rows, not stored (no ring);
 //   * own contributions accumulate in registers per row; partner contributions accumulate in a
 //     (4+2S)-column register window which the lanes exchange by warp shuffles (columns that
@@ -125,11 +131,14 @@ __host__ __device__ constexpr bool sym_first_pn(int g, int k) {
 }
 
 // the two lanes' differences u(q) - u(q+o) at window index t of the pair g
+// (half a at window index t of column k, half b at index t - 1 of column k - 1: "b lags")
 template <int P, int S, int OY, int G_>
 __device__ __forceinline__ float2 sym_df(const float* c18, const float* s18, int t) {
   using Q = SymPass<P, S, OY>;
-  if (Q::mixed(G_)) return s2_sub(make_float2(c18[t + S], c18[t + S]), make_float2(s18[t + 2 * S], c18[t + OY + S]));
-  return s2_sub(make_float2(c18[t + S], c18[t + S]), make_float2(s18[t + Q::oxa(G_) + S], s18[t + Q::oxa(G_) + S + 1]));
+  if (Q::mixed(G_))
+    return make_float2(__fsub_rn(c18[t + S], s18[t + 2 * S]), __fsub_rn(c18[t + S - 1], c18[t + OY + S - 1]));
+  const float sj = s18[t + Q::oxa(G_) + S];
+  return s2_sub(make_float2(c18[t + S], c18[t + S - 1]), make_float2(sj, sj));
 }
 
 template <int P, int S, int OY, int G_>
@@ -187,19 +196,20 @@ __device__ __forceinline__ void sym_H_all(float (&Hr)[S + 1][8], const float* c1
 // FFMA2 links.
 template <int P, int S, int OY, int G_ = 0>
 __device__ __forceinline__ void sym_slide_pq(float2 (&D)[S + 1][4], const float* Cd, const float* Cs,
-                                             const float* Sd, const float* Ss) {
+                                             const float* Sd, const float* Ss, const float2* CdL,
+                                             const float2* CsL) {
   using Q = SymPass<P, S, OY>;
   constexpr int C = 4, NCW = C + 2 * P;
   float2 pp[NCW], qq[NCW];
 #pragma unroll
   for (int t = 0; t < NCW; ++t) {
-    if (Q::mixed(G_)) {
-      pp[t] = s2_sub(make_float2(Cd[t + S], Cd[t + S]), make_float2(Sd[t + 2 * S], Cd[t + OY + S]));
-      qq[t] = s2_sub(make_float2(Cs[t + S], Cs[t + S]), make_float2(Ss[t + 2 * S], Cs[t + OY + S]));
-    } else {
+    if (Q::mixed(G_)) {  // halves from two windows: scalar (b lags: column k - 1)
+      pp[t] = make_float2(__fsub_rn(Cd[t + S], Sd[t + 2 * S]), __fsub_rn(Cd[t + S - 1], Cd[t + OY + S - 1]));
+      qq[t] = make_float2(__fsub_rn(Cs[t + S], Ss[t + 2 * S]), __fsub_rn(Cs[t + S - 1], Cs[t + OY + S - 1]));
+    } else {  // (Cd[t+S], Cd[t+S-1]) - Sd[j] broadcast
       const int j = t + Q::oxa(G_) + S;
-      pp[t] = s2_sub(make_float2(Cd[t + S], Cd[t + S]), make_float2(Sd[j], Sd[j + 1]));
-      qq[t] = s2_sub(make_float2(Cs[t + S], Cs[t + S]), make_float2(Ss[j], Ss[j + 1]));
+      pp[t] = s2_sub(CdL[t], make_float2(Sd[j], Sd[j]));
+      qq[t] = s2_sub(CsL[t], make_float2(Ss[j], Ss[j]));
     }
   }
   float2 a = s2_mul(pp[0], qq[0]);
@@ -212,7 +222,7 @@ __device__ __forceinline__ void sym_slide_pq(float2 (&D)[S + 1][4], const float*
     a = s2_fma(make_float2(-pp[k - 1].x, -pp[k - 1].y), qq[k - 1], a);
     D[G_][k] = s2_add(D[G_][k], a);
   }
-  if constexpr (G_ < S) sym_slide_pq<P, S, OY, G_ + 1>(D, Cd, Cs, Sd, Ss);
+  if constexpr (G_ < S) sym_slide_pq<P, S, OY, G_ + 1>(D, Cd, Cs, Sd, Ss, CdL, CsL);
 }
 
 template <int P, int S, int OY>
@@ -229,7 +239,22 @@ __device__ __forceinline__ void sym_slide_H(float2 (&D)[S + 1][4], const float* 
     Cd[j] = cd.x; Cd[j + 1] = cd.y; Cs[j] = cs.x; Cs[j + 1] = cs.y;
     Sd[j] = sd.x; Sd[j + 1] = sd.y; Ss[j] = ss.x; Ss[j + 1] = ss.y;
   }
-  sym_slide_pq<P, S, OY>(D, Cd, Cs, Sd, Ss);
+  // the lagged centre pairs (C[t+S], C[t+S-1]), formed once per step and shared by every pair:
+  // an aligned FADD2 result read swapped where t + S is odd, two scalar operations otherwise
+  constexpr int NCW = 4 + 2 * P;
+  float2 CdL[NCW], CsL[NCW];
+#pragma unroll
+  for (int t = 0; t < NCW; ++t) {
+    const int m = t + S;
+    if (m & 1) {
+      CdL[t] = make_float2(Cd[m], Cd[m - 1]);
+      CsL[t] = make_float2(Cs[m], Cs[m - 1]);
+    } else {
+      CdL[t] = make_float2(__fsub_rn(cn[m], co[m]), __fsub_rn(cn[m - 1], co[m - 1]));
+      CsL[t] = make_float2(__fadd_rn(cn[m], co[m]), __fadd_rn(cn[m - 1], co[m - 1]));
+    }
+  }
+  sym_slide_pq<P, S, OY>(D, Cd, Cs, Sd, Ss, CdL, CsL);
 }
 
 // One search row OY of the warp's walk (with the mixed pair's row-0 offset).  U: smem tile;
@@ -325,11 +350,12 @@ __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, ui
         // sliding sums can round below 0; a negative d with a tiny h would give w = inf (R29)
         const float2 t = s2_mul(make_float2(fmaxf(D[g][k].x, 0.0f), fmaxf(D[g][k].y, 0.0f)), nc);
         const float2 w = make_float2(ex2_approx(t.x), ex2_approx(t.y));
-        const float uq = iy[k + S];
+        const float uq = iy[k + S], uqb = iy[k + S - 1];  // u(q) of half a (column k), half b (k - 1)
         const bool first = g == 0;  // first write of A[k], B[k] (resolved at compile time)
         B[k] = first ? w : s2_add(B[k], w);
         if (Q::mixed(g)) {
-          A[k] = s2_fma(w, make_float2(ia[k + 2 * S], iy[k + OY + S]), A[k]);
+          A[k].x = fmaf(w.x, ia[k + 2 * S], A[k].x);
+          A[k].y = fmaf(w.y, iy[k + OY + S - 1], A[k].y);
           if (k < 2) {  // entries 2S, 2S + 1 were written by the last normal pair
             Pn[k + 2 * S].x = fmaf(w.x, uq, Pn[k + 2 * S].x);  // partner (q + (S, OY)): row y + OY
             Pd[k + 2 * S].x += w.x;
@@ -337,36 +363,36 @@ __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, ui
             Pn[k + 2 * S].x = w.x * uq;
             Pd[k + 2 * S].x = w.x;
           }
-          Zn[k] = w.y * uq;  // partner (q + (OY, 0)): row y
+          Zn[k] = w.y * uqb;  // partner (q + (OY, 0)) of source column k - 1: row y, column k - 1 + OY
           Zd[k] = w.y;
         } else {
-          const int ja = k + Q::oxa(g) + S;  // window index of column k + oxa
-          const float2 qa = make_float2(ia[ja], ia[ja + 1]);
+          const int ja = k + Q::oxa(g) + S;  // window index of column k + oxa (both halves)
+          const float2 qa = make_float2(ia[ja], ia[ja]);
           A[k] = first ? s2_mul(w, qa) : s2_fma(w, qa, A[k]);
           if (sym_first_pn(g, k)) {
-            Pn[ja] = s2_mul(w, make_float2(uq, uq));  // .x -> column ja, .y -> ja + 1
+            Pn[ja] = s2_mul(w, make_float2(uq, uqb));  // both halves -> column ja
             Pd[ja] = w;
           } else {
-            Pn[ja] = s2_fma(w, make_float2(uq, uq), Pn[ja]);
+            Pn[ja] = s2_fma(w, make_float2(uq, uqb), Pn[ja]);
             Pd[ja] = s2_add(Pd[ja], w);
           }
         }
       }
-    // partner window of row y + OY: column J collects Pn[J].x and Pn[J-1].y; columns outside
+    // partner window of row y + OY: column J collects Pn[J].x and Pn[J].y; columns outside
     // [S, S+C) belong to the lanes 1..2 to the left / right
     float on[NIW], od[NIW];
 #pragma unroll
     for (int j = 0; j < NIW; ++j) {
-      on[j] = j > 0 ? Pn[j].x + Pn[j - 1].y : Pn[j].x;
-      od[j] = j > 0 ? Pd[j].x + Pd[j - 1].y : Pd[j].x;
+      on[j] = Pn[j].x + Pn[j].y;
+      od[j] = Pd[j].x + Pd[j].y;
     }
     float rn[C], rd[C], zn[C], zd[C];
 #pragma unroll
     for (int k = 0; k < C; ++k) {
       rn[k] = on[k + S];
       rd[k] = od[k + S];
-      zn[k] = k >= OY ? Zn[k - OY] : 0.0f;
-      zd[k] = k >= OY ? Zd[k - OY] : 0.0f;
+      zn[k] = k + 1 >= OY ? Zn[k + 1 - OY] : 0.0f;  // source column k + 1 - OY - 1
+      zd[k] = k + 1 >= OY ? Zd[k + 1 - OY] : 0.0f;
     }
 #pragma unroll
     for (int dl = 1; dl <= 2; ++dl)
@@ -382,10 +408,10 @@ __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, ui
           rn[k] += __shfl_down_sync(0xffffffffu, on[k - 4 * dl + S], dl);
           rd[k] += __shfl_down_sync(0xffffffffu, od[k - 4 * dl + S], dl);
         }
-        // row-0 partner: source column k + 4 dl - OY of lane - dl
-        if (k + 4 * dl - OY >= 0 && k + 4 * dl - OY < C) {
-          zn[k] += __shfl_up_sync(0xffffffffu, Zn[k + 4 * dl - OY], dl);
-          zd[k] += __shfl_up_sync(0xffffffffu, Zd[k + 4 * dl - OY], dl);
+        // row-0 partner: entry k + 4 dl + 1 - OY of lane - dl (its source column one less)
+        if (k + 4 * dl + 1 - OY >= 0 && k + 4 * dl + 1 - OY < C) {
+          zn[k] += __shfl_up_sync(0xffffffffu, Zn[k + 4 * dl + 1 - OY], dl);
+          zd[k] += __shfl_up_sync(0xffffffffu, Zd[k + 4 * dl + 1 - OY], dl);
         }
       }
     // TMEM read-modify-write: own row y (own pairs + the row-0 partners), partner row y + OY
@@ -398,11 +424,14 @@ __device__ __forceinline__ void sym_pass(const float* U, int wrow0, int lane, ui
     tm_wait_ld();
     if (own_ok) tm_pin8(vo);
     if (par_ok) tm_pin8(vp);
+    // own sums: column k = half a of k + half b of k + 1 (k = 3: lane + 1's column 0; lane 31's
+    // column 3 and lane 0's column -1 are halo columns, never output)
+    const float an = __shfl_down_sync(0xffffffffu, A[0].y, 1), bd = __shfl_down_sync(0xffffffffu, B[0].y, 1);
     if (own_ok) {
 #pragma unroll
       for (int k = 0; k < C; ++k) {
-        vo[k] += (A[k].x + A[k].y) + zn[k];
-        vo[4 + k] += (B[k].x + B[k].y) + zd[k];
+        vo[k] += (A[k].x + (k + 1 < C ? A[k + 1].y : an)) + zn[k];
+        vo[4 + k] += (B[k].x + (k + 1 < C ? B[k + 1].y : bd)) + zd[k];
       }
       tm_st8(tm + 8 * y, vo);
     }
