@@ -494,7 +494,7 @@ def run_suite(args):
     roof["nlm"]["limiter"] = {
         "sym_tmem": "FP32 pipe: the H slide recomputes the row leaving the window (no register/TMEM room for a "
                     "ring); FFMA2s with three distinct register pairs issue at 2/3 rate; 8 warps/SM (TMEM: 256 "
-                    "columns x 2 CTAs; 222 registers), DESIGN.md §5",
+                    "columns x 2 CTAs; 236 registers), DESIGN.md §5",
         "sym_ring": "FFMA2 chain latency at 4 warps/SM (the TMEM ring takes all 512 columns), DESIGN.md §5",
     }.get(variants["nlm"], "shared-memory wavefronts (two-phase separable box sums: H round trip + accumulation "
                            "loads, DESIGN.md §5)")
