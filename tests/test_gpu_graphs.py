@@ -49,3 +49,49 @@ def test_capture_and_replay_all_filters():
     torch.cuda.synchronize()
     for got, want in zip(outs + [mask], ref):
         np.testing.assert_array_equal(got.cpu().numpy(), want.cpu().numpy())
+
+
+@pytest.mark.parametrize("variant", ["pm_w32x8_c1x1_blk_l1_u4", "pm_w16x8_c2x1_iwg_l1_u4"])
+def test_dependent_chain_with_programmatic_launch(variant):
+    """The small-image sepconv kernels are launched with programmatic dependent launch (the next grid
+    may start before the previous one ends; it waits in griddepcontrol.wait before touching memory).
+    A chain in which every call reads the previous call's output -- and writes the buffer the call
+    before it read -- must equal the same chain with a host synchronisation after every call, eagerly
+    and replayed as a CUDA graph, bit for bit."""
+    icl.force_variant("sepconv", variant)
+    try:
+        a = torch.from_numpy(synth.uniform_image(11, 512, 512)).to(DEV)
+        fx = synth.gaussian_taps(2)
+        bufs = [a.clone(), torch.empty_like(a), torch.empty_like(a)]
+        order = [(0, 1), (1, 2), (2, 0), (0, 1), (1, 2), (2, 0), (0, 1)]  # ping-pong through 3 buffers
+
+        def chain(st, sync):
+            for i, j in order:
+                icl.sepconv(bufs[i], bufs[j], fx, fx, "constant", stream=st)
+                if sync:
+                    st.synchronize()
+
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            chain(s, True)
+        s.synchronize()
+        ref = bufs[1].clone()
+        bufs[0].copy_(a)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s):
+            chain(s, False)
+        s.synchronize()
+        assert torch.equal(bufs[1], ref)
+        g = torch.cuda.CUDAGraph()
+        bufs[0].copy_(a)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            chain(s, False)
+        bufs[0].copy_(a)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(bufs[1], ref)
+        assert icl.variant_names("sepconv")[icl.last_variant("sepconv")] == variant
+    finally:
+        icl.force_variant("sepconv", None)
